@@ -1,0 +1,142 @@
+/*
+ * abft_b200.h — C-ABI of the B200-native ABFT-protected linear-layer path.
+ *
+ * The reference (abft_guard 0.1.0, pure Python) has no FFI; these entry points
+ * are what its hot-path functions become when the arithmetic moves to sm_100a.
+ * Each declaration cites the reference interface it replaces.  Plain pointers
+ * and sizes only; every data pointer is a DEVICE pointer owned by the caller;
+ * the library allocates nothing on the hot path.  All calls are asynchronous
+ * on `stream` (a cudaStream_t passed as void*); results are valid after the
+ * stream synchronises — the reference's deferred verification
+ * (checksum.py:207-211, :237).
+ *
+ * Return codes map onto the reference exceptions (errors.py:4-28):
+ *   ABFT_OK 0, ABFT_E_SHAPE 1 -> ShapeMismatchError, ABFT_E_VALUE 2 -> ValueError,
+ *   ABFT_E_OVERFLOW 3 -> ExactOverflowError, ABFT_E_CUDA 4 (launch/driver error),
+ *   ABFT_E_UNSUPPORTED 5 (a configuration the tensor-core path does not cover).
+ * The message of the last failure on the calling thread: abft_last_error().
+ */
+#ifndef ABFT_B200_H
+#define ABFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ABFT_OK = 0, ABFT_E_SHAPE = 1, ABFT_E_VALUE = 2, ABFT_E_OVERFLOW = 3, ABFT_E_CUDA = 4,
+       ABFT_E_UNSUPPORTED = 5 };
+
+/* storage element type of A / B (shapes.py:22-57: binary16 storage) */
+enum { ABFT_F16 = 0, ABFT_BF16 = 1 };
+/* output element type */
+enum { ABFT_OUT_F32 = 0, ABFT_OUT_F16 = 1, ABFT_OUT_BF16 = 2, ABFT_OUT_NONE = 3 };
+/* comparison rule (checksum.py:143-148): tau = r*K*max(|lhs|,|rhs|,1) with
+ * r = 0 (exact-int), 2^-10 (binary16), 2^-23 (binary32), 2^-7 (bf16, B200 extension) */
+enum { ABFT_NUM_EXACT = 0, ABFT_NUM_BINARY16 = 1, ABFT_NUM_BINARY32 = 2, ABFT_NUM_BF16 = 3 };
+/* tiled.py:42-48 (Scheme) — same order as the reference enum */
+enum { ABFT_UNPROTECTED = 0, ABFT_GLOBAL = 1, ABFT_ONE_SIDED = 2, ABFT_TWO_SIDED = 3,
+       ABFT_REPL_FULL = 4, ABFT_REPL_SINGLE = 5 };
+
+/* OutputFault / ThreadMmaFault after _fault_cell (tiled.py:92-121, :386-397) */
+typedef struct { int32_t row, col; float delta; } abft_fault_t;
+
+/* Verdict (checksum.py:35-43) */
+typedef struct { double lhs, rhs, tol; int32_t detected, k; } abft_verdict_t;
+
+/* ThreadVerdict (tiled.py:149-157) */
+typedef struct { int32_t t_row, t_col, detected, pad; double max_abs_diff, tol; } abft_thread_verdict_t;
+
+/*
+ * One protected GEMM C = A * B (tiled.py:400-503 execute; checksum.py:130 accumulate_matmul).
+ *   A  [M x K]  row-major (K-major), element `dtype`, leading dim lda (elements, %8 == 0)
+ *   Bt [N x K]  row-major = B^T (K-major weights, as prepared by abft_pack), ldbt %8 == 0
+ *   C  [M x N]  row-major, `out_dtype`; ReLU applied before the store when relu != 0
+ * Faults add delta to the fp32 accumulator before any checksum, ReLU or store
+ * (tiled.py:197-200; checksum.py:232-233).  Thread-level verdicts cover the
+ * tiling-padded extents m_ext x n_ext (tiled.py:423-431); tol_k is the K the
+ * thread-level tolerance uses (k_step-padded K, tiled.py:242).
+ * Global scheme: out_sum[0] += sum of the fp32 outputs (output_summation,
+ * checksum.py:120-127) — verification is deferred to abft_verify.
+ * next_colck (optional, [N]) += column sums of the STORED, ReLU'd, rounded
+ * outputs: the next layer's activation checksum fused into this epilogue
+ * (checksum.py:229 + :235).
+ */
+typedef struct {
+  const void* A;  int64_t lda;
+  const void* Bt; int64_t ldbt;
+  void* C;        int64_t ldc;
+  int32_t M, N, K;
+  int32_t m_ext, n_ext, tol_k;
+  int32_t dtype, out_dtype, numeric, scheme;
+  int32_t thread_m, thread_n;
+  int32_t relu;
+  int32_t ck_split;                     /* 1: checksum columns as hi+lo pairs (near-fp32), 0: single */
+  const abft_fault_t* faults; int32_t nfaults;
+  double* out_sum;                      /* global: [1] accumulated output summation */
+  float* next_colck;                    /* optional [N] */
+  abft_thread_verdict_t* verdicts;      /* optional [(m_ext/thread_m) x (n_ext/thread_n)] row-major */
+  int32_t* fired_count;                 /* optional: number of thread tiles whose check fired */
+  int32_t* fired;                       /* optional [fired_cap x 2] (t_row, t_col) of fired tiles */
+  int32_t fired_cap;
+  int32_t tile_n;                       /* CTA N tile: 0 = auto, else 64/128/256 */
+  int32_t num_sms;                      /* persistent grid size cap: 0 = all SMs */
+} abft_gemm_args_t;
+
+int abft_gemm(const abft_gemm_args_t* args, void* stream);
+
+/*
+ * Column sums of a row-major [rows x cols] matrix into out[cols] (fp32).
+ *   column_checksum(A)  (checksum.py:90-96):  X = A,   rows = M, cols = K
+ *   row_checksum(B)     (checksum.py:99-105):  X = B^T, rows = N, cols = K
+ *   offline_weight_checksum (checksum.py:175-187) = the latter, once per weight.
+ * accumulate != 0 adds into out (for batch shards / K4a+K4b mixes).
+ */
+int abft_colsum(const void* X, int32_t rows, int32_t cols, int64_t ldx, int32_t dtype,
+                float* out, int32_t accumulate, void* stream);
+
+/*
+ * Layout/padding pack (the zero-padded copies of tiled.py:428-431 and the
+ * K-major weight layout the tensor-core path consumes):
+ *   transpose == 0: dst[r][c] = src[r][c] for r<rows, c<cols; zero for c in [cols, dst_cols)
+ *   transpose != 0: dst[c][r] = src[r][c]  (dst is [cols x dst_cols], zero for r in [rows, dst_cols))
+ * Element size is 2 bytes (fp16/bf16).
+ */
+int abft_pack(const void* src, int32_t rows, int32_t cols, int64_t lds,
+              void* dst, int32_t dst_cols, int64_t ldd, int32_t transpose, void* stream);
+
+/* Element-type conversion helpers for host adapters: int64 (exact-int mode,
+ * values must be exactly representable) or fp32 -> fp16/bf16 storage. */
+int abft_convert_i64(const int64_t* src, int64_t n, int32_t dtype, void* dst, void* stream);
+
+/* Sum of all entries of a row-major matrix (output_summation, checksum.py:120-127):
+ * *out += sum in fp64; elem 0 = fp16, 1 = bf16, 2 = fp32. */
+int abft_matrix_sum(const void* X, int32_t rows, int32_t cols, int64_t ldx, int32_t elem, double* out,
+                    void* stream);
+
+/*
+ * Batched global-ABFT verification (checksum.py:108-117 checksum_dot, :151-169):
+ * for layer i, lhs_i = dot(colck_i, rowck_i) over k_i terms (fp64), rhs_i =
+ * *rhs_i, tau = r*k_i*max(|lhs|,|rhs|,1), detected = |lhs-rhs| > tau.
+ * `sums` receives [lhs_i, rhs_i] (so multi-GPU callers can all-reduce partials
+ * and call abft_verify_sums); `out` receives one Verdict per layer;
+ * `detected_count` (optional) += number of flagged layers.
+ */
+typedef struct { const float* colck; const float* rowck; const double* rhs; int32_t k, pad; } abft_global_task_t;
+
+int abft_global_lhs(const abft_global_task_t* tasks /*device*/, int32_t ntasks, double* sums /*[n][2]*/,
+                    void* stream);
+int abft_verify_sums(const double* sums /*[n][2]*/, const int32_t* k /*device [n]*/, int32_t ntasks,
+                     int32_t numeric, abft_verdict_t* out, int32_t* detected_count, void* stream);
+
+/* Library introspection */
+const char* abft_last_error(void);
+int abft_version(void);                 /* 10000*major + 100*minor + patch */
+int abft_device_sms(void);              /* SM count of the current device (0 if none) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABFT_B200_H */

@@ -1,0 +1,187 @@
+"""Parity of the sm_100a path against the reference's golden vectors and the oracle.
+
+Bar: exact-int mode is bit-exact (outputs, verdict values, flags); binary16
+outputs agree with the fp32-accumulate reference within GEMM_ATOL (summation
+order only) and fault flags agree exactly for faults outside [0.5 tau, 2 tau].
+"""
+
+import numpy as np
+import pytest
+
+from oracle import abft_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GEMM_RTOL = 2e-5      # fp32-accumulate reordering, relative to sum |a_ik b_kj|
+VERDICT_RTOL = 1e-2   # tau values: same formula on lhs/rhs that differ by rounding
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2104_09455_b200 as pkg
+    from paper_2104_09455_b200 import device
+    device.require_device()
+    return pkg
+
+
+def _tiling(P, meta):
+    f = meta["tiling_fields"]
+    return P.TilingConfig(**f)
+
+
+def _faults(P, meta):
+    out = []
+    for f in meta["faults"]:
+        if f[0] == "output":
+            out.append(P.OutputFault(row=f[1], col=f[2], delta=f[3]))
+        else:
+            out.append(P.ThreadMmaFault(thread_row=f[1], thread_col=f[2], step=f[3], local_index=f[4], delta=f[5]))
+    return out
+
+
+def _abs_bound(a, b):
+    return np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64))
+
+
+def test_execute_golden_cases(P, execute_cases):
+    failures = []
+    for meta, arr in execute_cases:
+        dtype = P.BINARY16 if meta["dtype"] == "binary16" else None
+        scheme = P.Scheme(meta["scheme"])
+        rep = P.execute(arr["a"], arr["b"], _tiling(P, meta), scheme, _faults(P, meta), dtype)
+        name = meta["name"]
+        exact = np.issubdtype(arr["a"].dtype, np.integer)
+        if exact:
+            if not np.array_equal(rep.output, arr["out"]):
+                failures.append(f"{name}: output mismatch")
+        else:
+            bound = _abs_bound(arr["a"], arr["b"])
+            err = np.abs(rep.output.astype(np.float64) - arr["out"])
+            if not (err <= GEMM_RTOL * bound + 1e-6).all():
+                failures.append(f"{name}: output err {err.max()}")
+        if rep.detected != meta["detected"]:
+            failures.append(f"{name}: detected {rep.detected} vs {meta['detected']}")
+        if scheme is P.Scheme.GLOBAL_ABFT:
+            v = rep.verdicts[0]
+            det, lhs, rhs, tol = meta["global"]
+            if v.detected != det:
+                failures.append(f"{name}: global flag")
+            if exact and (v.lhs, v.rhs, v.tolerance_used) != (lhs, rhs, tol):
+                failures.append(f"{name}: global values {(v.lhs, v.rhs)} vs {(lhs, rhs)}")
+            if not exact and abs(v.tolerance_used - tol) > VERDICT_RTOL * tol:
+                failures.append(f"{name}: global tol {v.tolerance_used} vs {tol}")
+        elif scheme is not P.Scheme.UNPROTECTED:
+            tv = arr["tv"]
+            if len(rep.verdicts) != len(tv):
+                failures.append(f"{name}: {len(rep.verdicts)} verdicts vs {len(tv)}")
+                continue
+            for v, ref in zip(rep.verdicts, tv):
+                if (v.thread_row, v.thread_col, v.detected) != (int(ref[0]), int(ref[1]), bool(ref[2])):
+                    failures.append(f"{name}: verdict {(v.thread_row, v.thread_col, v.detected)} vs {ref[:3]}")
+                    break
+                if exact and (v.max_abs_diff, v.tolerance_used) != (ref[3], ref[4]):
+                    failures.append(f"{name}: verdict values {(v.max_abs_diff, v.tolerance_used)} vs {ref[3:]}")
+                    break
+                if not exact and v.detected and abs(v.max_abs_diff - ref[3]) > VERDICT_RTOL * max(ref[3], 1):
+                    failures.append(f"{name}: fired diff {v.max_abs_diff} vs {ref[3]}")
+                    break
+        op = rep.op_counts
+        if [op.base_mma_count, op.redundant_mma_count, op.checksum_op_count] != meta["op_counts"]:
+            failures.append(f"{name}: op counts")
+    assert not failures, "\n".join(failures[:40])
+
+
+def test_pipeline_golden_cases(P, pipeline_cases):
+    from paper_2104_09455_b200.errors import ExactOverflowError
+    ran = 0
+    for meta, arr in pipeline_cases:
+        ws = [arr[f"w{j}"] for j in range(len(meta["verdicts"]))]
+        faults = {int(k): [tuple(x) for x in v] for k, v in meta["faults"].items()}
+        P.checksum.clear_weight_checksum_cache()
+        try:
+            vs = P.run_protected_pipeline(arr["a0"], ws, dtype=None if meta["exact"] else P.BINARY16, faults=faults)
+        except ExactOverflowError:
+            assert meta["exact"]
+            continue
+        ran += 1
+        for v, (det, lhs, rhs, tol) in zip(vs, meta["verdicts"]):
+            assert v.detected == det, meta["name"]
+            if meta["exact"]:
+                assert (v.lhs, v.rhs) == (lhs, rhs), meta["name"]
+            else:
+                assert abs(v.tolerance_used - tol) <= VERDICT_RTOL * tol, meta["name"]
+                assert abs(v.lhs - lhs) <= 1e-3 * tol and abs(v.rhs - rhs) <= 1e-3 * tol, meta["name"]
+    assert ran >= 16
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 256, 256), (1, 512, 13), (2048, 512, 512), (300, 200, 1000),
+                                   (4096, 4096, 4096)])
+def test_unprotected_gemm_matches_torch(P, m, n, k):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = (torch.rand((m, k), generator=g, device="cuda") * 2 - 1).half()
+    b = (torch.rand((k, n), generator=g, device="cuda") * 2 - 1).half()
+    rep = P.execute(a, b)
+    ref = a.float() @ b.float()
+    bound = a.float().abs() @ b.float().abs()
+    assert ((rep.output - ref).abs() <= GEMM_RTOL * bound + 1e-6).all()
+
+
+@pytest.mark.parametrize("scheme", ["thread-one-sided", "thread-two-sided", "global-abft"])
+@pytest.mark.parametrize("m,n,k", [(2048, 512, 512), (4096, 1024, 2304)])
+def test_no_false_positives_and_detection_at_scale(P, scheme, m, n, k):
+    import torch
+    sch = P.Scheme(scheme)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = (torch.rand((m, k), generator=g, device="cuda") - 0.5).half()
+    b = (torch.rand((k, n), generator=g, device="cuda") - 0.5).half()
+    tiling = P.TilingConfig()
+    clean = P.execute(a, b, tiling, sch)
+    assert clean.detected is False
+    # tau of the responsible check, then a fault 20x above it
+    if sch is P.Scheme.GLOBAL_ABFT:
+        tau = clean.verdicts[0].tolerance_used
+    else:
+        tau = max(v.tolerance_used for v in clean.verdicts)
+    faulty = P.execute(a, b, tiling, sch, [P.OutputFault(row=m // 2 + 3, col=n // 3 + 1, delta=20 * tau + 1)])
+    assert faulty.detected is True
+    if sch is not P.Scheme.GLOBAL_ABFT:
+        fired = [(v.thread_row, v.thread_col) for v in faulty.verdicts if v.detected]
+        assert fired == [((m // 2 + 3) // 16, (n // 3 + 1) // 8)]
+    diff = (faulty.output - clean.output)
+    assert float(diff[m // 2 + 3, n // 3 + 1]) == pytest.approx(20 * tau + 1, rel=1e-6)
+
+
+def test_bf16_path(P):
+    import torch
+    a = (torch.rand((512, 384), device="cuda") - 0.5).bfloat16()
+    b = (torch.rand((384, 256), device="cuda") - 0.5).bfloat16()
+    rep = P.execute(a, b, P.TilingConfig(), P.Scheme.THREAD_ONE_SIDED)
+    ref = a.float() @ b.float()
+    bound = a.float().abs() @ b.float().abs()
+    assert ((rep.output - ref).abs() <= GEMM_RTOL * bound + 1e-6).all()
+    assert rep.detected is False
+
+
+def test_checksum_helpers_match_oracle(P):
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, size=(300, 72)).astype(np.float16)
+    b = rng.uniform(-1, 1, size=(72, 40)).astype(np.float16)
+    assert np.allclose(P.column_checksum(a), O.colck(a), rtol=1e-5, atol=1e-4)
+    assert np.allclose(P.row_checksum(b), O.rowck(b), rtol=1e-5, atol=1e-4)
+    ai = rng.integers(-8, 9, size=(50, 30), dtype=np.int64)
+    assert P.column_checksum(ai).tolist() == O.colck(ai).tolist()
+    assert P.checksum_dot(np.array([4, 6]), np.array([3, 7])) == 54
+    c = O.matmul(ai, ai.T[:, :20].copy() if False else rng.integers(-8, 9, size=(30, 20), dtype=np.int64))
+    assert P.output_summation(c) == O.total(c)
+    v = P.global_abft_check(np.array([[1, 2], [3, 4]]), np.array([[5, 6], [7, 8]]), np.array([[19, 22], [43, 50]]))
+    assert v.detected is False and v.lhs == 134 and v.rhs == 134
+
+
+def test_shape_errors_map_to_reference_exceptions(P):
+    from paper_2104_09455_b200.errors import ShapeMismatchError
+    with pytest.raises(ShapeMismatchError):
+        P.execute(np.ones((4, 5), dtype=np.int64), np.ones((4, 5), dtype=np.int64))
+    with pytest.raises(ValueError):
+        P.execute(np.ones((16, 16), dtype=np.int64), np.ones((16, 16), dtype=np.int64), P.TilingConfig(),
+                  P.Scheme.GLOBAL_ABFT, [P.OutputFault(row=16, col=0, delta=1)])
