@@ -81,11 +81,27 @@ typedef struct {
   int32_t* fired_count;                 /* optional: number of thread tiles whose check fired */
   int32_t* fired;                       /* optional [fired_cap x 2] (t_row, t_col) of fired tiles */
   int32_t fired_cap;
-  int32_t tile_n;                       /* CTA N tile: 0 = auto, else 64/128/256 */
+  int32_t tile_n;                       /* CTA N tile: 0 = auto, else 32/64/128/192/256 */
   int32_t num_sms;                      /* persistent grid size cap: 0 = all SMs */
+  /* optional checksum rows prepared offline by abft_ck_rows for THIS call's plan; when null the
+   * checksum warps generate them on chip from each B^T tile (one-sided / two-sided only) */
+  const void* ck_rows; int64_t ldck; int32_t ck_rows_n;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
+
+/* The kernel configuration abft_gemm would use for `args` (no launch):
+ * out[0] tile_n, [1] bn_eff, [2] checksum groups per tile, [3] nck_pad, [4] pipeline stages,
+ * [5] 1 if offline checksum rows are recommended (B tiles re-read by > 2 M-blocks),
+ * [6] number of N blocks, [7] persistent grid size. */
+int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[8]*/);
+
+/* Offline checksum rows for a plan: out [(n_blocks*nck_pad) x ldo] (n_blocks = plan out[6], rows of
+ * blocks past N are zero), row nb*nck_pad + j holds
+ * the fp16/bf16 hi (j < G) / lo (G <= j < 2G, split) part of sum_{r<nt} Bt[nb*bn_eff + j*nt + r][:]
+ * (the weight-tile checksum of tiled.py:240, prepared once per weight like checksum.py:175). */
+int abft_ck_rows(const void* Bt, int32_t N, int32_t K, int64_t ldbt, int32_t dtype, int32_t bn_eff, int32_t nt,
+                 int32_t split, int32_t nck_pad, int32_t n_blocks, void* out, int64_t ldo, void* stream);
 
 /*
  * Column sums of a row-major [rows x cols] matrix into out[cols] (fp32).

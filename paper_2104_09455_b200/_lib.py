@@ -25,6 +25,8 @@ UNPROTECTED, GLOBAL, ONE_SIDED, TWO_SIDED, REPL_FULL, REPL_SINGLE = range(6)
 
 EXPORTED_SYMBOLS = (
     "abft_gemm",
+    "abft_gemm_plan",
+    "abft_ck_rows",
     "abft_colsum",
     "abft_pack",
     "abft_convert_i64",
@@ -79,6 +81,7 @@ class GemmArgs(ctypes.Structure):
         ("fired_cap", ctypes.c_int32),
         ("tile_n", ctypes.c_int32),
         ("num_sms", ctypes.c_int32),
+        ("ck_rows", ctypes.c_void_p), ("ldck", ctypes.c_int64), ("ck_rows_n", ctypes.c_int32),
     ]
 
 
@@ -94,6 +97,8 @@ _lib = None
 def _declare(lib):
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.abft_gemm.argtypes = [ctypes.POINTER(GemmArgs), vp]
+    lib.abft_gemm_plan.argtypes = [ctypes.POINTER(GemmArgs), vp]
+    lib.abft_ck_rows.argtypes = [vp, i32, i32, i64, i32, i32, i32, i32, i32, i32, vp, i64, vp]
     lib.abft_colsum.argtypes = [vp, i32, i32, i64, i32, vp, i32, vp]
     lib.abft_pack.argtypes = [vp, i32, i32, i64, vp, i32, i64, i32, vp]
     lib.abft_convert_i64.argtypes = [vp, i64, i32, vp, vp]

@@ -3,19 +3,24 @@
 // One persistent, warp-specialised tcgen05 GEMM whose epilogue carries every ABFT
 // scheme of the reference (tiled.py:400-503):
 //
-//   warp 0      TMA producer: A [128 x 64] and B^T [BN x 64] tiles (SW128) -> smem ring
+//   warp 0      TMA producer: A [128 x 64], B^T [BN x 64] (and, when prepared offline,
+//               the checksum rows [nck x 64]) tiles, SW128 -> smem ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5   epilogue: TMEM -> registers; fault injection; thread-level checks;
 //               output summation (global); ReLU / rounding / store; fused next-layer
 //               activation checksum
-//   warps 6-9   checksum generator (thread-level schemes only): per k-block it sums
-//               each group of Nt rows of the B^T tile on CUDA cores and writes the
-//               group-checksum rows into the smem ring, so one extra tcgen05.mma
-//               N-slice computes At * rowck(Bt) for every (row, column-group) pair
-//               (tiled.py:221-242) — no extra HBM traffic.
+//   warps 6-9   checksum generator (thread-level schemes, on-chip mode): per k-block it
+//               sums each group of Nt rows of the B^T tile on CUDA cores and writes the
+//               group-checksum rows into the smem ring, so one extra tcgen05.mma N-slice
+//               computes At * rowck(Bt) for every (row, column-group) (tiled.py:221-242)
+//               with no extra HBM traffic.
 //
-// Fault model: delta added to the fp32 accumulator before any checksum, ReLU or
-// store (tiled.py:197-200, :291-293); the checksum / shadow side stays clean.
+// The kernel is templated on the scheme class (plain / checksum / replication) and on the
+// checksum-group width Nt (8, 16 or generic) so each instance carries only its own
+// epilogue — the fully generic epilogue thrashed the instruction cache.
+//
+// Fault model: delta added to the fp32 accumulator before any checksum, ReLU or store
+// (tiled.py:197-200, :291-293); the checksum / shadow side stays clean.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -39,14 +44,18 @@ constexpr int EPI_WARP0 = 2;
 constexpr int CK_WARP0 = 6;
 constexpr int COLCK_SMEM_MAX = 4096;
 
+enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
+
 struct GemmParams {
   int M, N, K, m_ext, n_ext, tol_k;
-  int bm_eff, bn_eff, mt, nt, groups, nck, nck_pad;
+  int bn, bm_eff, bn_eff, mt, nt, groups, nck, nck_pad;
   int num_m_blocks, num_n_blocks, num_tiles, nkb;
   int stages, acc_stages, cols_per_acc, shadow_off, tmem_cols;
   int scheme, out_dtype, relu, split;
+  int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline)
+  int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
   double r;
-  uint32_t off_b, off_ck, off_rec, off_colck, off_bar;
+  uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_bar;
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
   void* C;
@@ -68,7 +77,6 @@ template <typename T>
 struct ElemTraits;
 template <>
 struct ElemTraits<__half> {
-  static __device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
   static __device__ __forceinline__ __half from_f(float x) { return __float2half_rn(x); }
   static __device__ __forceinline__ float2 unpack2(uint32_t u) {
     __half2 h = *reinterpret_cast<__half2*>(&u);
@@ -81,7 +89,6 @@ struct ElemTraits<__half> {
 };
 template <>
 struct ElemTraits<__nv_bfloat16> {
-  static __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
   static __device__ __forceinline__ __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
   static __device__ __forceinline__ float2 unpack2(uint32_t u) {
     __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
@@ -99,9 +106,8 @@ __device__ __forceinline__ float round_out(float y, int out_dtype) {
   return y;
 }
 
-__device__ __forceinline__ bool scheme_has_ck(int s) { return s == ABFT_ONE_SIDED || s == ABFT_TWO_SIDED; }
-__device__ __forceinline__ bool scheme_has_shadow(int s) { return s == ABFT_REPL_FULL || s == ABFT_REPL_SINGLE; }
-__device__ __forceinline__ bool scheme_thread_level(int s) { return s >= ABFT_ONE_SIDED; }
+// vector rule: per-row (or per-element) comparisons, worst one reported (tiled.py:203-218)
+__device__ __forceinline__ bool scheme_vector_rule(int s) { return s == ABFT_ONE_SIDED || s == ABFT_REPL_FULL; }
 
 // Butterfly transpose-reduction: on return lane l holds sum over the warp of v[l].
 __device__ __forceinline__ float warp_column_sums(float (&v)[32], int lane) {
@@ -118,10 +124,130 @@ __device__ __forceinline__ float warp_column_sums(float (&v)[32], int lane) {
   return v[0];
 }
 
-template <typename T, int BN>
+__device__ __noinline__ void emit_verdict(const GemmParams& p, int t_row, int t_col, bool fired, double diff,
+                                          double tol) {
+  if (p.verdicts != nullptr) {
+    abft_thread_verdict_t vv;
+    vv.t_row = t_row; vv.t_col = t_col; vv.detected = fired ? 1 : 0; vv.pad = 0;
+    vv.max_abs_diff = diff; vv.tol = tol;
+    p.verdicts[(long long)t_row * p.n_tcols + t_col] = vv;
+  }
+  if (fired && p.fired_count != nullptr) {
+    const int slot = atomicAdd(p.fired_count, 1);
+    if (p.fired != nullptr && slot < p.fired_cap) {
+      p.fired[2 * slot] = t_row;
+      p.fired[2 * slot + 1] = t_col;
+    }
+  }
+}
+
+// Verdict of one (thread-tile row, column group) once every row of the warp holds its
+// (x = checksum / shadow, y = row-group sum / output) pair.  Mt divides 32, so the Mt
+// rows of a thread tile are Mt consecutive lanes: shuffles + one ballot, no smem.
+//   vector rule: per-row compare, report the row maximising diff - tau (first on ties)
+//   scalar rule: compare sum_rows x with sum_rows y (two-sided / single-acc)
+__device__ __noinline__ void group_verdict_shuffle(const GemmParams& p, float x, float y, int lane, int t_row,
+                                                   int t_col, bool valid) {
+  const int mt = p.mt;
+  const unsigned seg = (mt == 32) ? 0xffffffffu : (((1u << mt) - 1u) << (lane & ~(mt - 1)));
+  const bool leader = (lane & (mt - 1)) == 0;
+  if (scheme_vector_rule(p.scheme)) {
+    const double dx = x, dy = y;
+    const double diff = fabs(dx - dy);
+    const double tol = tolerance(p.r, p.tol_k, dx, dy);
+    const bool fired = diff > tol;
+    const unsigned ball = __ballot_sync(0xffffffffu, fired && valid);
+    const bool tile_fired = (ball & seg) != 0;
+    if (p.verdicts != nullptr) {
+      float key = (float)(diff - tol);
+      int src = lane;
+      for (int off = 1; off < mt; off <<= 1) {
+        const float ok = __shfl_xor_sync(0xffffffffu, key, off);
+        const int os = __shfl_xor_sync(0xffffffffu, src, off);
+        if (ok > key || (ok == key && os < src)) { key = ok; src = os; }
+      }
+      const float bx = __shfl_sync(0xffffffffu, x, src);
+      const float by = __shfl_sync(0xffffffffu, y, src);
+      if (leader && valid) {
+        const double bd = fabs((double)bx - (double)by);
+        emit_verdict(p, t_row, t_col, tile_fired, bd, tolerance(p.r, p.tol_k, bx, by));
+      }
+    } else if (tile_fired && leader && valid) {
+      emit_verdict(p, t_row, t_col, true, 0.0, 0.0);
+    }
+  } else {
+    float sx = x, sy = y;
+    for (int off = 1; off < mt; off <<= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, off);
+      sy += __shfl_xor_sync(0xffffffffu, sy, off);
+    }
+    if (leader && valid) {
+      const double diff = fabs((double)sx - (double)sy);
+      const double tol = tolerance(p.r, p.tol_k, sx, sy);
+      if (p.verdicts != nullptr || diff > tol) emit_verdict(p, t_row, t_col, diff > tol, diff, tol);
+    }
+  }
+}
+
+// Generic-Mt path: verdicts of a whole tile from the smem records rec[row][group].
+__device__ __noinline__ void tile_verdicts_smem(const GemmParams& p, const float2* rec, int et, int m0, int n0) {
+  const int rs = p.rec_stride;
+  const int pairs = (p.bm_eff / p.mt) * p.groups;
+  const bool vector_rule = scheme_vector_rule(p.scheme);
+  for (int pi = et; pi < pairs; pi += 128) {
+    const int tr = pi / p.groups, gg = pi % p.groups;
+    const int vt_row = m0 / p.mt + tr, vt_col = n0 / p.nt + gg;
+    if (vt_row >= p.n_trows || vt_col >= p.n_tcols) continue;
+    double out_diff = 0.0, out_tol = 0.0;
+    bool fired = false;
+    if (vector_rule) {
+      double bk = -DBL_MAX;
+      for (int i = tr * p.mt; i < tr * p.mt + p.mt; ++i) {
+        const float2 rr = rec[i * rs + gg];
+        const double lhs = rr.x, rhs = rr.y;
+        const double diff = fabs(lhs - rhs);
+        const double tol = tolerance(p.r, p.tol_k, lhs, rhs);
+        fired |= diff > tol;
+        if (diff - tol > bk) { bk = diff - tol; out_diff = diff; out_tol = tol; }
+      }
+    } else {
+      float lhs = 0.f, rhs = 0.f;
+      for (int i = tr * p.mt; i < tr * p.mt + p.mt; ++i) {
+        const float2 rr = rec[i * rs + gg];
+        lhs += rr.x; rhs += rr.y;
+      }
+      out_diff = fabs((double)lhs - (double)rhs);
+      out_tol = tolerance(p.r, p.tol_k, lhs, rhs);
+      fired = out_diff > out_tol;
+    }
+    if (p.verdicts != nullptr || fired) emit_verdict(p, vt_row, vt_col, fired, out_diff, out_tol);
+  }
+}
+
+// One finished (row, group) pair: shuffle verdict or smem record.
+__device__ __forceinline__ void group_done(const GemmParams& p, float2* rec, int row, int lane, int g, float x,
+                                           float y, int n0, int t_row, bool row_verdict) {
+  if (p.shuffle_verdicts) {
+    const int t_col = (n0 + g * p.nt) / p.nt;
+    group_verdict_shuffle(p, x, y, lane, t_row, t_col, row_verdict && t_col < p.n_tcols);
+  } else {
+    rec[row * p.rec_stride + g] = make_float2(x, y);
+  }
+}
+
+// fault injection for one 32-column chunk of one row (rare path, kept compact)
+__device__ __noinline__ void apply_faults(const GemmParams& p, float* v, int gm, int gc0, int cmax) {
+  for (int f = 0; f < p.nfaults; ++f) {
+    const abft_fault_t ft = p.faults[f];
+    const int j = ft.col - gc0;
+    if (ft.row == gm && j >= 0 && j < 32 && j < cmax) v[j] += ft.delta;
+  }
+}
+
+template <typename T, int CLASS, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ GemmParams p) {
+                     const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ GemmParams p) {
   using TR = ElemTraits<T>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -130,7 +256,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sm_a = smem;
   uint8_t* sm_b = smem + p.off_b;
   uint8_t* sm_ck = smem + p.off_ck;
-  float2* rec = reinterpret_cast<float2*>(smem + p.off_rec);
+  float* cks = reinterpret_cast<float*>(smem + p.off_cks);       // [group][128] checksum column per row
+  float2* rec = reinterpret_cast<float2*>(smem + p.off_rec);     // [128][rec_stride] (generic Mt)
+  float* stg = reinterpret_cast<float*>(smem + p.off_stage);     // [2][32][128] chunk staging (generic Nt)
   float* colck_s = reinterpret_cast<float*>(smem + p.off_colck);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* full = bars;
@@ -143,28 +271,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool has_ck = scheme_has_ck(p.scheme);
-  const bool has_shadow = scheme_has_shadow(p.scheme);
-  const bool thread_level = scheme_thread_level(p.scheme);
+  constexpr bool has_ck = CLASS == CLASS_CHECKSUM;
+  constexpr bool has_shadow = CLASS == CLASS_REPLICA;
+  constexpr bool thread_level = CLASS != CLASS_PLAIN;
+  const bool ck_onchip = has_ck && p.ck_mode == 1;
+  const bool ck_loaded = has_ck && p.ck_mode == 2;
+  const int bn = p.bn;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&ckfull[s], 128);
+      ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], 4);    // one arrival per epilogue warp
     }
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
+    if (ck_loaded) ptx::tma_prefetch(&tmCK);
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
-  if (warp >= CK_WARP0 && has_ck) {
+  if (warp >= CK_WARP0 && ck_onchip) {
     // zero the padding checksum rows [nck, nck_pad) of every stage once
     const int ct = threadIdx.x - CK_WARP0 * 32;
     const int pad_rows = p.nck_pad - p.nck;
@@ -187,24 +319,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = p.stage_a_bytes + p.stage_b_bytes;
+      const uint32_t tx = p.stage_a_bytes + p.stage_b_bytes + (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int nb = tile % p.num_n_blocks;
         const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
-        const int n0 = (tile % p.num_n_blocks) * p.bn_eff;
+        const int n0 = nb * p.bn_eff;
+#pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], tx);
           ptx::tma_load_2d(sm_a + s * p.stage_a_bytes, &tmA, &full[s], kb * BK, m0);
           ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, n0);
+          if (ck_loaded) ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.nck_pad);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
+    // The checksum N-slice of a stage generated on chip is issued one stage late, so the
+    // main MMAs never wait for the checksum warps.
     if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
+      int s = 0, ps = 0;
+      uint32_t ph = 0, pph = 0;
       int t_local = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
         const int acc = t_local % p.acc_stages;
@@ -212,9 +349,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.cols_per_acc);
+#pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&full[s], ph);
-          if (has_ck) ptx::mbar_wait(&ckfull[s], ph);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
           const uint32_t b_addr = ptx::smem_u32(sm_b + s * p.stage_b_bytes);
@@ -225,34 +362,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
             ptx::mma_f16_ss(d, adesc, bdesc, p.idesc_main, accum);
-            if (has_ck) ptx::mma_f16_ss(d + BN, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
+            if (ck_loaded) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
             if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
           }
-          ptx::mma_commit(&empty[s]);
+          if (ck_onchip) {
+            if (kb > 0) {
+              // checksum slice of the previous stage, then release that stage
+              ptx::mbar_wait(&ckfull[ps], pph);
+              ptx::tc_fence_after();
+              const uint32_t pa = ptx::smem_u32(sm_a + ps * p.stage_a_bytes);
+              const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                ptx::mma_f16_ss(d + bn, ptx::desc_kmajor_sw128(pa + k * 32), ptx::desc_kmajor_sw128(pc + k * 32),
+                                p.idesc_ck, (kb - 1 > 0 || k > 0) ? 1u : 0u);
+              ptx::mma_commit(&empty[ps]);
+            }
+            ps = s; pph = ph;
+          } else {
+            ptx::mma_commit(&empty[s]);
+          }
           if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+        if (ck_onchip) {
+          ptx::mbar_wait(&ckfull[ps], pph);
+          ptx::tc_fence_after();
+          const uint32_t pa = ptx::smem_u32(sm_a + ps * p.stage_a_bytes);
+          const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::mma_f16_ss(d + bn, ptx::desc_kmajor_sw128(pa + k * 32), ptx::desc_kmajor_sw128(pc + k * 32),
+                            p.idesc_ck, (p.nkb - 1 > 0 || k > 0) ? 1u : 0u);
+          ptx::mma_commit(&empty[ps]);
         }
         ptx::mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= CK_WARP0) {
     // ----------------------------------------------- checksum-row generator
-    if (has_ck) {
+    if (ck_onchip) {
       const int ct = threadIdx.x - CK_WARP0 * 32;
       const int items = p.groups * 8;
+      const int nt = NT > 0 ? NT : p.nt;
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+#pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&full[s], ph);
           const uint8_t* bt = sm_b + s * p.stage_b_bytes;
           uint8_t* ck = sm_ck + s * p.stage_ck_bytes;
+#pragma unroll 1
           for (int it = ct; it < items; it += 128) {
             const int g = it >> 3, c = it & 7;
             float acc[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-            const int r0 = g * p.nt;
-            for (int r = 0; r < p.nt; ++r) {
+            const int r0 = g * nt;
+#pragma unroll 4
+            for (int r = 0; r < nt; ++r) {
               const int n = r0 + r;
               const uint4 raw = *reinterpret_cast<const uint4*>(bt + n * 128 + ((c ^ (n & 7)) << 4));
               const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
@@ -278,7 +446,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&ckfull[s]);
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ckfull[s]);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       }
@@ -289,7 +458,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;                         // TMEM lane quadrant of this warp
     const int row = q * 32 + lane;                  // tile row == TMEM lane
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const int rs = p.rec_stride;
     double rhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
     int t_local = 0;
@@ -301,6 +469,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int gm = m0 + row;
       const bool row_in_tile = row < p.bm_eff;
       const bool row_store = row_in_tile && gm < p.M;
+      const int t_row = thread_level ? gm / p.mt : 0;
+      const bool row_verdict = row_in_tile && t_row < p.n_trows;
       bool row_fault = false;
       if (row_in_tile)
         for (int f = 0; f < p.nfaults; ++f) row_fault |= (p.faults[f].row == gm);
@@ -311,64 +481,97 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::tc_fence_after();
       const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * p.cols_per_acc);
 
-      if (has_ck) {
-        // checksum column per (row, group): hi (+ lo) TMEM columns -> rec[row][g].x
-        for (int c0 = 0; c0 < p.groups; c0 += 32) {
-          float hi[32], lo[32];
-          __syncwarp();
-          ptx::tmem_ld32(tacc + BN + c0, hi);
-          if (p.split) ptx::tmem_ld32(tacc + BN + p.groups + c0, lo);
-          ptx::tmem_ld_wait();
+      if constexpr (has_ck) {
+        // checksum column per (row, group) -> cks[g][row] (groups <= 32)
+        float hi[32], lo[32];
+        __syncwarp();
+        ptx::tmem_ld32(tacc + bn, hi);
+        if (p.split) ptx::tmem_ld32(tacc + bn + p.groups, lo);
+        ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (c0 + j < p.groups) rec[row * rs + c0 + j].x = p.split ? hi[j] + lo[j] : hi[j];
-          }
-        }
+        for (int j = 0; j < 32; ++j)
+          if (j < p.groups) cks[j * BM + row] = p.split ? hi[j] + lo[j] : hi[j];
       }
 
+      // generic-Nt running state
       float gsum = 0.f, ssum = 0.f, best_c = 0.f, best_s = 0.f;
-      double best_key = -DBL_MAX;
+      float best_key = -FLT_MAX;
       int cnt = 0, g = 0;
       float tsum = 0.f;
+#pragma unroll 1
       for (int c0 = 0; c0 < p.bn_eff; c0 += 32) {
         float v[32], sh[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
-        if (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
+        if constexpr (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
         ptx::tmem_ld_wait();
         const int gc0 = n0 + c0;
-        if (row_fault) {
+        const int cmax = p.bn_eff - c0;
+        if (row_fault) apply_faults(p, v, gm, gc0, cmax);
+        if constexpr (thread_level && NT > 0) {
+          // static group structure: 32 / NT complete groups per chunk (NT divides 32 and bn_eff)
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            for (int f = 0; f < p.nfaults; ++f)
-              if (p.faults[f].row == gm && p.faults[f].col == gc0 + j && c0 + j < p.bn_eff) v[j] += p.faults[f].delta;
-        }
-        if (thread_level) {
+          for (int gi = 0; gi < 32 / NT; ++gi) {
+            if (gi * NT < cmax) {
+              const int gg = c0 / NT + gi;
+              float x, y = 0.f;
+              if constexpr (has_ck) {
+#pragma unroll
+                for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
+                x = cks[gg * BM + row];
+              } else {
+                if (p.scheme == ABFT_REPL_FULL) {
+                  float bk = -FLT_MAX;
+                  x = 0.f;
+#pragma unroll
+                  for (int e = 0; e < NT; ++e) {
+                    const float cv = v[gi * NT + e], sv = sh[gi * NT + e];
+                    const float key = (float)(fabs((double)cv - (double)sv) - tolerance(p.r, p.tol_k, sv, cv));
+                    if (key > bk) { bk = key; x = sv; y = cv; }
+                  }
+                } else {
+                  x = 0.f;
+#pragma unroll
+                  for (int e = 0; e < NT; ++e) { x += sh[gi * NT + e]; y += v[gi * NT + e]; }
+                }
+              }
+              group_done(p, rec, row, lane, gg, x, y, n0, t_row, row_verdict);
+            }
+          }
+        } else if constexpr (thread_level) {
+          // generic Nt: stage the chunk in smem and walk it with dynamic group boundaries
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            if (c0 + j < p.bn_eff) {
-              const float x = v[j];
-              gsum += x;
+            stg[j * BM + row] = v[j];
+            if constexpr (has_shadow) stg[(32 + j) * BM + row] = sh[j];
+          }
+          const int jmax = min(32, cmax);
+#pragma unroll 1
+          for (int j = 0; j < jmax; ++j) {
+            const float xv = stg[j * BM + row];
+            gsum += xv;
+            if constexpr (has_shadow) {
+              const float sv = stg[(32 + j) * BM + row];
               if (p.scheme == ABFT_REPL_FULL) {
-                const double dx = x, ds = sh[j];
-                const double key = fabs(dx - ds) - tolerance(p.r, p.tol_k, ds, dx);
-                if (key > best_key) { best_key = key; best_c = x; best_s = sh[j]; }
-              } else if (p.scheme == ABFT_REPL_SINGLE) {
-                ssum += sh[j];
+                const float key = (float)(fabs((double)xv - (double)sv) - tolerance(p.r, p.tol_k, sv, xv));
+                if (key > best_key) { best_key = key; best_c = xv; best_s = sv; }
+              } else {
+                ssum += sv;
               }
-              if (++cnt == p.nt) {
-                float2& rr = rec[row * rs + g];
-                if (p.scheme == ABFT_REPL_FULL) rr = make_float2(best_s, best_c);
-                else if (p.scheme == ABFT_REPL_SINGLE) rr = make_float2(ssum, gsum);
-                else rr.y = gsum;
-                gsum = 0.f; ssum = 0.f; best_key = -DBL_MAX; cnt = 0; ++g;
-              }
+            }
+            if (++cnt == p.nt) {
+              float x, y;
+              if constexpr (has_ck) { x = cks[g * BM + row]; y = gsum; }
+              else if (p.scheme == ABFT_REPL_FULL) { x = best_s; y = best_c; }
+              else { x = ssum; y = gsum; }
+              group_done(p, rec, row, lane, g, x, y, n0, t_row, row_verdict);
+              gsum = 0.f; ssum = 0.f; best_key = -FLT_MAX; cnt = 0; ++g;
             }
           }
         }
         if (p.out_sum != nullptr) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) tsum += (c0 + j < p.bn_eff) ? v[j] : 0.f;
+          for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
         }
         if (p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) {
           // ReLU + rounding to the storage grid (checksum.py:235 storage_array(activation(c)))
@@ -377,7 +580,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float y = p.relu ? fmaxf(v[j], 0.f) : v[j];
             v[j] = round_out(y, p.out_dtype);
           }
-          const bool full_chunk = (c0 + 32 <= p.bn_eff) && (gc0 + 32 <= p.N);
+          const bool full_chunk = (cmax >= 32) && (gc0 + 32 <= p.N);
           if (row_store && p.out_dtype != ABFT_OUT_NONE) {
             if (p.out_dtype == ABFT_OUT_F32) {
               float* dst = reinterpret_cast<float*>(p.C) + (long long)gm * p.ldc + gc0;
@@ -386,9 +589,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int j = 0; j < 32; j += 4)
                   *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
               } else {
-#pragma unroll
+#pragma unroll 1
                 for (int j = 0; j < 32; ++j)
-                  if (c0 + j < p.bn_eff && gc0 + j < p.N) dst[j] = v[j];
+                  if (j < cmax && gc0 + j < p.N) dst[j] = v[j];
               }
             } else {
               T* dst = reinterpret_cast<T*>(p.C) + (long long)gm * p.ldc + gc0;
@@ -403,17 +606,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   *reinterpret_cast<uint4*>(dst + j) = u;
                 }
               } else {
-#pragma unroll
+#pragma unroll 1
                 for (int j = 0; j < 32; ++j)
-                  if (c0 + j < p.bn_eff && gc0 + j < p.N) dst[j] = TR::from_f(v[j]);
+                  if (j < cmax && gc0 + j < p.N) dst[j] = TR::from_f(v[j]);
               }
             }
           }
           if (p.next_colck != nullptr) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = (row_store && c0 + j < p.bn_eff && gc0 + j < p.N) ? v[j] : 0.f;
+            for (int j = 0; j < 32; ++j) v[j] = (row_store && j < cmax && gc0 + j < p.N) ? v[j] : 0.f;
             const float colsum = warp_column_sums(v, lane);
-            if (c0 + lane < p.bn_eff && gc0 + lane < p.N && colsum != 0.f) {
+            if (lane < cmax && gc0 + lane < p.N && colsum != 0.f) {
               if (p.colck_in_smem) atomicAdd(&colck_s[gc0 + lane], colsum);
               else atomicAdd(&p.next_colck[gc0 + lane], colsum);
             }
@@ -422,55 +625,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // TMEM accumulator stage fully read: hand it back to the MMA issuer
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       if (row_in_tile) rhs_acc += (double)tsum;
 
-      if (thread_level) {
+      if (thread_level && !p.shuffle_verdicts) {
         ptx::named_bar_sync(1, 128);
-        const int tr_count = p.bm_eff / p.mt;
-        const int pairs = tr_count * p.groups;
-        const bool vector_rule = (p.scheme == ABFT_ONE_SIDED || p.scheme == ABFT_REPL_FULL);
-        for (int pi = et; pi < pairs; pi += 128) {
-          const int tr = pi / p.groups, gg = pi % p.groups;
-          const int t_row = m0 / p.mt + tr, t_col = n0 / p.nt + gg;
-          if (t_row >= p.n_trows || t_col >= p.n_tcols) continue;
-          double out_diff, out_tol;
-          bool fired = false;
-          if (vector_rule) {
-            double bk = -DBL_MAX;
-            out_diff = 0.0; out_tol = 0.0;
-            for (int i = tr * p.mt; i < tr * p.mt + p.mt; ++i) {
-              const float2 rr = rec[i * rs + gg];
-              const double lhs = rr.x, rhs = rr.y;
-              const double diff = fabs(lhs - rhs);
-              const double tol = tolerance(p.r, p.tol_k, lhs, rhs);
-              fired |= diff > tol;
-              if (diff - tol > bk) { bk = diff - tol; out_diff = diff; out_tol = tol; }
-            }
-          } else {
-            double lhs = 0.0, rhs = 0.0;
-            for (int i = tr * p.mt; i < tr * p.mt + p.mt; ++i) {
-              const float2 rr = rec[i * rs + gg];
-              lhs += rr.x; rhs += rr.y;
-            }
-            out_diff = fabs(lhs - rhs);
-            out_tol = tolerance(p.r, p.tol_k, lhs, rhs);
-            fired = out_diff > out_tol;
-          }
-          if (p.verdicts != nullptr) {
-            abft_thread_verdict_t vv;
-            vv.t_row = t_row; vv.t_col = t_col; vv.detected = fired ? 1 : 0; vv.pad = 0;
-            vv.max_abs_diff = out_diff; vv.tol = out_tol;
-            p.verdicts[(long long)t_row * p.n_tcols + t_col] = vv;
-          }
-          if (fired && p.fired_count != nullptr) {
-            const int slot = atomicAdd(p.fired_count, 1);
-            if (p.fired != nullptr && slot < p.fired_cap) {
-              p.fired[2 * slot] = t_row;
-              p.fired[2 * slot + 1] = t_col;
-            }
-          }
-        }
+        tile_verdicts_smem(p, rec, et, m0, n0);
         ptx::named_bar_sync(1, 128);
       }
     }
@@ -557,30 +718,32 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
   return ABFT_OK;
 }
 
-template <typename T, int BN>
-int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, size_t smem, int grid,
-              cudaStream_t st) {
+template <typename T, int CLASS, int NT>
+int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const GemmParams& p, size_t smem,
+                int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
-  abft_gemm_kernel<T, BN><<<grid, NUM_THREADS, smem, st>>>(ma, mb, p);
+  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
 template <typename T>
-int launch_typed(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, size_t smem, int grid,
-                 cudaStream_t st) {
-  switch (bn) {
-    case 32: return launch_bn<T, 32>(ma, mb, p, smem, grid, st);
-    case 64: return launch_bn<T, 64>(ma, mb, p, smem, grid, st);
-    case 128: return launch_bn<T, 128>(ma, mb, p, smem, grid, st);
-    case 256: return launch_bn<T, 256>(ma, mb, p, smem, grid, st);
+int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                 const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, p, smem, grid, st);
+  if (cls == CLASS_CHECKSUM) {
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, p, smem, grid, st);
+    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, p, smem, grid, st);
   }
-  return fail(ABFT_E_VALUE, "unsupported tile_n");
+  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, p, smem, grid, st);
+  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, p, smem, grid, st);
+  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, p, smem, grid, st);
 }
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -591,79 +754,93 @@ uint32_t pow2_at_least(uint32_t x) {
   return r;
 }
 
-}  // namespace
-}  // namespace abft
+struct Plan {
+  GemmParams p;
+  int cls, ntc;
+  size_t smem;
+  int grid;
+  int ck_offline_recommended;
+};
 
-using namespace abft;
+int tile_cols(int bn, int nt, bool has_ck, bool has_shadow, int split) {
+  int cols = bn;
+  if (has_ck) cols += round_up((bn / nt) * (split ? 2 : 1), 16);
+  if (has_shadow) cols += bn;
+  return cols;
+}
 
-extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_args_t* a, void* stream) {
+// Choose the CTA tile and carve shared memory / TMEM for one call.
+int make_plan(const abft_gemm_args_t* a, Plan& out) {
   if (a == nullptr) return fail(ABFT_E_VALUE, "null args");
   if (a->M < 1 || a->N < 1 || a->K < 1) return fail(ABFT_E_SHAPE, "GEMM extents must be >= 1");
   if (a->dtype != ABFT_F16 && a->dtype != ABFT_BF16) return fail(ABFT_E_VALUE, "dtype must be ABFT_F16 or ABFT_BF16");
   if (a->scheme < ABFT_UNPROTECTED || a->scheme > ABFT_REPL_SINGLE) return fail(ABFT_E_VALUE, "unknown scheme");
-  if (a->lda < a->K || a->ldbt < a->K || (a->lda % 8) || (a->ldbt % 8))
-    return fail(ABFT_E_SHAPE, "lda/ldbt must be >= K and multiples of 8 (16-byte TMA row pitch)");
-  if ((reinterpret_cast<uintptr_t>(a->A) & 15) || (reinterpret_cast<uintptr_t>(a->Bt) & 15))
-    return fail(ABFT_E_VALUE, "A and Bt must be 16-byte aligned");
-  if (a->out_dtype != ABFT_OUT_NONE && (a->C == nullptr || a->ldc < a->N))
-    return fail(ABFT_E_SHAPE, "C must be non-null with ldc >= N");
   const bool thread_level = a->scheme >= ABFT_ONE_SIDED;
   const bool has_ck = a->scheme == ABFT_ONE_SIDED || a->scheme == ABFT_TWO_SIDED;
   const bool has_shadow = a->scheme == ABFT_REPL_FULL || a->scheme == ABFT_REPL_SINGLE;
-  int mt = thread_level ? a->thread_m : 1, nt = thread_level ? a->thread_n : 1;
-  int m_ext = thread_level ? a->m_ext : a->M, n_ext = thread_level ? a->n_ext : a->N;
+  const int mt = thread_level ? a->thread_m : 1, nt = thread_level ? a->thread_n : 1;
+  const int m_ext = thread_level ? a->m_ext : a->M, n_ext = thread_level ? a->n_ext : a->N;
   if (thread_level) {
     if (mt < 1 || nt < 1 || mt > BM || nt > 256) return fail(ABFT_E_UNSUPPORTED, "thread tile must be <= 128 x 256");
     if (m_ext < a->M || n_ext < a->N || m_ext % mt || n_ext % nt)
       return fail(ABFT_E_SHAPE, "m_ext/n_ext must cover M/N and be multiples of the thread tile");
   }
-  if (a->scheme == ABFT_GLOBAL && a->out_sum == nullptr) return fail(ABFT_E_VALUE, "global scheme needs out_sum");
-
+  const int split = (has_ck && a->ck_split) ? 1 : 0;
   const int sms = a->num_sms > 0 ? a->num_sms : num_sms();
-  // ---- CTA N tile
+  const int bm_eff = (BM / mt) * mt;
+  const int m_blocks = ceil_div(m_ext, bm_eff);
+
   int bn = a->tile_n;
   if (bn == 0) {
-    // largest tile that still gives >= one tile per SM; otherwise the smallest
-    // efficient one (max parallelism for bandwidth-bound layers).  Thread-level
-    // schemes keep <= 32 checksum groups per tile (epilogue record budget).
-    const int cap = thread_level ? std::min(256, 32 * nt) : 256;
-    const int m_blocks = ceil_div(m_ext, (BM / mt) * mt);
-    int smallest = 0;
-    bn = 0;
-    for (int cand : {256, 128, 64, 32}) {
-      if (cand > cap || cand < nt) continue;
-      if (cand > 32 && cand / 2 >= round_up(n_ext, 32)) continue;     // > 2x wider than needed
-      if (cand == 32 && n_ext > 32 && cap >= 64 && nt <= 64) continue;  // 64 is the narrowest efficient tile
-      const int eff = (cand / nt) * nt;
-      if (bn == 0 && (long long)m_blocks * ceil_div(n_ext, eff) >= sms) bn = cand;
-      smallest = cand;
+    // largest tile that still gives >= one tile per SM, preferring TMEM double buffering;
+    // otherwise the narrowest efficient tile (max parallelism for bandwidth-bound layers).
+    // Thread-level schemes keep <= 32 checksum groups per tile.
+    int best = 0, smallest = 0;
+    for (int pass = 0; pass < 2 && best == 0; ++pass) {
+      for (int cand : {256, 192, 128, 64, 32}) {
+        if (cand < nt || (thread_level && cand / nt > 32)) continue;
+        if (cand > 32 && cand / 2 >= round_up(n_ext, 32) && cand != 64) continue;   // far wider than needed
+        if (cand == 32 && n_ext > 32 && nt <= 64 && cand * 2 <= 32 * nt) continue;  // 64 is the narrowest efficient tile
+        const int cols = tile_cols(cand, nt, has_ck, has_shadow, split);
+        if (cols > 512) continue;
+        if (pass == 0 && 2 * cols > 512) continue;                                   // pass 0: double-buffered only
+        const int eff = (cand / nt) * nt;
+        if (best == 0 && (long long)m_blocks * ceil_div(n_ext, eff) >= sms) best = cand;
+        smallest = cand;
+      }
+      if (best == 0 && pass == 0 && smallest != 0) best = smallest;
     }
-    if (bn == 0) bn = smallest;
+    bn = best;
     if (bn == 0) return fail(ABFT_E_UNSUPPORTED, "no CTA tile fits this thread tile");
   }
-  if (bn != 32 && bn != 64 && bn != 128 && bn != 256) return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/256");
+  if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 256)
+    return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/192/256");
   if (bn < nt) return fail(ABFT_E_UNSUPPORTED, "thread_n larger than the CTA tile");
 
-  GemmParams p{};
+  GemmParams& p = out.p;
+  p = GemmParams{};
   p.M = a->M; p.N = a->N; p.K = a->K; p.m_ext = m_ext; p.n_ext = n_ext; p.tol_k = a->tol_k > 0 ? a->tol_k : a->K;
+  p.bn = bn;
   p.mt = mt; p.nt = nt;
-  p.bm_eff = (BM / mt) * mt;
+  p.bm_eff = bm_eff;
   p.bn_eff = (bn / nt) * nt;
   p.groups = thread_level ? p.bn_eff / nt : 0;
   if (thread_level && p.groups > 32) return fail(ABFT_E_UNSUPPORTED, "more than 32 checksum groups per CTA tile");
-  p.split = (has_ck && a->ck_split) ? 1 : 0;
-  p.nck = has_ck ? p.groups * (p.split ? 2 : 1) : 0;
+  p.split = split;
+  p.nck = has_ck ? p.groups * (split ? 2 : 1) : 0;
   p.nck_pad = has_ck ? round_up(p.nck, 16) : 0;
-  p.num_m_blocks = ceil_div(m_ext, p.bm_eff);
+  p.num_m_blocks = m_blocks;
   p.num_n_blocks = ceil_div(n_ext, p.bn_eff);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   p.nkb = ceil_div(a->K, BK);
-  p.cols_per_acc = bn + p.nck_pad + (has_shadow ? bn : 0);
+  p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split);
   p.shadow_off = bn + p.nck_pad;
-  p.acc_stages = (2 * p.cols_per_acc <= 512) ? 2 : 1;
   if (p.cols_per_acc > 512) return fail(ABFT_E_UNSUPPORTED, "TMEM budget exceeded");
+  p.acc_stages = (2 * p.cols_per_acc <= 512) ? 2 : 1;
   p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
+  p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : 0;
+  p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
   p.C = a->C; p.ldc = a->ldc;
   p.faults = a->faults; p.nfaults = a->faults ? a->nfaults : 0;
@@ -676,36 +853,133 @@ extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = has_ck ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
+  out.cls = has_ck ? CLASS_CHECKSUM : has_shadow ? CLASS_REPLICA : CLASS_PLAIN;
+  // static group width when it divides both the 32-column chunk and the tile
+  out.ntc = (thread_level && (nt == 8 || nt == 16) && p.bn_eff % 32 == 0) ? nt : 0;
 
   // ---- shared memory carve-up (all tile buffers 1024-aligned)
   p.stage_a_bytes = BM * BK * 2;
   p.stage_b_bytes = bn * BK * 2;
   p.stage_ck_bytes = (uint32_t)round_up(p.nck_pad * BK * 2, 1024);
-  p.rec_stride = thread_level ? (p.groups | 1) : 0;
-  const uint32_t rec_bytes = thread_level ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
+  p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
+  const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
+  const uint32_t rec_bytes = p.rec_stride ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
+  const uint32_t stage_bytes_ep = (thread_level && out.ntc == 0) ? (uint32_t)(2 * 32 * BM * 4) : 0;
   const uint32_t colck_bytes = p.colck_in_smem ? (uint32_t)round_up(a->N * 4, 1024) : 0;
   const uint32_t bar_bytes = 1024;
+  const uint32_t extras = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + bar_bytes;
   const uint32_t stage_bytes = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes;
-  const int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)(rec_bytes + colck_bytes + bar_bytes);
+  const int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
   int stages = budget / (int)stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(ABFT_E_UNSUPPORTED, "shared memory budget too small for a 2-stage pipeline");
   p.stages = stages;
   p.off_b = stages * p.stage_a_bytes;
   p.off_ck = p.off_b + stages * p.stage_b_bytes;
-  p.off_rec = p.off_ck + stages * p.stage_ck_bytes;
-  p.off_colck = p.off_rec + rec_bytes;
+  p.off_cks = p.off_ck + stages * p.stage_ck_bytes;
+  p.off_rec = p.off_cks + cks_bytes;
+  p.off_stage = p.off_rec + rec_bytes;
+  p.off_colck = p.off_stage + stage_bytes_ep;
   p.off_bar = p.off_colck + colck_bytes;
-  const size_t smem = (size_t)p.off_bar + bar_bytes + 1024;
+  out.smem = (size_t)p.off_bar + bar_bytes + 1024;
+  out.grid = std::min(p.num_tiles, sms);
+  out.ck_offline_recommended = (has_ck && p.num_m_blocks > 2) ? 1 : 0;
+  return ABFT_OK;
+}
 
-  CUtensorMap ma, mb;
-  int rc = cached_map(&ma, a->A, a->dtype, a->K, a->M, a->lda, BM);
-  if (rc != ABFT_OK) return rc;
-  rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, bn);
-  if (rc != ABFT_OK) return rc;
+// offline checksum rows: out[nb*nck_pad + j][k] = hi/lo of sum_{r<nt} Bt[nb*bn_eff + j*nt + r][k]
+// (row j < G: hi of group j; G <= j < 2G with split: lo of group j-G; else 0) — the same fp32
+// summation order as the on-chip generator, so both modes give identical checksum columns.
+template <typename T>
+__global__ void ck_rows_kernel(const T* __restrict__ bt, int n, int k, long long ldbt, int bn_eff, int nt, int groups,
+                               int split, int nck_pad, int n_blocks, T* __restrict__ out, long long ldo, int kcols) {
+  const long long total = (long long)n_blocks * nck_pad * kcols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / kcols), kk = (int)(i % kcols);
+    const int nb = row / nck_pad, j = row % nck_pad;
+    const int g = (j < groups) ? j : (split && j < 2 * groups ? j - groups : -1);
+    float acc = 0.f;
+    if (g >= 0 && kk < k) {
+      for (int r = 0; r < nt; ++r) {
+        const int nrow = nb * bn_eff + g * nt + r;
+        const float v = nrow < n ? (float)bt[(long long)nrow * ldbt + kk] : 0.f;
+        acc += v;
+      }
+    }
+    float val = 0.f;
+    if (g >= 0) {
+      const float hi = (float)ElemTraits<T>::from_f(acc);
+      val = (j < groups) ? hi : acc - hi;
+    }
+    out[(long long)row * ldo + kk] = ElemTraits<T>::from_f(val);
+  }
+}
 
-  const int grid = std::min(p.num_tiles, sms);
+}  // namespace
+}  // namespace abft
+
+using namespace abft;
+
+extern "C" __attribute__((visibility("default"))) int abft_gemm_plan(const abft_gemm_args_t* a, int32_t* out) {
+  Plan pl;
+  int rc = make_plan(a, pl);
+  if (rc != ABFT_OK) return rc;
+  out[0] = pl.p.bn; out[1] = pl.p.bn_eff; out[2] = pl.p.groups; out[3] = pl.p.nck_pad; out[4] = pl.p.stages;
+  out[5] = pl.ck_offline_recommended; out[6] = pl.p.num_n_blocks; out[7] = pl.grid;
+  return ABFT_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_ck_rows(const void* Bt, int32_t N, int32_t K, int64_t ldbt,
+                                                                  int32_t dtype, int32_t bn_eff, int32_t nt,
+                                                                  int32_t split, int32_t nck_pad, int32_t n_blocks,
+                                                                  void* out, int64_t ldo, void* stream) {
+  if (N < 1 || K < 1 || nt < 1 || bn_eff < nt || bn_eff % nt || nck_pad < 16 || nck_pad % 16 || ldo < K || ldbt < K)
+    return fail(ABFT_E_SHAPE, "ck_rows: bad extents");
+  const int groups = bn_eff / nt;
+  if (groups * (split ? 2 : 1) > nck_pad) return fail(ABFT_E_SHAPE, "ck_rows: nck_pad too small");
+  if (n_blocks < ceil_div(N, bn_eff)) return fail(ABFT_E_SHAPE, "ck_rows: n_blocks does not cover N");
+  const int kcols = (int)ldo;
+  const long long total = (long long)n_blocks * nck_pad * kcols;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
   cudaStream_t st = as_stream(stream);
-  if (a->dtype == ABFT_BF16) return launch_typed<__nv_bfloat16>(bn, ma, mb, p, smem, grid, st);
-  return launch_typed<__half>(bn, ma, mb, p, smem, grid, st);
+  if (dtype == ABFT_BF16)
+    ck_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)Bt, N, K, ldbt, bn_eff, nt, groups,
+                                                          split, nck_pad, n_blocks, (__nv_bfloat16*)out, ldo, kcols);
+  else
+    ck_rows_kernel<__half><<<blocks, 256, 0, st>>>((const __half*)Bt, N, K, ldbt, bn_eff, nt, groups, split, nck_pad,
+                                                   n_blocks, (__half*)out, ldo, kcols);
+  return cuda_check(cudaGetLastError(), "ck_rows launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_args_t* a, void* stream) {
+  if (a == nullptr) return fail(ABFT_E_VALUE, "null args");
+  if (a->lda < a->K || a->ldbt < a->K || (a->lda % 8) || (a->ldbt % 8))
+    return fail(ABFT_E_SHAPE, "lda/ldbt must be >= K and multiples of 8 (16-byte TMA row pitch)");
+  if ((reinterpret_cast<uintptr_t>(a->A) & 15) || (reinterpret_cast<uintptr_t>(a->Bt) & 15))
+    return fail(ABFT_E_VALUE, "A and Bt must be 16-byte aligned");
+  if (a->out_dtype != ABFT_OUT_NONE && (a->C == nullptr || a->ldc < a->N))
+    return fail(ABFT_E_SHAPE, "C must be non-null with ldc >= N");
+  if (a->scheme == ABFT_GLOBAL && a->out_sum == nullptr) return fail(ABFT_E_VALUE, "global scheme needs out_sum");
+  Plan pl;
+  int rc = make_plan(a, pl);
+  if (rc != ABFT_OK) return rc;
+  const GemmParams& p = pl.p;
+
+  CUtensorMap ma, mb, mc;
+  rc = cached_map(&ma, a->A, a->dtype, a->K, a->M, a->lda, BM);
+  if (rc != ABFT_OK) return rc;
+  rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
+  if (rc != ABFT_OK) return rc;
+  if (p.ck_mode == 2) {
+    if (a->ck_rows_n != p.num_n_blocks * p.nck_pad || a->ldck < a->K || (a->ldck % 8) ||
+        (reinterpret_cast<uintptr_t>(a->ck_rows) & 15))
+      return fail(ABFT_E_SHAPE, "ck_rows do not match this call's plan (see abft_gemm_plan)");
+    rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
+    if (rc != ABFT_OK) return rc;
+  } else {
+    mc = mb;   // unused
+  }
+  cudaStream_t st = as_stream(stream);
+  if (a->dtype == ABFT_BF16) return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
+  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
 }

@@ -27,17 +27,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // spin on try_wait without a suspend-time hint: the hinted form compiles to a
+  // NANOSLEEP loop whose wake-up latency sits on every pipeline hand-off
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t"
       ".reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
       "}" ::"r"(addr),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity)
       : "memory");
 }
 

@@ -23,7 +23,8 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
          relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
          tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
          fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-         num_sms: int = 0) -> None:
+         num_sms: int = 0, ck_rows=None, plan_only: bool = False):
+    """Enqueue one protected GEMM (or, with plan_only, return the kernel plan dict)."""
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = bt.data_ptr(), ldbt
@@ -42,7 +43,25 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
     args.fired = fired.data_ptr() if fired is not None else None
     args.fired_cap = fired_cap
     args.tile_n, args.num_sms = tile_n, num_sms
+    if ck_rows is not None:
+        args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
+    if plan_only:
+        out = (ctypes.c_int32 * 8)()
+        _lib.check(_lib.load().abft_gemm_plan(ctypes.byref(args), out))
+        return dict(tile_n=out[0], bn_eff=out[1], groups=out[2], nck_pad=out[3], stages=out[4],
+                    ck_offline_recommended=bool(out[5]), n_blocks=out[6], grid=out[7])
     _lib.check(_lib.load().abft_gemm(ctypes.byref(args), stream_handle()))
+    return None
+
+
+def ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, split: bool):
+    """Offline checksum rows of a K-major weight for one kernel plan (abft_ck_rows)."""
+    t = torch()
+    rows = plan["n_blocks"] * plan["nck_pad"]
+    out = t.empty((rows, bt.shape[1]), dtype=bt.dtype, device="cuda")
+    _lib.call("abft_ck_rows", ptr(bt), n, k, bt.stride(0), storage_code(dtype), plan["bn_eff"], thread_n,
+              int(split), plan["nck_pad"], plan["n_blocks"], ptr(out), out.stride(0), stream_handle())
+    return out
 
 
 def colsum(x, rows: int, cols: int, ldx: int, dtype: DType, out, accumulate: bool = False) -> None:

@@ -112,7 +112,7 @@ def _thread_verdicts(raw: np.ndarray, exact: bool) -> tuple:
 
 def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme.UNPROTECTED,
             faults: Sequence[FaultSpec] = (), dtype: DType | None = None, *, ck_split: bool = True,
-            tile_n: int = 0) -> ExecutionReport:
+            tile_n: int = 0, ck_source: str = "auto") -> ExecutionReport:
     """Run the protected GEMM under ``scheme`` with optional injected faults.
 
     Output is fp32 (int64 in exact-int mode) and identical across schemes for
@@ -146,10 +146,20 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
         ntr, ntc = padded.m // tiling.thread_m, padded.n // tiling.thread_n
         verdicts = t.empty(ntr * ntc * _TV_DTYPE.itemsize, dtype=t.uint8, device="cuda")
     out_sum = t.zeros(1, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
+    if ck_source not in ("auto", "onchip", "offline"):
+        raise ValueError(f"ck_source must be 'auto', 'onchip' or 'offline', got {ck_source!r}")
+    split = ck_split and not dtype.is_exact
+    call = dict(out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
+                m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
+                out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n)
+    ckr = None
+    if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED) and ck_source != "onchip":
+        plan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
+                            plan_only=True, **call)
+        if ck_source == "offline" or plan["ck_offline_recommended"]:
+            ckr = kernels.ck_rows(bt_dev, n, k, dtype, plan, tiling.thread_n, split)
     kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
-                 out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
-                 m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
-                 out_sum=out_sum, verdicts=verdicts, ck_split=ck_split and not dtype.is_exact, tile_n=tile_n)
+                 ck_rows=ckr, **call)
     if scheme is Scheme.GLOBAL_ABFT:
         colck = D.colck_device(a_dev, m, dtype)
         rowck = t.empty(bt_dev.shape[1], dtype=t.float32, device="cuda")

@@ -128,8 +128,9 @@ def test_unprotected_gemm_matches_torch(P, m, n, k):
 
 
 @pytest.mark.parametrize("scheme", ["thread-one-sided", "thread-two-sided", "global-abft"])
-@pytest.mark.parametrize("m,n,k", [(2048, 512, 512), (4096, 1024, 2304)])
+@pytest.mark.parametrize("m,n,k", [(2048, 512, 512), (4096, 1024, 768), (8192, 2048, 1000)])
 def test_no_false_positives_and_detection_at_scale(P, scheme, m, n, k):
+    """Full-size property test (K < 1024 so that r*K < 1 and a fault is detectable)."""
     import torch
     sch = P.Scheme(scheme)
     g = torch.Generator(device="cuda").manual_seed(7)
@@ -138,18 +139,64 @@ def test_no_false_positives_and_detection_at_scale(P, scheme, m, n, k):
     tiling = P.TilingConfig()
     clean = P.execute(a, b, tiling, sch)
     assert clean.detected is False
-    # tau of the responsible check, then a fault 20x above it
+    row, col = m // 2 + 3, n // 3 + 1
     if sch is P.Scheme.GLOBAL_ABFT:
-        tau = clean.verdicts[0].tolerance_used
+        v = clean.verdicts[0]
+        lhs = max(abs(v.lhs), abs(v.rhs))
     else:
-        tau = max(v.tolerance_used for v in clean.verdicts)
-    faulty = P.execute(a, b, tiling, sch, [P.OutputFault(row=m // 2 + 3, col=n // 3 + 1, delta=20 * tau + 1)])
+        v = clean.verdicts[(row // 16) * (n // 8) + col // 8]
+        lhs = v.tolerance_used / (2.0 ** -10 * k)        # max(|lhs|,|rhs|,1) of the worst row
+    # the tolerance grows with |rhs| (which includes the fault): pick delta well past the fixed point
+    rk = 2.0 ** -10 * k
+    delta = 3.0 * (rk * (lhs + 64.0)) / (1.0 - rk) + 64.0
+    faulty = P.execute(a, b, tiling, sch, [P.OutputFault(row=row, col=col, delta=delta)])
     assert faulty.detected is True
     if sch is not P.Scheme.GLOBAL_ABFT:
         fired = [(v.thread_row, v.thread_col) for v in faulty.verdicts if v.detected]
-        assert fired == [((m // 2 + 3) // 16, (n // 3 + 1) // 8)]
-    diff = (faulty.output - clean.output)
-    assert float(diff[m // 2 + 3, n // 3 + 1]) == pytest.approx(20 * tau + 1, rel=1e-6)
+        assert fired == [(row // 16, col // 8)]
+    diff = faulty.output - clean.output
+    assert float(diff[row, col]) == pytest.approx(delta, rel=1e-5)
+    assert float(diff.abs().sum()) == pytest.approx(delta, rel=1e-5)
+
+
+def test_reference_tolerance_is_vacuous_for_k_at_least_1024(P):
+    """tau = 2^-10 K max(|lhs|,|rhs|,1) >= |delta| once K >= 1024 (checksum.py:143-148):
+    no single fault is detectable — on the reference and, by parity, here."""
+    import torch
+    m, n, k = 1024, 512, 2304
+    a = (torch.rand((m, k), device="cuda") - 0.5).half()
+    b = (torch.rand((k, n), device="cuda") - 0.5).half()
+    for sch in (P.Scheme.THREAD_ONE_SIDED, P.Scheme.GLOBAL_ABFT):
+        for delta in (1.0, 1e3, 1e6):
+            rep = P.execute(a, b, P.TilingConfig(), sch, [P.OutputFault(row=5, col=7, delta=delta)])
+            assert rep.detected is False
+
+
+@pytest.mark.parametrize("source", ["onchip", "offline"])
+@pytest.mark.parametrize("tiling", [dict(thread_m=16, thread_n=8), dict(thread_m=6, thread_n=6, warp_m=24, warp_n=24,
+                                                                        tb_m=48, tb_n=48, k_step=3),
+                                    dict(thread_m=32, thread_n=16, warp_m=64, warp_n=64)])
+def test_checksum_sources_agree(P, source, tiling):
+    """On-chip and offline checksum rows give the same verdicts (same fp32 sum order)."""
+    rng = np.random.default_rng(11)
+    a = rng.integers(-8, 9, size=(700, 200), dtype=np.int64)
+    b = rng.integers(-8, 9, size=(200, 300), dtype=np.int64)
+    t = P.TilingConfig(**tiling)
+    faults = [P.OutputFault(row=5, col=7, delta=3), P.OutputFault(row=650, col=290, delta=-11)]
+    out_ref, v_ref = O.execute(a, b, O.Tiling(tb_m=t.tb_m, tb_n=t.tb_n, thread_m=t.thread_m, thread_n=t.thread_n,
+                                              k_step=t.k_step), "thread-one-sided",
+                               [("output", 5, 7, 3), ("output", 650, 290, -11)])
+    for scheme in (P.Scheme.THREAD_ONE_SIDED, P.Scheme.THREAD_TWO_SIDED):
+        rep = P.execute(a, b, t, scheme, faults, ck_source=source)
+        assert np.array_equal(rep.output, out_ref)
+        fired = [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected]
+        assert fired == [(v.thread_row, v.thread_col) for v in v_ref if v.detected]
+    xf = rng.uniform(-1, 1, size=(600, 320)).astype(np.float16)
+    wf = rng.uniform(-1, 1, size=(320, 256)).astype(np.float16)
+    r1 = P.execute(xf, wf, t, P.Scheme.THREAD_ONE_SIDED, ck_source="onchip")
+    r2 = P.execute(xf, wf, t, P.Scheme.THREAD_ONE_SIDED, ck_source="offline")
+    assert [(v.detected, v.max_abs_diff, v.tolerance_used) for v in r1.verdicts] == \
+           [(v.detected, v.max_abs_diff, v.tolerance_used) for v in r2.verdicts]
 
 
 def test_bf16_path(P):
