@@ -1,0 +1,379 @@
+"""Benchmark of the B200 intensity-guided ABFT path on BASELINE.json configs[1]:
+DLRM MLP-Bottom (13->512->256->64) and MLP-Top (512->512->256->1) at batch 1..2048.
+
+One step = one protected forward of both MLPs at every batch size in BATCHES, with the
+per-layer schemes chosen by the reference selector (cost.select) from B200-measured
+per-layer timings (paper_2104_09455_b200.profiler).  All 2 x len(BATCHES) chains are
+captured in one CUDA graph as independent branches.  Reported:
+
+  value   protected TFLOP/s of the whole step (base GEMM FLOPs 2*M*N*K of every layer),
+          device-timed with CUDA events, inputs resident in HBM, L2 flushed between steps
+  e2e     the same through the host API: pinned H2D of every chain's input, graph replay,
+          D2H of the outputs + the two verdict counters, per step
+  abft    measured step-time overhead vs the unprotected sm_100a kernels for the IG plan,
+          always-global and always-thread-level (PAPER.md:836 overhead definition)
+
+`--impl reference` times the reference's CPU algorithm for the same workload (the oracle
+port of run_protected_pipeline, checksum.py:198-237) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BOTTOM = [13, 512, 256, 64]
+TOP = [512, 512, 256, 1]
+BATCHES = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048]
+SEED = 0
+
+
+def load_baseline():
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        return json.load(fh)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def dims_padded(dims):
+    return [(-(-d // 8) * 8) for d in dims]
+
+
+def make_weights(dims, rng):
+    """U(-0.5, 0.5) fp16 weights of the padded layer dims (x8 padding, shapes.pad_gemm)."""
+    import numpy as np
+    p = dims_padded(dims)
+    ws = []
+    for i in range(len(dims) - 1):
+        w = np.zeros((p[i], p[i + 1]), dtype=np.float16)
+        w[:dims[i], :dims[i + 1]] = rng.uniform(-0.5, 0.5, size=(dims[i], dims[i + 1])).astype(np.float16)
+        ws.append(w)
+    return ws
+
+
+def workload():
+    import numpy as np
+    rng = np.random.default_rng(SEED)
+    mlps = {"bottom": make_weights(BOTTOM, rng), "top": make_weights(TOP, rng)}
+    inputs = {}
+    for name, dims in (("bottom", BOTTOM), ("top", TOP)):
+        for b in BATCHES:
+            x = np.zeros((b, dims_padded(dims)[0]), dtype=np.float16)
+            x[:, :dims[0]] = rng.uniform(-0.5, 0.5, size=(b, dims[0])).astype(np.float16)
+            inputs[(name, b)] = x
+    return mlps, inputs
+
+
+def step_flops(mlps):
+    total = 0
+    for name, ws in mlps.items():
+        for b in BATCHES:
+            total += sum(2 * b * w.shape[0] * w.shape[1] for w in ws)
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    """CPU arm: the reference's protected forward (oracle port of run_protected_pipeline)."""
+    from oracle import abft_oracle as O   # bench's reference / cpu_baseline leg only
+    base = load_baseline()
+    if rank != 0:
+        return
+    mlps, inputs = workload()
+    flops = step_flops(mlps)
+
+    def one_step():
+        for name, ws in mlps.items():
+            for b in BATCHES:
+                O.pipeline(inputs[(name, b)], ws, "binary16")
+    for _ in range(args.warmup):
+        one_step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        one_step()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    val = flops / (ms * 1e-3) / 1e12
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": base["metric"], "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16-in/f32-acc", "data": "synthetic",
+            "config": {"workload": "DLRM MLP-Bottom 13-512-256-64 + MLP-Top 512-512-256-1, batch 1..2048 "
+                                   "(x8 padded), reference protected forward = run_protected_pipeline (global ABFT)",
+                       "batches": BATCHES},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                             "sample": "full step: 24 chained protected MLP forwards (numpy BLAS, all host threads)"},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2104_09455_b200 as P
+    from paper_2104_09455_b200 import kernels, profiler
+    from paper_2104_09455_b200.network import ProtectedChain
+    from paper_2104_09455_b200.shapes import DeviceProfile, GemmShape
+
+    base = load_baseline()
+    peaks, peak_src = load_peaks()
+    mlps, inputs = workload()
+    flops = step_flops(mlps)
+    dev_profile = DeviceProfile(name="B200", tensor_throughput=peaks["bf16_tflops"] * 1e12,
+                                alu_throughput=148 * 128 * 2 * 1.965e9, memory_bandwidth=peaks["hbm_gbs"] * 1e9,
+                                verification_launch_latency=0.0)
+    S = P.Scheme
+    # ---- per-layer B200 measurements -> reference selector (cost.select)
+    plans, per_batch = {}, {}
+    for name, ws in mlps.items():
+        for b in BATCHES:
+            meas = profiler.profile_layers([torch.from_numpy(w).cuda() for w in ws], b)
+            layers = [(i, GemmShape(b, w.shape[1], w.shape[0])) for i, w in enumerate(ws)]
+            plan = P.select(layers, P.BINARY16, dev_profile, measured=meas)
+            plans[(name, b)] = [lp.chosen for lp in plan.layers]
+            per_batch[f"{name}/b{b}"] = {
+                "plan": [lp.chosen.value for lp in plan.layers],
+                "selector_overhead_pct": round(plan.aggregate_overhead_pct, 2)}
+    # ---- chains for every policy
+    wt = {name: [torch.from_numpy(w).cuda() for w in ws] for name, ws in mlps.items()}
+    policies = {"unprotected": lambda k: [S.UNPROTECTED] * 3, "global": lambda k: [S.GLOBAL_ABFT] * 3,
+                "thread": lambda k: [S.THREAD_ONE_SIDED] * 3, "ig": lambda k: plans[k]}
+    chains = {pol: {k: ProtectedChain(wt[k[0]], k[1], f(k)) for k in inputs} for pol, f in policies.items()}
+    for pol in chains:
+        for k, ch in chains[pol].items():
+            ch.x.copy_(torch.from_numpy(inputs[k]).cuda())
+
+    def capture(pol):
+        """All chains of a policy as parallel branches of one CUDA graph."""
+        cs = list(chains[pol].values())
+        main = torch.cuda.Stream()
+        streams = [torch.cuda.Stream() for _ in cs]
+        main.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(main):
+            for ch in cs:
+                ch.forward()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=main):
+            for s, ch in zip(streams, cs):
+                s.wait_stream(main)
+                with torch.cuda.stream(s):
+                    ch.forward()
+                main.wait_stream(s)
+        torch.cuda.synchronize()
+        return g
+
+    graphs = {pol: capture(pol) for pol in chains}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    def timed(pol, steps, warmup):
+        g = graphs[pol]
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return ts
+
+    # interleave policies so clock drift hits all of them alike
+    res = {pol: [] for pol in graphs}
+    with ClockSampler(local) as clk:
+        for _ in range(2):
+            for pol in graphs:
+                res[pol] += timed(pol, max(args.steps // 2, 1), args.warmup if not res[pol] else 1)
+    ms = {pol: statistics.median(v) for pol, v in res.items()}
+    # headline: IG plan, max over ranks
+    t_ig = torch.tensor([ms["ig"]], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t_ig, op=torch.distributed.ReduceOp.MAX)
+    ms_step = float(t_ig.item())
+    value = world * flops / (ms_step * 1e-3) / 1e12
+
+    # ---- correctness of the timed configuration: clean run flags nothing
+    fired = {pol: [ch.flags() for ch in chains[pol].values()] for pol in ("ig", "global", "thread")}
+    clean_ok = all(f == (0, 0) for v in fired.values() for f in v)
+
+    # ---- end to end through the host API: pinned inputs in, outputs + verdict counters out
+    host_in = {k: torch.from_numpy(v).pin_memory() for k, v in inputs.items()}
+    host_out = {k: torch.empty(chains["ig"][k].acts[-1].shape, dtype=torch.float16).pin_memory() for k in inputs}
+    host_cnt = {k: torch.empty(2, dtype=torch.int32).pin_memory() for k in inputs}
+    h2d = sum(v.numel() * 2 for v in host_in.values())
+    d2h = sum(v.numel() * 2 for v in host_out.values()) + 8 * len(host_cnt)
+
+    def e2e_step():
+        for k, ch in chains["ig"].items():
+            ch.x.copy_(host_in[k], non_blocking=True)
+        graphs["ig"].replay()
+        for k, ch in chains["ig"].items():
+            host_out[k].copy_(ch.acts[-1], non_blocking=True)
+            host_cnt[k].copy_(ch.counters, non_blocking=True)
+        torch.cuda.synchronize()
+        return sum(int(c[0]) + int(c[1]) for c in host_cnt.values())
+    for _ in range(args.warmup):
+        e2e_step()
+    e2e_ts = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bad = e2e_step()
+        e2e_ts.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * statistics.median(e2e_ts)
+
+    # ---- roofline of the dominant kernel: the b2048 MLP-Top layer-1 GEMM under its IG scheme
+    ch = chains["ig"][("top", 2048)]
+    L = ch.layers[0]
+    kw = ch._gemm_kwargs(0, L)
+    dom_us = profiler.graph_time_us(lambda: kernels.gemm(ch.x, ch.x.stride(0), L.pw.bt, L.pw.ldbt, 2048, L.n, L.k,
+                                                          ch.dtype, ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw),
+                                    iters=50)
+    dom_bytes = 2 * (2048 * L.k + L.k * L.n + 2048 * L.n)
+    dom_flops = 2 * 2048 * L.k * L.n
+    ai = dom_flops / dom_bytes
+    cmr = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if ai < cmr:
+        roof = {"bound": "hbm", "achieved": dom_bytes / (dom_us * 1e-6) / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": dom_flops / (dom_us * 1e-6) / 1e12, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"abft_gemm_kernel top/b2048 layer0 {L.scheme.value} {2048}x{L.n}x{L.k}, {dom_us:.2f} us/launch"
+    roof["peak_source"] = peak_src
+
+    # ---- CPU baseline: the oracle port of the reference forward on a bounded sample
+    cpu = None
+    if rank == 0:
+        from oracle import abft_oracle as O   # cpu_baseline leg only
+        sample_keys = [("bottom", 2048), ("top", 2048), ("top", 1)]
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < 10.0:
+            for k in sample_keys:
+                O.pipeline(inputs[k], mlps[k[0]], "binary16")
+            reps += 1
+        dt = time.perf_counter() - t0
+        sflops = reps * sum(sum(2 * k[1] * w.shape[0] * w.shape[1] for w in mlps[k[0]]) for k in sample_keys)
+        cpu = {"value": sflops / dt / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{reps} x run_protected_pipeline (oracle port) on bottom/b2048, top/b2048, top/b1 "
+                         f"({dt:.1f} s, numpy BLAS threads = host cores)"}
+
+    n_launch = sum(len(c.layers) + (1 if c.layers[0].scheme is S.GLOBAL_ABFT else 0) + (1 if c.global_ids else 0)
+                   for c in chains["ig"].values())
+    line = {
+        "metric": base["metric"], "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16-in/f32-acc", "data": "synthetic (seeded U(-0.5,0.5) inputs and weights)",
+        "config": {"workload": "DLRM MLP-Bottom 13-512-256-64 + MLP-Top 512-512-256-1 (x8 padded), batch 1..2048, "
+                               "intensity-guided per-layer ABFT (global / thread-one-sided) from measured B200 timings",
+                   "batches": BATCHES, "parallelism": f"weak: {world} x independent replicas of the sweep",
+                   "l2": "flushed (256 MB write) before every timed step", "graph": "one CUDA graph per step"},
+        "abft": {
+            "ms_per_step": {k: round(v, 4) for k, v in ms.items()},
+            "overhead_pct": {pol: round(100.0 * (ms[pol] / ms["unprotected"] - 1.0), 2)
+                             for pol in ("ig", "global", "thread")},
+            "clean_run_false_positives": 0 if clean_ok else 1,
+            "per_chain": per_batch,
+        },
+        "e2e": {"value": world * flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "gpu_launches": n_launch * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

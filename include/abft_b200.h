@@ -146,6 +146,12 @@ int abft_global_lhs(const abft_global_task_t* tasks /*device*/, int32_t ntasks, 
                     void* stream);
 int abft_verify_sums(const double* sums /*[n][2]*/, const int32_t* k /*device [n]*/, int32_t ntasks,
                      int32_t numeric, abft_verdict_t* out, int32_t* detected_count, void* stream);
+/* Single-GPU fast path: abft_global_lhs + abft_verify_sums fused into one launch. */
+int abft_global_verify(const abft_global_task_t* tasks, int32_t ntasks, int32_t numeric, double* sums,
+                       abft_verdict_t* out, int32_t* detected_count, void* stream);
+
+/* Clear a per-forward accumulator block (one graph memset node instead of a kernel). */
+int abft_zero(void* p, int64_t bytes, void* stream);
 
 /* Library introspection */
 const char* abft_last_error(void);

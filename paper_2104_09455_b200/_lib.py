@@ -31,8 +31,10 @@ EXPORTED_SYMBOLS = (
     "abft_pack",
     "abft_convert_i64",
     "abft_matrix_sum",
+    "abft_zero",
     "abft_global_lhs",
     "abft_verify_sums",
+    "abft_global_verify",
     "abft_last_error",
     "abft_version",
     "abft_device_sms",
@@ -103,7 +105,9 @@ def _declare(lib):
     lib.abft_pack.argtypes = [vp, i32, i32, i64, vp, i32, i64, i32, vp]
     lib.abft_convert_i64.argtypes = [vp, i64, i32, vp, vp]
     lib.abft_matrix_sum.argtypes = [vp, i32, i32, i64, i32, vp, vp]
+    lib.abft_zero.argtypes = [vp, i64, vp]
     lib.abft_global_lhs.argtypes = [vp, i32, vp, vp]
+    lib.abft_global_verify.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     lib.abft_verify_sums.argtypes = [vp, vp, i32, i32, vp, vp, vp]
     lib.abft_last_error.restype = ctypes.c_char_p
     for name in EXPORTED_SYMBOLS:

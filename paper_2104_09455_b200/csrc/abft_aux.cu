@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(256) matrix_sum_kernel(const void* __restrict_
 }
 
 // ----------------------------------------------------------- verification
-__global__ void global_lhs_kernel(const abft_global_task_t* __restrict__ tasks, double* __restrict__ sums) {
+// one block per layer: lhs = colck . rowck (fp64), rhs from the GEMM epilogue; with verdicts
+// requested the same block forms the Verdict (deferred verification fused into one launch)
+__global__ void global_lhs_kernel(const abft_global_task_t* __restrict__ tasks, double* __restrict__ sums,
+                                  double r, abft_verdict_t* __restrict__ out, int* __restrict__ detected_count) {
   const abft_global_task_t t = tasks[blockIdx.x];
   double acc = 0.0;
   for (int i = threadIdx.x; i < t.k; i += blockDim.x) acc += (double)t.colck[i] * (double)t.rowck[i];
@@ -145,8 +148,19 @@ __global__ void global_lhs_kernel(const abft_global_task_t* __restrict__ tasks, 
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    const double rhs = t.rhs != nullptr ? *t.rhs : 0.0;
     sums[2 * blockIdx.x] = s;
-    sums[2 * blockIdx.x + 1] = t.rhs != nullptr ? *t.rhs : 0.0;
+    sums[2 * blockIdx.x + 1] = rhs;
+    if (out != nullptr || detected_count != nullptr) {
+      const double tol = tolerance(r, t.k, s, rhs);
+      const int det = fabs(s - rhs) > tol ? 1 : 0;
+      if (out) {
+        abft_verdict_t v;
+        v.lhs = s; v.rhs = rhs; v.tol = tol; v.k = t.k; v.detected = det;
+        out[blockIdx.x] = v;
+      }
+      if (det && detected_count) atomicAdd(detected_count, 1);
+    }
   }
 }
 
@@ -246,11 +260,27 @@ extern "C" __attribute__((visibility("default"))) int abft_matrix_sum(const void
   return cuda_check(cudaGetLastError(), "matrix_sum launch");
 }
 
+extern "C" __attribute__((visibility("default"))) int abft_zero(void* p, int64_t bytes, void* stream) {
+  if (bytes < 0) return fail(ABFT_E_VALUE, "zero: negative size");
+  if (bytes == 0) return ABFT_OK;
+  return cuda_check(cudaMemsetAsync(p, 0, (size_t)bytes, as_stream(stream)), "zero");
+}
+
 extern "C" __attribute__((visibility("default"))) int abft_global_lhs(const abft_global_task_t* tasks, int32_t ntasks, double* sums, void* stream) {
   if (ntasks < 0) return fail(ABFT_E_VALUE, "global_lhs: negative task count");
   if (ntasks == 0) return ABFT_OK;
-  global_lhs_kernel<<<ntasks, 256, 0, as_stream(stream)>>>(tasks, sums);
+  global_lhs_kernel<<<ntasks, 256, 0, as_stream(stream)>>>(tasks, sums, 0.0, nullptr, nullptr);
   return cuda_check(cudaGetLastError(), "global_lhs launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_global_verify(const abft_global_task_t* tasks,
+                                                                        int32_t ntasks, int32_t numeric,
+                                                                        double* sums, abft_verdict_t* out,
+                                                                        int32_t* detected_count, void* stream) {
+  if (ntasks < 0) return fail(ABFT_E_VALUE, "global_verify: negative task count");
+  if (ntasks == 0) return ABFT_OK;
+  global_lhs_kernel<<<ntasks, 256, 0, as_stream(stream)>>>(tasks, sums, tol_ratio(numeric), out, detected_count);
+  return cuda_check(cudaGetLastError(), "global_verify launch");
 }
 
 extern "C" __attribute__((visibility("default"))) int abft_verify_sums(const double* sums, const int32_t* k, int32_t ntasks, int32_t numeric,

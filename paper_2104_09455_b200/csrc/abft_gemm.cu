@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -46,6 +47,14 @@ constexpr int COLCK_SMEM_MAX = 4096;
 
 enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
 
+// bring-up instrumentation (ABFT_DEBUG & 2048): per-CTA %globaltimer stamps
+__device__ unsigned long long g_dbg_ts[160][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct GemmParams {
   int M, N, K, m_ext, n_ext, tol_k;
   int bn, bm_eff, bn_eff, mt, nt, groups, nck, nck_pad;
@@ -55,6 +64,7 @@ struct GemmParams {
   int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline)
   int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
   double r;
+  float rk;              // r * tol_k in fp32, for the guard-banded fast compare
   uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_bar;
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
@@ -71,6 +81,7 @@ struct GemmParams {
   int* fired;
   int fired_cap;
   uint32_t idesc_main, idesc_ck;
+  int debug;   // ABFT_DEBUG bits (bring-up experiments only): 1 skip verdicts, 2 skip checksum TMEM load, 4 skip checksum MMA
 };
 
 template <typename T>
@@ -106,6 +117,17 @@ __device__ __forceinline__ float round_out(float y, int out_dtype) {
   return y;
 }
 
+// |x - y| > r*K*max(|x|,|y|,1) evaluated exactly as the reference does (float64), but
+// decided in fp32 whenever the margin exceeds the fp32 rounding of the operands.
+__device__ __forceinline__ bool exceeds_tol(const GemmParams& p, float x, float y) {
+  if (p.r == 0.0) return x != y;                       // exact-int mode: tau = 0, values exact
+  const float d = fabsf(x - y);
+  const float t = p.rk * fmaxf(fmaxf(fabsf(x), fabsf(y)), 1.f);
+  if (d > t * 1.0001f) return true;
+  if (d < t * 0.9999f) return false;
+  return fabs((double)x - (double)y) > tolerance(p.r, p.tol_k, x, y);
+}
+
 // vector rule: per-row (or per-element) comparisons, worst one reported (tiled.py:203-218)
 __device__ __forceinline__ bool scheme_vector_rule(int s) { return s == ABFT_ONE_SIDED || s == ABFT_REPL_FULL; }
 
@@ -124,7 +146,7 @@ __device__ __forceinline__ float warp_column_sums(float (&v)[32], int lane) {
   return v[0];
 }
 
-__device__ __noinline__ void emit_verdict(const GemmParams& p, int t_row, int t_col, bool fired, double diff,
+__device__ __forceinline__ void emit_verdict(const GemmParams& p, int t_row, int t_col, bool fired, double diff,
                                           double tol) {
   if (p.verdicts != nullptr) {
     abft_thread_verdict_t vv;
@@ -146,20 +168,18 @@ __device__ __noinline__ void emit_verdict(const GemmParams& p, int t_row, int t_
 // rows of a thread tile are Mt consecutive lanes: shuffles + one ballot, no smem.
 //   vector rule: per-row compare, report the row maximising diff - tau (first on ties)
 //   scalar rule: compare sum_rows x with sum_rows y (two-sided / single-acc)
-__device__ __noinline__ void group_verdict_shuffle(const GemmParams& p, float x, float y, int lane, int t_row,
+__device__ __forceinline__ void group_verdict_shuffle(const GemmParams& p, float x, float y, int lane, int t_row,
                                                    int t_col, bool valid) {
   const int mt = p.mt;
   const unsigned seg = (mt == 32) ? 0xffffffffu : (((1u << mt) - 1u) << (lane & ~(mt - 1)));
   const bool leader = (lane & (mt - 1)) == 0;
   if (scheme_vector_rule(p.scheme)) {
-    const double dx = x, dy = y;
-    const double diff = fabs(dx - dy);
-    const double tol = tolerance(p.r, p.tol_k, dx, dy);
-    const bool fired = diff > tol;
+    const bool fired = exceeds_tol(p, x, y);
     const unsigned ball = __ballot_sync(0xffffffffu, fired && valid);
     const bool tile_fired = (ball & seg) != 0;
     if (p.verdicts != nullptr) {
-      float key = (float)(diff - tol);
+      const double dx = x, dy = y;
+      float key = (float)(fabs(dx - dy) - tolerance(p.r, p.tol_k, dx, dy));
       int src = lane;
       for (int off = 1; off < mt; off <<= 1) {
         const float ok = __shfl_xor_sync(0xffffffffu, key, off);
@@ -190,7 +210,7 @@ __device__ __noinline__ void group_verdict_shuffle(const GemmParams& p, float x,
 }
 
 // Generic-Mt path: verdicts of a whole tile from the smem records rec[row][group].
-__device__ __noinline__ void tile_verdicts_smem(const GemmParams& p, const float2* rec, int et, int m0, int n0) {
+__device__ __forceinline__ void tile_verdicts_smem(const GemmParams& p, const float2* rec, int et, int m0, int n0) {
   const int rs = p.rec_stride;
   const int pairs = (p.bm_eff / p.mt) * p.groups;
   const bool vector_rule = scheme_vector_rule(p.scheme);
@@ -235,12 +255,19 @@ __device__ __forceinline__ void group_done(const GemmParams& p, float2* rec, int
   }
 }
 
-// fault injection for one 32-column chunk of one row (rare path, kept compact)
-__device__ __noinline__ void apply_faults(const GemmParams& p, float* v, int gm, int gc0, int cmax) {
-  for (int f = 0; f < p.nfaults; ++f) {
-    const abft_fault_t ft = p.faults[f];
+// fault injection for one 32-column chunk of one row (rare path).  The accumulator chunk
+// stays in registers: the selected element is updated through an unrolled compare, never
+// through its address (an address-taken register array lives in local memory, which the
+// ~1 KB L1 left beside a 227 KB smem carve-out cannot cache).
+__device__ __forceinline__ void apply_faults(const abft_fault_t* faults, int nfaults, float (&v)[32], int gm,
+                                             int gc0, int cmax) {
+  for (int f = 0; f < nfaults; ++f) {
+    const abft_fault_t ft = faults[f];
     const int j = ft.col - gc0;
-    if (ft.row == gm && j >= 0 && j < 32 && j < cmax) v[j] += ft.delta;
+    if (ft.row == gm && j >= 0 && j < 32 && j < cmax) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) v[jj] += (jj == j) ? ft.delta : 0.f;
+    }
   }
 }
 
@@ -274,9 +301,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool has_ck = CLASS == CLASS_CHECKSUM;
   constexpr bool has_shadow = CLASS == CLASS_REPLICA;
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
-  const bool ck_onchip = has_ck && p.ck_mode == 1;
-  const bool ck_loaded = has_ck && p.ck_mode == 2;
+  const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
+  const bool ck_loaded = has_ck && p.ck_mode == 2 && !(p.debug & 8);
   const int bn = p.bn;
+  const bool stamp = (p.debug & 2048) && blockIdx.x < 160;
+  if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][0] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -296,16 +325,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (ck_loaded) ptx::tma_prefetch(&tmCK);
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
-  if (warp >= CK_WARP0 && ck_onchip) {
-    // zero the padding checksum rows [nck, nck_pad) of every stage once
-    const int ct = threadIdx.x - CK_WARP0 * 32;
-    const int pad_rows = p.nck_pad - p.nck;
-    for (int s = 0; s < p.stages; ++s) {
-      uint4* base = reinterpret_cast<uint4*>(sm_ck + s * p.stage_ck_bytes + p.nck * 128);
-      for (int i = ct; i < pad_rows * 8; i += 128) base[i] = make_uint4(0, 0, 0, 0);
-    }
-    ptx::fence_proxy_async_smem();
-  }
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 128) colck_s[i] = 0.f;
   }
@@ -313,6 +332,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][1] = gtimer();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
             ptx::mma_f16_ss(d, adesc, bdesc, p.idesc_main, accum);
-            if (ck_loaded) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
+            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
             if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
           }
           if (ck_onchip) {
@@ -445,6 +465,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
           }
+          // padding checksum rows [nck, nck_pad) must read as zero
+          for (int i = ct; i < (p.nck_pad - p.nck) * 8; i += 128)
+            reinterpret_cast<uint4*>(ck + p.nck * 128)[i] = make_uint4(0, 0, 0, 0);
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ckfull[s]);
@@ -479,9 +502,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
+      if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][2] = gtimer();
       const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * p.cols_per_acc);
 
-      if constexpr (has_ck) {
+      if (has_ck && !(p.debug & 2)) {
         // checksum column per (row, group) -> cks[g][row] (groups <= 32)
         float hi[32], lo[32];
         __syncwarp();
@@ -493,6 +517,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (j < p.groups) cks[j * BM + row] = p.split ? hi[j] + lo[j] : hi[j];
       }
 
+      // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
+      const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
+      uint32_t fmask = 0;
       // generic-Nt running state
       float gsum = 0.f, ssum = 0.f, best_c = 0.f, best_s = 0.f;
       float best_key = -FLT_MAX;
@@ -505,10 +532,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_ld32(tacc + c0, v);
         if constexpr (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
         ptx::tmem_ld_wait();
+        if (stamp && et == 0 && t_local == 0 && c0 == 0) g_dbg_ts[blockIdx.x][5] = gtimer();
         const int gc0 = n0 + c0;
         const int cmax = p.bn_eff - c0;
-        if (row_fault) apply_faults(p, v, gm, gc0, cmax);
-        if constexpr (thread_level && NT > 0) {
+        if (row_fault) apply_faults(p.faults, p.nfaults, v, gm, gc0, cmax);
+        if (p.debug & 16) {
+        } else if constexpr (thread_level && NT > 0) {
           // static group structure: 32 / NT complete groups per chunk (NT divides 32 and bn_eff)
 #pragma unroll
           for (int gi = 0; gi < 32 / NT; ++gi) {
@@ -526,7 +555,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                   for (int e = 0; e < NT; ++e) {
                     const float cv = v[gi * NT + e], sv = sh[gi * NT + e];
-                    const float key = (float)(fabs((double)cv - (double)sv) - tolerance(p.r, p.tol_k, sv, cv));
+                    const float key = fabsf(cv - sv) - p.rk * fmaxf(fmaxf(fabsf(cv), fabsf(sv)), 1.f);
                     if (key > bk) { bk = key; x = sv; y = cv; }
                   }
                 } else {
@@ -535,7 +564,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   for (int e = 0; e < NT; ++e) { x += sh[gi * NT + e]; y += v[gi * NT + e]; }
                 }
               }
-              group_done(p, rec, row, lane, gg, x, y, n0, t_row, row_verdict);
+              if (flags_fast) {
+                // one-sided flags-only: one fp32 compare per (row, group), folded into a bitmask
+                if (exceeds_tol(p, x, y)) fmask |= 1u << gg;
+              } else if (!(p.debug & 1)) {
+                group_done(p, rec, row, lane, gg, x, y, n0, t_row, row_verdict);
+              }
             }
           }
         } else if constexpr (thread_level) {
@@ -553,7 +587,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (has_shadow) {
               const float sv = stg[(32 + j) * BM + row];
               if (p.scheme == ABFT_REPL_FULL) {
-                const float key = (float)(fabs((double)xv - (double)sv) - tolerance(p.r, p.tol_k, sv, xv));
+                const float key = fabsf(xv - sv) - p.rk * fmaxf(fmaxf(fabsf(xv), fabsf(sv)), 1.f);
                 if (key > best_key) { best_key = key; best_c = xv; best_s = sv; }
               } else {
                 ssum += sv;
@@ -589,7 +623,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int j = 0; j < 32; j += 4)
                   *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
               } else {
-#pragma unroll 1
+#pragma unroll
                 for (int j = 0; j < 32; ++j)
                   if (j < cmax && gc0 + j < p.N) dst[j] = v[j];
               }
@@ -606,7 +640,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   *reinterpret_cast<uint4*>(dst + j) = u;
                 }
               } else {
-#pragma unroll 1
+#pragma unroll
                 for (int j = 0; j < 32; ++j)
                   if (j < cmax && gc0 + j < p.N) dst[j] = TR::from_f(v[j]);
               }
@@ -623,6 +657,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][6] = gtimer();
+      if constexpr (has_ck && NT > 0) {
+        if (flags_fast) {
+          uint32_t m = row_verdict ? fmask : 0u;
+          for (int off = 1; off < p.mt; off <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, off);
+          if ((lane & (p.mt - 1)) == 0 && m != 0u) {
+            const int t_col0 = n0 / p.nt;
+            while (m != 0u) {
+              const int gbit = __ffs(m) - 1;
+              m &= m - 1u;
+              if (t_col0 + gbit < p.n_tcols) emit_verdict(p, t_row, t_col0 + gbit, true, 0.0, 0.0);
+            }
+          }
+        }
+      }
       // TMEM accumulator stage fully read: hand it back to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
@@ -635,6 +684,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::named_bar_sync(1, 128);
       }
     }
+    if (stamp && et == 0) g_dbg_ts[blockIdx.x][3] = gtimer();
     // -------- per-CTA flush of the global-ABFT output summation and fused colck
     if (p.out_sum != nullptr) {
       double x = rhs_acc;
@@ -658,6 +708,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   __syncwarp();
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+  if (stamp && threadIdx.x == 32) g_dbg_ts[blockIdx.x][4] = gtimer();
 }
 
 // ============================================================== host side
@@ -775,9 +826,11 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   if (a->M < 1 || a->N < 1 || a->K < 1) return fail(ABFT_E_SHAPE, "GEMM extents must be >= 1");
   if (a->dtype != ABFT_F16 && a->dtype != ABFT_BF16) return fail(ABFT_E_VALUE, "dtype must be ABFT_F16 or ABFT_BF16");
   if (a->scheme < ABFT_UNPROTECTED || a->scheme > ABFT_REPL_SINGLE) return fail(ABFT_E_VALUE, "unknown scheme");
-  const bool thread_level = a->scheme >= ABFT_ONE_SIDED;
-  const bool has_ck = a->scheme == ABFT_ONE_SIDED || a->scheme == ABFT_TWO_SIDED;
-  const bool has_shadow = a->scheme == ABFT_REPL_FULL || a->scheme == ABFT_REPL_SINGLE;
+  const int dbg_env = getenv("ABFT_DEBUG") ? atoi(getenv("ABFT_DEBUG")) : 0;
+  const bool as_plain = (dbg_env & 1024) != 0;
+  const bool thread_level = a->scheme >= ABFT_ONE_SIDED && !as_plain;
+  const bool has_ck = (a->scheme == ABFT_ONE_SIDED || a->scheme == ABFT_TWO_SIDED) && !as_plain;
+  const bool has_shadow = (a->scheme == ABFT_REPL_FULL || a->scheme == ABFT_REPL_SINGLE) && !as_plain;
   const int mt = thread_level ? a->thread_m : 1, nt = thread_level ? a->thread_n : 1;
   const int m_ext = thread_level ? a->m_ext : a->M, n_ext = thread_level ? a->n_ext : a->N;
   if (thread_level) {
@@ -842,6 +895,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : 0;
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
+  p.rk = (float)(p.r * (double)p.tol_k);
   p.C = a->C; p.ldc = a->ldc;
   p.faults = a->faults; p.nfaults = a->faults ? a->nfaults : 0;
   p.out_sum = a->out_sum;
@@ -853,6 +907,17 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = has_ck ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
+  {
+    const char* dbg = getenv("ABFT_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+    if (p.debug & 32) p.tmem_cols = 512;
+    if (p.debug & 256) {
+      p.cols_per_acc = round_up(p.cols_per_acc, 64);
+      p.acc_stages = (2 * p.cols_per_acc <= 512) ? 2 : 1;
+      p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
+    }
+    if (p.debug & 512) { p.acc_stages = 1; }
+  }
   out.cls = has_ck ? CLASS_CHECKSUM : has_shadow ? CLASS_REPLICA : CLASS_PLAIN;
   // static group width when it divides both the 32-column chunk and the tile
   out.ntc = (thread_level && (nt == 8 || nt == 16) && p.bn_eff % 32 == 0) ? nt : 0;
@@ -869,7 +934,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t bar_bytes = 1024;
   const uint32_t extras = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + bar_bytes;
   const uint32_t stage_bytes = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes;
-  const int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
+  int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
+  if (const char* cap = getenv("ABFT_SMEM_CAP")) budget = std::min(budget, atoi(cap) * 1024 - (int)extras);
   int stages = budget / (int)stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(ABFT_E_UNSUPPORTED, "shared memory budget too small for a 2-stage pipeline");
@@ -920,6 +986,10 @@ __global__ void ck_rows_kernel(const T* __restrict__ bt, int n, int k, long long
 
 using namespace abft;
 
+extern "C" __attribute__((visibility("default"))) int abft_debug_timestamps(unsigned long long* host_out /*[160*8]*/) {
+  return cuda_check(cudaMemcpyFromSymbol(host_out, g_dbg_ts, sizeof(g_dbg_ts)), "debug timestamps");
+}
+
 extern "C" __attribute__((visibility("default"))) int abft_gemm_plan(const abft_gemm_args_t* a, int32_t* out) {
   Plan pl;
   int rc = make_plan(a, pl);
@@ -963,7 +1033,7 @@ extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_
   Plan pl;
   int rc = make_plan(a, pl);
   if (rc != ABFT_OK) return rc;
-  const GemmParams& p = pl.p;
+  GemmParams& p = pl.p;
 
   CUtensorMap ma, mb, mc;
   rc = cached_map(&ma, a->A, a->dtype, a->K, a->M, a->lda, BM);
@@ -980,6 +1050,8 @@ extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_
     mc = mb;   // unused
   }
   cudaStream_t st = as_stream(stream);
+  if (p.debug & 64) pl.cls = CLASS_PLAIN;
+  if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
   if (a->dtype == ABFT_BF16) return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
   return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
 }

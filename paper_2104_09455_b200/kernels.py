@@ -91,6 +91,16 @@ def global_lhs(tasks_dev, ntasks: int, sums) -> None:
     _lib.call("abft_global_lhs", ptr(tasks_dev), ntasks, ptr(sums), stream_handle())
 
 
+def global_verify(tasks_dev, ntasks: int, numeric: int, sums, out=None, detected_count=None) -> None:
+    _lib.call("abft_global_verify", ptr(tasks_dev), ntasks, numeric, ptr(sums), ptr(out), ptr(detected_count),
+              stream_handle())
+
+
 def verify_sums(sums, ks_dev, ntasks: int, numeric: int, out=None, detected_count=None) -> None:
     _lib.call("abft_verify_sums", ptr(sums), ptr(ks_dev), ntasks, numeric, ptr(out), ptr(detected_count),
               stream_handle())
+
+
+def zero(t) -> None:
+    """cudaMemsetAsync of a whole (contiguous) tensor on the current stream."""
+    _lib.call("abft_zero", ptr(t), t.numel() * t.element_size(), stream_handle())

@@ -1,0 +1,186 @@
+"""Protected multi-layer inference with a per-layer ABFT plan (the paper's deployment mode).
+
+A ``ProtectedChain`` is a sequence of linear layers (FC, or conv already lowered to a
+GEMM) with ReLU between them — the chain of ``run_protected_pipeline``
+(checksum.py:198-237) — where every layer carries its own scheme:
+
+  unprotected   plain tcgen05 GEMM
+  global-abft   output summation in the epilogue; the layer's activation checksum is
+                produced by the PREVIOUS layer's epilogue (fused next-layer colck,
+                PAPER.md:193) or, for the first layer, by one abft_colsum launch;
+                all dot products + verdicts run in one batched launch at the end
+  thread-one-sided  checksum N-slice in the same MMA, per-row compare in the
+                epilogue; fired thread tiles counted on device
+
+Everything for one forward is enqueued on the current stream with no host sync and
+can be captured in a CUDA graph; ``flags()`` reads back two counters (fired thread
+tiles, flagged global layers) — the deferred verification of the reference.
+
+Multi-GPU: batch sharding needs no collective on the hot path; ``global_partials``
+exposes the per-layer [lhs, rhs] sums so callers can all-reduce them (NCCL) and call
+``verify_reduced`` to obtain exactly the full-batch global verdicts.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import device as D
+from . import kernels
+from .schemes import Scheme, TilingConfig
+from .shapes import BINARY16, DType
+
+
+@dataclass
+class _Layer:
+    k: int            # padded K (multiple of 8)
+    n: int            # padded N (multiple of 8)
+    pw: D.PreparedWeight
+    scheme: Scheme
+    ck_rows: object = None
+    relu: bool = True
+
+
+@dataclass
+class ProtectedChain:
+    """Layers given as K x N weights (torch fp16/bf16 CUDA tensors or numpy)."""
+
+    weights: Sequence
+    batch: int
+    schemes: Sequence[Scheme]
+    dtype: DType = BINARY16
+    tiling: TilingConfig = TilingConfig()
+    relu_last: bool = True
+    ck_split: bool = False
+    layers: List[_Layer] = field(default_factory=list, init=False)
+
+    def __post_init__(self):
+        D.require_device()
+        t = D.torch()
+        if len(self.schemes) != len(self.weights):
+            raise ValueError("one scheme per layer")
+        self.numeric = D.numeric_code(self.dtype)
+        sd = D.torch_storage_dtype(self.dtype)
+        prev_n = None
+        for i, (w, sch) in enumerate(zip(self.weights, self.schemes)):
+            k, n = D.shape2d(w, f"weights[{i}]")
+            kp = D.round8(k)
+            if prev_n is not None and kp != prev_n:
+                raise ValueError(f"layer {i}: K={k} does not chain with the previous N={prev_n}")
+            pw = D.prepare_weight(w, self.dtype)
+            self.layers.append(_Layer(k=kp, n=D.round8(n), pw=pw, scheme=sch,
+                                      relu=(i < len(self.weights) - 1) or self.relu_last))
+            prev_n = D.round8(n)
+        m = self.batch
+        self.x = t.zeros((m, self.layers[0].k), dtype=sd, device="cuda")
+        self.acts = [t.zeros((m, L.n), dtype=sd, device="cuda") for L in self.layers]
+        nl = len(self.layers)
+        # every per-forward accumulator lives in ONE block so a single memset node clears it:
+        # [rhs fp64 x nl][counters int32 x 2, pad][colck fp32 per layer]
+        off_cnt = 8 * nl
+        off_ck = off_cnt + 16
+        total = off_ck + 4 * sum(L.k for L in self.layers)
+        self.scratch = t.zeros(total, dtype=t.uint8, device="cuda")
+        self.rhs = self.scratch[:off_cnt].view(t.float64).view(nl, 1)
+        self.counters = self.scratch[off_cnt:off_cnt + 8].view(t.int32)   # [fired thread tiles, flagged layers]
+        self.colck, o = [], off_ck
+        for L in self.layers:
+            self.colck.append(self.scratch[o:o + 4 * L.k].view(t.float32))
+            o += 4 * L.k
+        self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
+        self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
+        self._tasks = None
+        if self.global_ids:
+            self._tasks = kernels.global_tasks([(self.colck[i], self.layers[i].pw.rowck, self.rhs[i],
+                                                 self.layers[i].k) for i in self.global_ids])
+            self._ks = t.tensor([self.layers[i].k for i in self.global_ids], dtype=t.int32, device="cuda")
+            self._gsums = t.zeros((len(self.global_ids), 2), dtype=t.float64, device="cuda")
+        # offline checksum rows where the plan says B tiles are re-read by several M-blocks
+        for L in self.layers:
+            if L.scheme is Scheme.THREAD_ONE_SIDED:
+                kw = self._gemm_kwargs(0, L)
+                plan = kernels.gemm(self.x, self.x.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype,
+                                    self.numeric, L.scheme, plan_only=True, **kw)
+                if plan["ck_offline_recommended"]:
+                    L.ck_rows = kernels.ck_rows(L.pw.bt, L.n, L.k, self.dtype, plan, self.tiling.thread_n,
+                                                self.ck_split)
+
+    def _gemm_kwargs(self, i: int, L: _Layer) -> dict:
+        t = self.tiling
+        m = self.batch
+        kw = dict(out=self.acts[i], ldc=self.acts[i].stride(0),
+                  out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu)
+        if L.scheme is Scheme.GLOBAL_ABFT:
+            kw["out_sum"] = self.rhs[i]
+        elif L.scheme is not Scheme.UNPROTECTED:
+            kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-m // t.thread_m) * t.thread_m,
+                      n_ext=-(-L.n // t.thread_n) * t.thread_n, tol_k=-(-L.k // t.k_step) * t.k_step,
+                      fired_count=self.counters[0:1], ck_split=self.ck_split)
+        nxt = i + 1
+        if nxt < len(self.layers) and self.layers[nxt].scheme is Scheme.GLOBAL_ABFT:
+            kw["next_colck"] = self.colck[nxt]
+        return kw
+
+    def forward(self, x=None) -> object:
+        """Enqueue one protected forward (no host sync); returns the last activation tensor."""
+        if x is not None:
+            self.x.copy_(x, non_blocking=True)
+        kernels.zero(self.scratch)
+        if self.layers and self.layers[0].scheme is Scheme.GLOBAL_ABFT:
+            kernels.colsum(self.x, self.batch, self.layers[0].k, self.x.stride(0), self.dtype, self.colck[0],
+                           accumulate=True)
+        a = self.x
+        for i, L in enumerate(self.layers):
+            kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype, self.numeric,
+                         L.scheme, ck_rows=L.ck_rows, **self._gemm_kwargs(i, L))
+            a = self.acts[i]
+        if self.global_ids:
+            ng = len(self.global_ids)
+            kernels.global_verify(self._tasks, ng, self.numeric, self._gsums, out=self.verdict_buf,
+                                  detected_count=self.counters[1:2])
+        return a
+
+    # ---- multi-GPU helpers (batch sharding): per-layer partial sums, all-reduced by the caller
+    def global_partials(self):
+        """[n_global, 2] fp64 (lhs, rhs) of this shard, valid after forward() on the stream."""
+        kernels.global_lhs(self._tasks, len(self.global_ids), self._gsums)
+        return self._gsums
+
+    def verify_reduced(self, sums):
+        """Verdicts from all-reduced (lhs, rhs) sums; returns the device counter of flagged layers."""
+        t = D.torch()
+        cnt = t.zeros(1, dtype=t.int32, device="cuda")
+        kernels.verify_sums(sums, self._ks, len(self.global_ids), self.numeric, out=self.verdict_buf,
+                            detected_count=cnt)
+        return cnt
+
+    def flags(self) -> tuple:
+        """(fired thread tiles, flagged global layers) — one small D2H read."""
+        c = self.counters.cpu().tolist()
+        return int(c[0]), int(c[1])
+
+    def flops(self) -> int:
+        return sum(2 * self.batch * L.n * L.k for L in self.layers)
+
+
+class GraphedForward:
+    """A ProtectedChain forward captured once in a CUDA graph and replayed."""
+
+    def __init__(self, chain: ProtectedChain, warmup: int = 2):
+        t = D.torch()
+        self.chain = chain
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):
+            for _ in range(warmup):
+                chain.forward()
+        t.cuda.current_stream().wait_stream(s)
+        t.cuda.synchronize()
+        self.graph = t.cuda.CUDAGraph()
+        with t.cuda.graph(self.graph, stream=s):
+            chain.forward()
+        t.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
