@@ -254,9 +254,11 @@ def main():
             if world > 1:
                 torch.distributed.barrier()
             torch.cuda.synchronize()
+            torch.cuda.nvtx.range_push(f"timed_{pol}")   # ncu --nvtx-include "timed_ig/" selects these launches
             e0.record()
             g.replay()
             e1.record()
+            torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         return ts

@@ -140,7 +140,9 @@ int abft_matrix_sum(const void* X, int32_t rows, int32_t cols, int64_t ldx, int3
  * and call abft_verify_sums); `out` receives one Verdict per layer;
  * `detected_count` (optional) += number of flagged layers.
  */
-typedef struct { const float* colck; const float* rowck; const double* rhs; int32_t k, pad; } abft_global_task_t;
+/* k = checksum length; tol_k = the K of the tau rule when it differs (0 = k): the unpadded
+ * K of the reference GEMM (tiled.py:471-473), e.g. C*R*S of a conv whose channels were padded */
+typedef struct { const float* colck; const float* rowck; const double* rhs; int32_t k, tol_k; } abft_global_task_t;
 
 int abft_global_lhs(const abft_global_task_t* tasks /*device*/, int32_t ntasks, double* sums /*[n][2]*/,
                     void* stream);
@@ -149,6 +151,38 @@ int abft_verify_sums(const double* sums /*[n][2]*/, const int32_t* k /*device [n
 /* Single-GPU fast path: abft_global_lhs + abft_verify_sums fused into one launch. */
 int abft_global_verify(const abft_global_task_t* tasks, int32_t ntasks, int32_t numeric, double* sums,
                        abft_verdict_t* out, int32_t* detected_count, void* stream);
+
+/*
+ * Implicit-GEMM convolution with the same ABFT epilogues (the reference lowers
+ * convs to GEMMs by im2col, shapes.py:156-180 layer_to_gemm: M = n*P*Q, N = OC, K = C*R*S).
+ *   gemm.A    the NHWC input [n][h][w][c] (c = physical channels, a multiple of 8; channels
+ *             past the model's real C are zero), read through a TMA im2col map — the im2col
+ *             matrix is never materialised.  gemm.lda is ignored.
+ *   gemm.Bt   packed weights [OC x K], K = r*s*c ordered (r, s, c) (abft_conv_pack_weight)
+ *   gemm.M/K  derived (M = n*P*Q, K = r*s*c); pass 0 or the same values
+ *   gemm.C    output [M x OC] = NHWC [n][P][Q][OC]
+ * All scheme / fault / verdict / fused-checksum fields keep their GEMM meaning with
+ * row = output pixel index (n*P + p)*Q + q and col = output channel.
+ * 1x1 / stride-1 / pad-0 convs run as the plain GEMM of the NHWC matrix.
+ */
+typedef struct {
+  abft_gemm_args_t gemm;
+  int32_t n, h, w, c;
+  int32_t r, s, stride_h, stride_w, pad_h, pad_w;
+} abft_conv_args_t;
+
+int abft_conv2d(const abft_conv_args_t* args, void* stream);
+/* out[0] A-load mode (0 GEMM, 1 im2col 64-channel chunks, 2 im2col 8-channel chunks),
+ * [1] packed-weight channel stride, [2] P, [3] Q, [4] K = r*s*c, [5] M = n*P*Q */
+int abft_conv_plan(const abft_conv_args_t* args, int32_t* out /*[6]*/);
+/* torch-layout weight [OC][cin][r][s] -> K-major [OC][(r, s, ck)], channels >= cin zero */
+int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin, int32_t r, int32_t s, int32_t ck, void* out,
+                          void* stream);
+/* windowed activation checksum of the conv's im2col matrix, out[(ri*s + si)*c + ch]
+ * (column_checksum of the lowered A, checksum.py:90-96), fp32; accumulate != 0 adds */
+int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w, int32_t c, int32_t r, int32_t s,
+                    int32_t stride_h, int32_t stride_w, int32_t pad_h, int32_t pad_w, int32_t dtype, float* out,
+                    int32_t accumulate, void* stream);
 
 /* Clear a per-forward accumulator block (one graph memset node instead of a kernel). */
 int abft_zero(void* p, int64_t bytes, void* stream);

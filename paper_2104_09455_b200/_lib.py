@@ -32,6 +32,10 @@ EXPORTED_SYMBOLS = (
     "abft_convert_i64",
     "abft_matrix_sum",
     "abft_zero",
+    "abft_conv2d",
+    "abft_conv_plan",
+    "abft_conv_pack_weight",
+    "abft_conv_colck",
     "abft_global_lhs",
     "abft_verify_sums",
     "abft_global_verify",
@@ -87,9 +91,16 @@ class GemmArgs(ctypes.Structure):
     ]
 
 
+class ConvArgs(ctypes.Structure):
+    _fields_ = [("gemm", GemmArgs),
+                ("n", ctypes.c_int32), ("h", ctypes.c_int32), ("w", ctypes.c_int32), ("c", ctypes.c_int32),
+                ("r", ctypes.c_int32), ("s", ctypes.c_int32), ("stride_h", ctypes.c_int32),
+                ("stride_w", ctypes.c_int32), ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32)]
+
+
 class GlobalTask(ctypes.Structure):
     _fields_ = [("colck", ctypes.c_void_p), ("rowck", ctypes.c_void_p), ("rhs", ctypes.c_void_p),
-                ("k", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("k", ctypes.c_int32), ("tol_k", ctypes.c_int32)]
 
 
 _lock = threading.Lock()
@@ -109,6 +120,10 @@ def _declare(lib):
     lib.abft_global_lhs.argtypes = [vp, i32, vp, vp]
     lib.abft_global_verify.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     lib.abft_verify_sums.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+    lib.abft_conv2d.argtypes = [ctypes.POINTER(ConvArgs), vp]
+    lib.abft_conv_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]
+    lib.abft_conv_pack_weight.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp]
+    lib.abft_conv_colck.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, i32, vp]
     lib.abft_last_error.restype = ctypes.c_char_p
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)

@@ -152,11 +152,12 @@ __global__ void global_lhs_kernel(const abft_global_task_t* __restrict__ tasks, 
     sums[2 * blockIdx.x] = s;
     sums[2 * blockIdx.x + 1] = rhs;
     if (out != nullptr || detected_count != nullptr) {
-      const double tol = tolerance(r, t.k, s, rhs);
+      const int tk = t.tol_k > 0 ? t.tol_k : t.k;
+      const double tol = tolerance(r, tk, s, rhs);
       const int det = fabs(s - rhs) > tol ? 1 : 0;
       if (out) {
         abft_verdict_t v;
-        v.lhs = s; v.rhs = rhs; v.tol = tol; v.k = t.k; v.detected = det;
+        v.lhs = s; v.rhs = rhs; v.tol = tol; v.k = tk; v.detected = det;
         out[blockIdx.x] = v;
       }
       if (det && detected_count) atomicAdd(detected_count, 1);
@@ -177,9 +178,146 @@ __global__ void verify_kernel(const double* __restrict__ sums, const int* __rest
   if (v.detected && detected_count) atomicAdd(detected_count, 1);
 }
 
+// ------------------------------------------------------- conv companions
+// Weight [OC][Cin][R][S] (torch layout) -> K-major [OC][(r, s, c)] with c padded to ck (zeros):
+// the B^T operand of the implicit-GEMM conv, K ordered like the im2col columns.
+__global__ void conv_pack_weight_kernel(const uint16_t* __restrict__ w, int oc, int cin, int r, int s, int ck,
+                                        uint16_t* __restrict__ out) {
+  const long long kk = (long long)r * s * ck;
+  const long long total = (long long)oc * kk;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int o = (int)(i / kk);
+    const int k = (int)(i - (long long)o * kk);
+    const int tap = k / ck, c = k - tap * ck;
+    const int ri = tap / s, si = tap - ri * s;
+    out[i] = c < cin ? w[(((long long)o * cin + c) * r + ri) * s + si] : (uint16_t)0;
+  }
+}
+
+// Windowed activation checksum of an implicit-GEMM conv (global ABFT):
+//   colck[(ri*S + si)*C + c] = sum over images n and output pixels (p, q) of
+//                              X[n][p*sh - ph + ri][q*sw - pw + si][c]   (zero outside the image)
+// i.e. column_checksum (checksum.py:90-96) of the im2col matrix, without materialising it.
+// One CTA owns a band of input rows and a slab of images: it sums the slab into a
+// [WT x C] smem tile per (row, w-tile), turns each tile into per-(s, c) window sums, and
+// adds them to a CTA-private [R*S*C] partial in smem for every filter row r whose window
+// covers the input row; one global atomicAdd per entry at the end.  X is read once.
+template <typename T>
+__global__ void __launch_bounds__(256) conv_colck_kernel(const T* __restrict__ x, int nimg, int H, int W, int C,
+                                                         int R, int S, int sh, int sw, int ph, int pw, int P, int Q,
+                                                         int rows_per_cta, int imgs_per_cta, int wt,
+                                                         float* __restrict__ out) {
+  extern __shared__ float sm[];
+  float* part = sm;                        // [R*S*C]
+  float* tile = sm + R * S * C;            // [wt][C]
+  const int nrsc = R * S * C;
+  for (int i = threadIdx.x; i < nrsc; i += blockDim.x) part[i] = 0.f;
+  const int cv = C / 8;
+  const int h_begin = blockIdx.x * rows_per_cta, h_end = min(H, h_begin + rows_per_cta);
+  const int i_begin = blockIdx.y * imgs_per_cta, i_end = min(nimg, i_begin + imgs_per_cta);
+  for (int hh = h_begin; hh < h_end; ++hh) {
+    // filter rows whose windows include input row hh: hh = p*sh - ph + r, 0 <= p < P
+    for (int w0 = 0; w0 < W; w0 += wt) {
+      const int wn = min(wt, W - w0);
+      __syncthreads();
+      for (int v = threadIdx.x; v < wn * cv; v += blockDim.x) {
+        const int wl = v / cv, c8 = v - wl * cv;
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int n = i_begin; n < i_end; ++n) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + (((long long)n * H + hh) * W + w0 + wl) * C + c8 * 8));
+          const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += (float)e[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tile[wl * C + c8 * 8 + j] = acc[j];
+      }
+      __syncthreads();
+      for (int it = threadIdx.x; it < S * C; it += blockDim.x) {
+        const int si = it / C, c = it - si * C;
+        // input columns w = q*sw - pw + si inside [w0, w0 + wn), 0 <= q < Q
+        int qlo = w0 + pw - si;
+        qlo = qlo <= 0 ? 0 : (qlo + sw - 1) / sw;
+        float u = 0.f;
+        for (int q = qlo; q < Q; ++q) {
+          const int w = q * sw - pw + si;
+          if (w >= w0 + wn) break;
+          u += tile[(w - w0) * C + c];
+        }
+        if (u != 0.f) {
+          for (int ri = 0; ri < R; ++ri) {
+            const int t = hh + ph - ri;
+            if (t < 0 || t % sh != 0 || t / sh >= P) continue;
+            part[(ri * S + si) * C + c] += u;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrsc; i += blockDim.x)
+    if (part[i] != 0.f) atomicAdd(&out[i], part[i]);
+}
+
 }  // namespace abft
 
 using namespace abft;
+
+extern "C" __attribute__((visibility("default"))) int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin,
+                                                                           int32_t r, int32_t s, int32_t ck,
+                                                                           void* out, void* stream) {
+  if (oc < 1 || cin < 1 || r < 1 || s < 1 || ck < cin || ck % 8) return fail(ABFT_E_SHAPE, "conv_pack_weight: bad extents");
+  const long long total = (long long)oc * r * s * ck;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 8LL * num_sms());
+  conv_pack_weight_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const uint16_t*)w, oc, cin, r, s, ck, (uint16_t*)out);
+  return cuda_check(cudaGetLastError(), "conv_pack_weight launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w,
+                                                                     int32_t c, int32_t r, int32_t s, int32_t stride_h,
+                                                                     int32_t stride_w, int32_t pad_h, int32_t pad_w,
+                                                                     int32_t dtype, float* out, int32_t accumulate,
+                                                                     void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || r < 1 || s < 1 || stride_h < 1 || stride_w < 1 || pad_h < 0 ||
+      pad_w < 0)
+    return fail(ABFT_E_SHAPE, "conv_colck: bad extents (channels must be a multiple of 8)");
+  if ((reinterpret_cast<uintptr_t>(X) & 15)) return fail(ABFT_E_VALUE, "conv_colck: X must be 16-byte aligned");
+  const int P = (h + 2 * pad_h - r) / stride_h + 1, Q = (w + 2 * pad_w - s) / stride_w + 1;
+  if (P < 1 || Q < 1) return fail(ABFT_E_SHAPE, "conv_colck: output extent is not positive");
+  cudaStream_t st = as_stream(stream);
+  const long long rsc = (long long)r * s * c;
+  if (!accumulate) {
+    int rc = cuda_check(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)rsc, st), "conv_colck memset");
+    if (rc) return rc;
+  }
+  // smem: [R*S*C] partial + [wt x C] tile within 96 KB
+  const long long budget = 96 * 1024 / 4;
+  if (rsc + 8LL * c > budget) return fail(ABFT_E_UNSUPPORTED, "conv_colck: R*S*C too large for the on-chip partial");
+  int wt = (int)std::min<long long>((budget - rsc) / c, 256);
+  wt = std::max(1, std::min(wt, w));
+  // grid: row bands x image slabs, about 4 CTAs per SM
+  const int sms = num_sms();
+  const long long want = 4LL * sms;
+  int islabs = (int)std::min<long long>(n, std::max<long long>(1, want / h));
+  int imgs_per_cta = (n + islabs - 1) / islabs;
+  islabs = (n + imgs_per_cta - 1) / imgs_per_cta;
+  int bands = (int)std::min<long long>(h, std::max<long long>(1, want / islabs));
+  int rows_per_cta = (h + bands - 1) / bands;
+  bands = (h + rows_per_cta - 1) / rows_per_cta;
+  const size_t smem = sizeof(float) * (size_t)(rsc + (long long)wt * c);
+  dim3 grid(bands, islabs);
+  if (dtype == ABFT_BF16) {
+    cudaFuncSetAttribute(conv_colck_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    conv_colck_kernel<__nv_bfloat16><<<grid, 256, smem, st>>>((const __nv_bfloat16*)X, n, h, w, c, r, s, stride_h,
+                                                              stride_w, pad_h, pad_w, P, Q, rows_per_cta,
+                                                              imgs_per_cta, wt, out);
+  } else {
+    cudaFuncSetAttribute(conv_colck_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    conv_colck_kernel<__half><<<grid, 256, smem, st>>>((const __half*)X, n, h, w, c, r, s, stride_h, stride_w, pad_h,
+                                                       pad_w, P, Q, rows_per_cta, imgs_per_cta, wt, out);
+  }
+  return cuda_check(cudaGetLastError(), "conv_colck launch");
+}
 
 extern "C" __attribute__((visibility("default"))) int abft_colsum(const void* X, int32_t rows, int32_t cols, int64_t ldx, int32_t dtype, float* out,
                            int32_t accumulate, void* stream) {

@@ -18,13 +18,12 @@ from .shapes import DType
 OUT_CODES = {"f32": _lib.OUT_F32, "f16": _lib.OUT_F16, "bf16": _lib.OUT_BF16, None: _lib.OUT_NONE}
 
 
-def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numeric: int,
-         scheme: Scheme = Scheme.UNPROTECTED, out=None, ldc: int = 0, out_kind: Optional[str] = "f32",
-         relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
-         tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
-         fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-         num_sms: int = 0, ck_rows=None, plan_only: bool = False):
-    """Enqueue one protected GEMM (or, with plan_only, return the kernel plan dict)."""
+def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numeric: int,
+               scheme: Scheme = Scheme.UNPROTECTED, out=None, ldc: int = 0, out_kind: Optional[str] = "f32",
+               relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
+               tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
+               fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
+               num_sms: int = 0, ck_rows=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = bt.data_ptr(), ldbt
@@ -45,6 +44,15 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
     args.tile_n, args.num_sms = tile_n, num_sms
     if ck_rows is not None:
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
+    return args
+
+
+def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numeric: int,
+         scheme: Scheme = Scheme.UNPROTECTED, plan_only: bool = False, **kw):
+    """Enqueue one protected GEMM (or, with plan_only, return the kernel plan dict).
+
+    Keyword arguments are the fields of abft_gemm_args_t (see _gemm_args)."""
+    args = _gemm_args(a, lda, bt, ldbt, m, n, k, dtype, numeric, scheme, **kw)
     if plan_only:
         out = (ctypes.c_int32 * 8)()
         _lib.check(_lib.load().abft_gemm_plan(ctypes.byref(args), out))
@@ -52,6 +60,47 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
                     ck_offline_recommended=bool(out[5]), n_blocks=out[6], grid=out[7])
     _lib.check(_lib.load().abft_gemm(ctypes.byref(args), stream_handle()))
     return None
+
+
+def conv_args(x, geom: dict, bt, oc: int, dtype: DType, numeric: int, scheme: Scheme = Scheme.UNPROTECTED,
+              **kw):
+    """abft_conv_args_t for an NHWC input x [n, h, w, c] and packed weights bt [OC x r*s*c].
+
+    geom: n, h, w, c, r, s, stride_h, stride_w, pad_h, pad_w."""
+    g = _gemm_args(x, geom["c"], bt, bt.stride(0), 0, oc, 0, dtype, numeric, scheme, **kw)
+    args = _lib.ConvArgs()
+    args.gemm = g
+    for f in ("n", "h", "w", "c", "r", "s", "stride_h", "stride_w", "pad_h", "pad_w"):
+        setattr(args, f, int(geom[f]))
+    return args
+
+
+def conv_plan(args) -> dict:
+    out = (ctypes.c_int32 * 6)()
+    _lib.check(_lib.load().abft_conv_plan(ctypes.byref(args), out))
+    return dict(a_mode=out[0], ck=out[1], p=out[2], q=out[3], k=out[4], m=out[5])
+
+
+def conv2d(args) -> None:
+    """Enqueue one protected implicit-GEMM convolution (abft_conv2d)."""
+    _lib.check(_lib.load().abft_conv2d(ctypes.byref(args), stream_handle()))
+
+
+def conv_pack_weight(w, ck: int):
+    """torch-layout weight [OC, cin, r, s] (CUDA fp16/bf16) -> packed K-major [OC, r*s*ck]."""
+    t = torch()
+    oc, cin, r, s = (int(v) for v in w.shape)
+    w = w.contiguous()
+    out = t.empty((oc, r * s * ck), dtype=w.dtype, device="cuda")
+    _lib.call("abft_conv_pack_weight", ptr(w), oc, cin, r, s, ck, ptr(out), stream_handle())
+    return out
+
+
+def conv_colck(x, geom: dict, dtype: DType, out, accumulate: bool = False) -> None:
+    """Windowed activation checksum of the conv's im2col matrix -> out [r*s*c] fp32."""
+    _lib.call("abft_conv_colck", ptr(x), geom["n"], geom["h"], geom["w"], geom["c"], geom["r"], geom["s"],
+              geom["stride_h"], geom["stride_w"], geom["pad_h"], geom["pad_w"], storage_code(dtype), ptr(out),
+              int(accumulate), stream_handle())
 
 
 def ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, split: bool):
@@ -76,13 +125,14 @@ def matrix_sum(x, out) -> None:
 
 
 def global_tasks(tasks):
-    """[(colck, rowck, rhs_tensor_or_None, k)] -> device array of abft_global_task_t."""
+    """[(colck, rowck, rhs_tensor_or_None, k[, tol_k])] -> device array of abft_global_task_t."""
     t = torch()
     arr = (_lib.GlobalTask * len(tasks))()
-    for i, (ca, rb, rhs, k) in enumerate(tasks):
+    for i, task in enumerate(tasks):
+        ca, rb, rhs, k = task[:4]
         arr[i].colck, arr[i].rowck = ca.data_ptr(), rb.data_ptr()
         arr[i].rhs = rhs.data_ptr() if rhs is not None else None
-        arr[i].k, arr[i].pad = k, 0
+        arr[i].k, arr[i].tol_k = k, (task[4] if len(task) > 4 else 0)
     host = t.frombuffer(bytearray(bytes(arr)), dtype=t.uint8)
     return host.to("cuda")
 

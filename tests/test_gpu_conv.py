@@ -1,0 +1,116 @@
+"""Parity of the implicit-GEMM convolution path (TMA im2col) against the oracle.
+
+The reference checks a conv as the GEMM of its im2col lowering (shapes.py:156-180); the
+oracle restates that lowering (im2col_nhwc, K ordered (r, s, c)) and runs the reference
+execute / global check on it.  Bar: exact-int bit-exact (outputs, verdict values, flags);
+binary16 outputs within the fp32-accumulate reordering bound, flags identical for faults
+far outside tau.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import abft_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GEMM_RTOL = 2e-5
+
+# (n, h, w, c, oc, r, s, stride, pad): every A-load mode of the kernel
+CASES = [
+    (2, 20, 22, 3, 64, 7, 7, 2, 3),      # stem: 8-channel im2col columns (mode 2)
+    (2, 13, 11, 64, 48, 3, 3, 1, 1),     # 64-channel chunks, SW128 (mode 1)
+    (3, 9, 10, 16, 40, 3, 3, 2, 1),      # strided, 8-channel columns
+    (2, 12, 12, 32, 24, 1, 1, 1, 0),     # pointwise = plain GEMM of the NHWC matrix (mode 0)
+    (2, 14, 14, 64, 32, 1, 1, 2, 0),     # strided pointwise (downsample) through im2col
+    (1, 35, 33, 3, 16, 11, 11, 4, 2),    # AlexNet stem geometry
+    (2, 9, 9, 24, 136, 5, 5, 1, 2),      # several 8-channel chunks per tap, N > one CTA tile
+    (1, 8, 8, 128, 64, 3, 3, 1, 1),      # two 64-channel chunks per tap
+]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2104_09455_b200 as pkg
+    from paper_2104_09455_b200 import device
+    device.require_device()
+    return pkg
+
+
+def _data(case, exact, seed=0):
+    n, h, w, c, oc, r, s, st, pd = case
+    rng = np.random.default_rng(seed)
+    if exact:
+        x = rng.integers(-3, 4, size=(n, h, w, c)).astype(np.int64)
+        wt = rng.integers(-3, 4, size=(oc, c, r, s)).astype(np.int64)
+    else:
+        x = rng.uniform(-1, 1, size=(n, h, w, c)).astype(np.float16)
+        wt = rng.uniform(-1, 1, size=(oc, c, r, s)).astype(np.float16)
+    cols = O.im2col_nhwc(x, r, s, st, pd)
+    wmat = np.ascontiguousarray(wt.transpose(2, 3, 1, 0).reshape(r * s * c, oc))
+    return x, wt, cols, wmat
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("scheme", ["unprotected", "global-abft", "thread-one-sided"])
+def test_conv_exact_int_bit_exact(P, case, scheme):
+    n, h, w, c, oc, r, s, st, pd = case
+    x, wt, cols, wmat = _data(case, exact=True)
+    tiling = P.TilingConfig()
+    m = cols.shape[0]
+    faults_ref = [("output", m // 2, oc - 1, 5)] if scheme != "unprotected" else []
+    faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in faults_ref]
+    rep = P.conv2d(x, wt, stride=st, padding=pd, tiling=tiling, scheme=P.Scheme(scheme), faults=faults)
+    out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, faults_ref)
+    assert rep.output.shape == (n, (h + 2 * pd - r) // st + 1, (w + 2 * pd - s) // st + 1, oc)
+    assert np.array_equal(rep.output.reshape(m, oc), out)
+    assert (rep.shape.m, rep.shape.n, rep.shape.k) == (m, oc, c * r * s)
+    if scheme == "global-abft":
+        v, rv = rep.verdicts[0], verdicts[0]
+        assert (v.detected, v.lhs, v.rhs, v.tolerance_used) == (rv.detected, rv.lhs, rv.rhs, rv.tolerance_used)
+    elif scheme == "thread-one-sided":
+        got = [(v.thread_row, v.thread_col, v.detected) for v in rep.verdicts]
+        ref = [(v.thread_row, v.thread_col, v.detected) for v in verdicts]
+        assert got == ref
+    assert rep.detected == any(v.detected for v in verdicts)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_binary16_outputs_and_flags(P, case):
+    x, wt, cols, wmat = _data(case, exact=False, seed=1)
+    n, h, w, c, oc, r, s, st, pd = case
+    m = cols.shape[0]
+    ref_out, _ = O.execute(cols, wmat, O.Tiling(), "unprotected", [], "binary16")
+    bound = np.abs(cols.astype(np.float64)) @ np.abs(wmat.astype(np.float64))
+    for scheme in ("unprotected", "global-abft", "thread-one-sided"):
+        rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), dtype=P.BINARY16)
+        err = np.abs(rep.output.reshape(m, oc).astype(np.float64) - ref_out)
+        assert (err <= GEMM_RTOL * bound + 1e-6).all(), scheme
+        assert rep.detected is False, scheme          # zero false positives on clean runs
+    # a fault far above tau is flagged by both schemes, at the same thread tile as the oracle
+    g = O.global_check(cols, wmat, ref_out, "binary16")
+    delta = float(50 * g.tolerance_used + 1)
+    row, col = m - 1, oc // 2
+    for scheme in ("global-abft", "thread-one-sided"):
+        rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme),
+                       faults=[P.OutputFault(row=row, col=col, delta=delta)], dtype=P.BINARY16)
+        _, ref_v = O.execute(cols, wmat, O.Tiling(), scheme, [("output", row, col, delta)], "binary16")
+        assert rep.detected is True
+        if scheme == "thread-one-sided":
+            assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \
+                [(v.thread_row, v.thread_col) for v in ref_v if v.detected]
+
+
+def test_conv_colck_is_the_im2col_column_sum(P):
+    import torch
+    from paper_2104_09455_b200 import conv as C, kernels
+    for case in CASES:
+        n, h, w, c, oc, r, s, st, pd = case
+        x, wt, cols, _ = _data(case, exact=True, seed=2)
+        xd = C.upload_nhwc(x, P.EXACT_INT)
+        pc = C.prepare_conv_weight(wt, P.EXACT_INT, ck=int(xd.shape[3]))
+        geom = C.geometry(xd, pc, st, pd)
+        out = torch.empty(r * s * xd.shape[3], dtype=torch.float32, device="cuda")
+        kernels.conv_colck(xd, geom, P.EXACT_INT, out)
+        ref = O.colck(O.im2col_nhwc(np.pad(x, ((0, 0), (0, 0), (0, 0), (0, xd.shape[3] - c))), r, s, st, pd))
+        assert np.array_equal(out.cpu().numpy().astype(np.int64), ref), case

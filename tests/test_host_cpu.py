@@ -223,3 +223,17 @@ def test_scheme_names_and_abi_codes():
     assert SCHEME_CODE[P.Scheme.THREAD_REPLICATION_SINGLE_ACC] == _lib.REPL_SINGLE
     with pytest.raises(ValueError):
         P.Scheme("bogus")
+
+
+def test_network_layer_lists_reproduce_paper_fig4():
+    # PAPER.md:284-291 (Fig 4): aggregate FP16 AI at 1080x1920, batch 1, x8 padding
+    pytest.importorskip("torchvision")
+    import paper_2104_09455_b200 as P
+    from paper_2104_09455_b200 import networks
+    from paper_2104_09455_b200.shapes import PaddingPolicy
+    fig4 = {"squeezenet1_0": 71.1, "shufflenet_v2_x1_0": 76.6, "resnet50": 122.0, "alexnet": 125.5, "vgg16": 155.5}
+    for name, ai in fig4.items():
+        layers = networks.capture(name, 1, 1080, 1920)
+        agg = P.aggregate_intensity([P.pad_gemm(l.gemm(), PaddingPolicy.MULTIPLE_OF_8) for l in layers], P.BINARY16)
+        assert agg == pytest.approx(ai, abs=0.05), name
+    assert len(networks.capture("resnet50", 1, 224, 224)) == 54
