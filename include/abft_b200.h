@@ -86,6 +86,10 @@ typedef struct {
   /* optional checksum rows prepared offline by abft_ck_rows for THIS call's plan; when null the
    * checksum warps generate them on chip from each B^T tile (one-sided / two-sided only) */
   const void* ck_rows; int64_t ldck; int32_t ck_rows_n;
+  /* optional [K] fp32, global scheme: += column sums of A as the kernel stages it (the activation
+   * checksum of checksum.py:90-96 / :229 computed from the shared-memory A tiles the MMA consumes,
+   * so the global scheme needs no extra pass over A; for a conv this is the windowed im2col sum) */
+  float* a_colck;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);

@@ -88,6 +88,7 @@ class GemmArgs(ctypes.Structure):
         ("tile_n", ctypes.c_int32),
         ("num_sms", ctypes.c_int32),
         ("ck_rows", ctypes.c_void_p), ("ldck", ctypes.c_int64), ("ck_rows_n", ctypes.c_int32),
+        ("a_colck", ctypes.c_void_p),
     ]
 
 

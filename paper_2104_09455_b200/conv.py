@@ -7,7 +7,8 @@ contract — same schemes, tiling meaning, fault coordinates (row = output pixel
 (n*P + p)*Q + q, col = output channel), verdict ordering and report type as ``execute``
 on the im2col matrix — but never builds the im2col matrix: the sm_100a kernel reads the
 NHWC activation through a TMA im2col map (implicit GEMM), and the global scheme's
-activation checksum is the windowed column sum ``abft_conv_colck``.
+activation checksum — the column sum of the im2col matrix — is accumulated by the same
+kernel from the A tiles it stages (or by the standalone windowed pass ``abft_conv_colck``).
 
 K ordering is (r, s, c); input channels are zero-padded to a multiple of 8
 (the reference's x8 padding rule, shapes.py:187-195, also the TMA 16-byte pitch rule).
@@ -93,11 +94,14 @@ def geometry(x_dev, pc: PreparedConv, stride, padding) -> dict:
 
 
 def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig(),
-           scheme: Scheme = Scheme.UNPROTECTED, faults: Sequence[FaultSpec] = (), dtype: DType | None = None):
+           scheme: Scheme = Scheme.UNPROTECTED, faults: Sequence[FaultSpec] = (), dtype: DType | None = None,
+           colck_source: str = "fused"):
     """Protected NHWC convolution; returns the reference's ExecutionReport for the lowered GEMM.
 
     ``report.output`` is [n, P, Q, OC] fp32 (int64 in exact-int mode); ``report.shape`` is
-    the reference lowering GemmShape(n*P*Q, OC, C*R*S)."""
+    the reference lowering GemmShape(n*P*Q, OC, C*R*S).  Global scheme: the windowed
+    activation checksum comes from the A tiles inside the conv kernel ("fused") or from the
+    standalone pass over the input ("standalone", abft_conv_colck)."""
     from .checksum import Verdict
     from .tiled import _TV_DTYPE, ExecutionReport, _counts, _thread_verdicts
 
@@ -128,15 +132,19 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     if thread_level:
         ntr, ntc = padded.m // tiling.thread_m, padded.n // tiling.thread_n
         verdicts = t.empty(ntr * ntc * _TV_DTYPE.itemsize, dtype=t.uint8, device="cuda")
+    if colck_source not in ("fused", "standalone"):
+        raise ValueError(f"colck_source must be 'fused' or 'standalone', got {colck_source!r}")
     out_sum = t.zeros(1, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
+    colck = t.zeros(pc.bt.shape[1], dtype=t.float32, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
+    fused = colck if colck_source == "fused" else None
     args = kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, out=out, ldc=pc.oc, out_kind="f32",
                              thread_m=tiling.thread_m, thread_n=tiling.thread_n, m_ext=padded.m, n_ext=padded.n,
                              tol_k=padded.k, faults=f_dev, nfaults=nf, out_sum=out_sum, verdicts=verdicts,
-                             ck_split=not dtype.is_exact)
+                             ck_split=not dtype.is_exact, a_colck=fused)
     kernels.conv2d(args)
     if scheme is Scheme.GLOBAL_ABFT:
-        colck = t.empty(pc.bt.shape[1], dtype=t.float32, device="cuda")
-        kernels.conv_colck(x_dev, geom, dtype, colck)
+        if colck_source == "standalone":
+            kernels.conv_colck(x_dev, geom, dtype, colck)
         sums = t.empty(2, dtype=t.float64, device="cuda")
         vbuf = t.empty(32, dtype=t.uint8, device="cuda")
         kernels.global_verify(kernels.global_tasks([(colck, pc.rowck, out_sum, pc.bt.shape[1], k_ref)]), 1,

@@ -7,10 +7,10 @@ buffers (NHWC input, packed weight, checksums, output) and enqueues it under
 unprotected / global / one-sided ABFT:
 
   unprotected       implicit-GEMM conv (or GEMM), fp16 store
-  global-abft       the same kernel with the output summation in its epilogue
-                    + the layer's windowed activation checksum (abft_conv_colck: the
-                    input comes out of pooling / residual / BN glue, so it cannot be
-                    fused into the producer)
+  global-abft       the same kernel with the output summation in its epilogue and the
+                    layer's windowed activation checksum accumulated from the A tiles it
+                    stages (the input comes out of pooling / residual / BN glue, so it
+                    cannot be fused into the producer's epilogue)
                     + its share of the network's single batched verification
   thread-one-sided  checksum N-slice in the same MMA, per-row compares in the epilogue
 
@@ -69,6 +69,7 @@ class LayerRunner:
                   relu=True)
         if scheme is Scheme.GLOBAL_ABFT:
             kw["out_sum"] = self.rhs
+            kw["a_colck"] = self.colck
         elif scheme is Scheme.THREAD_ONE_SIDED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-self.m // t.thread_m) * t.thread_m,
                       n_ext=-(-self.spec.oc // t.thread_n) * t.thread_n,
@@ -101,7 +102,7 @@ class LayerRunner:
         """One protected execution of the layer (verification included for global)."""
         if scheme is Scheme.GLOBAL_ABFT:
             kernels.zero(self.scratch)
-            self.colck_pass()
+            kernels.zero(self.colck)
             self.conv(scheme)
             self.verify()
         else:

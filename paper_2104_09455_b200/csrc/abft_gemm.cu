@@ -65,7 +65,10 @@ struct GemmParams {
   int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
   double r;
   float rk;              // r * tol_k in fp32, for the guard-banded fast compare
-  uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_bar;
+  uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_out, off_acolck, off_bar;
+  float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
+  int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
+  int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
   void* C;
@@ -279,7 +282,8 @@ __device__ __forceinline__ void apply_faults(const abft_fault_t* faults, int nfa
 template <typename T, int CLASS, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ GemmParams p) {
+                     const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ GemmParams p) {
   using TR = ElemTraits<T>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -292,6 +296,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   float2* rec = reinterpret_cast<float2*>(smem + p.off_rec);     // [128][rec_stride] (generic Mt)
   float* stg = reinterpret_cast<float*>(smem + p.off_stage);     // [2][32][128] chunk staging (generic Nt)
   float* colck_s = reinterpret_cast<float*>(smem + p.off_colck);
+  uint8_t* out_stage = smem + p.off_out;
+  float* acolck_s = reinterpret_cast<float*>(smem + p.off_acolck);  // [K] (acolck_in_smem)                         // [4 warps][2 buffers][32 rows x 128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* full = bars;
   uint64_t* ckfull = bars + p.stages;
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < p.stages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], p.a_colck != nullptr ? 5 : 1);   // + one arrival per A-checksum warp
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -328,10 +334,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
     if (ck_loaded) ptx::tma_prefetch(&tmCK);
+    if (p.tma_store) ptx::tma_prefetch(&tmC);
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 128) colck_s[i] = 0.f;
+  }
+  if (warp >= CK_WARP0 && p.acolck_in_smem) {
+    for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128) acolck_s[i] = 0.f;
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -517,6 +527,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       }
+    } else if (p.a_colck != nullptr) {
+      // ------------------------------------- global: activation column checksum
+      // Each A tile is summed over its 128 rows once (in the tile's first N block): thread
+      // (chunk c = 8 columns, row group g) reads 8 rows; shuffles fold the warp's 4 row groups.
+      // OOB rows / padded channels arrive as zeros from the TMA, so no masking is needed.
+      const int ct = threadIdx.x - CK_WARP0 * 32;
+      const int c = ct & 7, g = ct >> 3;
+      const bool a_none = p.a_mode == 2;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const bool count = (tile % p.num_n_blocks) == 0;
+#pragma unroll 1
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          ptx::mbar_wait(&full[s], ph);
+          if (count) {
+            const uint8_t* at = sm_a + s * p.stage_a_bytes;
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = g + 16 * i;
+              const uint8_t* src = a_none ? at + c * 2048 + r * 16 : at + r * 128 + ((c ^ (r & 7)) << 4);
+              const uint4 raw = *reinterpret_cast<const uint4*>(src);
+              const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = TR::unpack2(w[e]);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
+              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+            }
+            if (lane < 8) {
+              const int k0 = kb * BK + c * 8;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                if (k0 + e < p.K && acc[e] != 0.f) {
+                  if (p.acolck_in_smem) atomicAdd(&acolck_s[k0 + e], acc[e]);
+                  else atomicAdd(&p.a_colck[k0 + e], acc[e]);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&empty[s]);
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+      }
+      if (p.acolck_in_smem) {
+        ptx::named_bar_sync(2, 128);
+        for (int i = ct; i < p.K; i += 128)
+          if (acolck_s[i] != 0.f) atomicAdd(&p.a_colck[i], acolck_s[i]);
+      }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
@@ -526,6 +595,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     double rhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
+    int sbuf = 0;                                   // output staging buffer of this warp (double-buffered)
+    uint8_t* my_stage = out_stage + q * 8192;
     int t_local = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
@@ -657,6 +728,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float y = p.relu ? fmaxf(v[j], 0.f) : v[j];
             v[j] = round_out(y, p.out_dtype);
           }
+          if (p.tma_store) {
+            // stage 128-byte row segments (32 fp32 or 64 16-bit columns) in SW128 order, then one
+            // elected lane writes the [32 rows x 128 B] box with a bulk tensor store
+            const bool f32 = p.out_dtype == ABFT_OUT_F32;
+            const int half = f32 ? 0 : ((c0 >> 5) & 1);
+            uint8_t* buf = my_stage + sbuf * 4096;
+            if (half == 0) {
+              if (lane == 0) ptx::bulk_wait_read<1>();
+              __syncwarp();
+            }
+            uint8_t* rowp = buf + lane * 128;
+            if (f32) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 u;
+                u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+                u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+                u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+                u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+                *reinterpret_cast<uint4*>(rowp + (((half * 4 + j) ^ (lane & 7)) << 4)) = u;
+              }
+            }
+            if (f32 || half == 1) {
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_2d(&tmC, buf, gc0 - (f32 ? 0 : 32), m0 + q * 32);
+                ptx::bulk_commit();
+              }
+              sbuf ^= 1;
+            }
+          } else {
           const bool full_chunk = (cmax >= 32) && (gc0 + 32 <= p.N);
           if (row_store && p.out_dtype != ABFT_OUT_NONE) {
             if (p.out_dtype == ABFT_OUT_F32) {
@@ -688,6 +796,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   if (j < cmax && gc0 + j < p.N) dst[j] = TR::from_f(v[j]);
               }
             }
+          }
           }
           if (p.next_colck != nullptr) {
 #pragma unroll
@@ -737,6 +846,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::named_bar_sync(1, 128);
       if (et == 0) atomicAdd(p.out_sum, red_d[0] + red_d[1] + red_d[2] + red_d[3]);
     }
+    if (p.tma_store && lane == 0) ptx::bulk_wait_all();
     if (p.next_colck != nullptr && p.colck_in_smem) {
       ptx::named_bar_sync(1, 128);
       for (int i = col_lo + et; i < col_hi; i += 128) {
@@ -813,8 +923,8 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
 }
 
 template <typename T, int CLASS, int NT>
-int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const GemmParams& p, size_t smem,
-                int grid, cudaStream_t st) {
+int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo,
+                const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -822,22 +932,40 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
-  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, p);
+  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                 const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, p, smem, grid, st);
+                 const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, mo, p, smem, grid, st);
   if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, p, smem, grid, st);
-    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, mo, p, smem, grid, st);
+    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, mo, p, smem, grid, st);
   }
-  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, p, smem, grid, st);
-  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, p, smem, grid, st);
-  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, p, smem, grid, st);
+  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, mo, p, smem, grid, st);
+  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, mo, p, smem, grid, st);
+  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, mo, p, smem, grid, st);
+}
+
+// output map for the bulk tensor stores: dims {N, M}, box {128 B of columns, 32 rows}, SW128
+int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a) {
+  auto enc = get_encode_fn();
+  if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
+  CUtensorMapDataType dt = a->out_dtype == ABFT_OUT_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                           : a->out_dtype == ABFT_OUT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  cuuint64_t dims[2] = {(cuuint64_t)a->N, (cuuint64_t)a->M};
+  cuuint64_t strides[1] = {(cuuint64_t)(a->ldc * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, a->C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled(C) failed with CUresult " + std::to_string((int)r));
+  return ABFT_OK;
 }
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -974,8 +1102,23 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t rec_bytes = p.rec_stride ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
   const uint32_t stage_bytes_ep = (thread_level && out.ntc == 0) ? (uint32_t)(2 * 32 * BM * 4) : 0;
   const uint32_t colck_bytes = p.colck_in_smem ? (uint32_t)round_up(a->N * 4, 1024) : 0;
+  {
+    // bulk tensor stores of the output: whole 128-row tiles, 128-byte row units (32 fp32 / 64
+    // 16-bit columns) that tile bn_eff exactly, 16-byte aligned base and row pitch
+    const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
+    const int unit = 128 / esz;
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % unit == 0 &&
+                   ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
+                   !(dbg_env & 8192)) ? 1 : 0;
+  }
+  const uint32_t out_bytes = p.tma_store ? 4u * 8192u : 0u;
+  p.a_colck = (a->scheme == ABFT_GLOBAL || as_plain) ? a->a_colck : nullptr;
+  if (p.a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
+  p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
+  const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : 0u;
   const uint32_t bar_bytes = 1024;
-  const uint32_t extras = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + bar_bytes;
+  const uint32_t extras =
+      cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + out_bytes + acolck_bytes + bar_bytes;
   const uint32_t stage_bytes = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes;
   int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
   if (const char* cap = getenv("ABFT_SMEM_CAP")) budget = std::min(budget, atoi(cap) * 1024 - (int)extras);
@@ -989,7 +1132,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.off_rec = p.off_cks + cks_bytes;
   p.off_stage = p.off_rec + rec_bytes;
   p.off_colck = p.off_stage + stage_bytes_ep;
-  p.off_bar = p.off_colck + colck_bytes;
+  p.off_out = p.off_colck + colck_bytes;
+  p.off_acolck = p.off_out + out_bytes;
+  p.off_bar = p.off_acolck + acolck_bytes;
   out.smem = (size_t)p.off_bar + bar_bytes + 1024;
   out.grid = std::min(p.num_tiles, sms);
   out.ck_offline_recommended = (has_ck && p.num_m_blocks > 2) ? 1 : 0;
@@ -1092,11 +1237,19 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   } else {
     mc = mb;   // unused
   }
+  CUtensorMap mo;
+  if (p.tma_store) {
+    rc = make_out_map(&mo, a);
+    if (rc != ABFT_OK) return rc;
+  } else {
+    mo = mb;   // unused
+  }
   cudaStream_t st = as_stream(stream);
   if (p.debug & 64) pl.cls = CLASS_PLAIN;
   if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
-  if (a->dtype == ABFT_BF16) return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
-  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, p, pl.smem, pl.grid, st);
+  if (a->dtype == ABFT_BF16)
+    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
+  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
 }
 
 // ---------------------------------------------------------------- implicit-GEMM conv

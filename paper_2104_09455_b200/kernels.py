@@ -23,7 +23,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-               num_sms: int = 0, ck_rows=None):
+               num_sms: int = 0, ck_rows=None, a_colck=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = bt.data_ptr(), ldbt
@@ -44,6 +44,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     args.tile_n, args.num_sms = tile_n, num_sms
     if ck_rows is not None:
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
+    args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     return args
 
 

@@ -6,9 +6,10 @@ GEMM) with ReLU between them — the chain of ``run_protected_pipeline``
 
   unprotected   plain tcgen05 GEMM
   global-abft   output summation in the epilogue; the layer's activation checksum is
-                produced by the PREVIOUS layer's epilogue (fused next-layer colck,
-                PAPER.md:193) or, for the first layer, by one abft_colsum launch;
-                all dot products + verdicts run in one batched launch at the end
+                accumulated inside the same kernel from the A tiles it stages (the
+                kernel-fused activation checksum of PAPER.md:193, with no extra pass
+                over the activations); all dot products + verdicts run in one batched
+                launch at the end
   thread-one-sided  checksum N-slice in the same MMA, per-row compare in the
                 epilogue; fired thread tiles counted on device
 
@@ -113,13 +114,11 @@ class ProtectedChain:
                   out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu)
         if L.scheme is Scheme.GLOBAL_ABFT:
             kw["out_sum"] = self.rhs[i]
+            kw["a_colck"] = self.colck[i]
         elif L.scheme is not Scheme.UNPROTECTED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-m // t.thread_m) * t.thread_m,
                       n_ext=-(-L.n // t.thread_n) * t.thread_n, tol_k=-(-L.k // t.k_step) * t.k_step,
                       fired_count=self.counters[0:1], ck_split=self.ck_split)
-        nxt = i + 1
-        if nxt < len(self.layers) and self.layers[nxt].scheme is Scheme.GLOBAL_ABFT:
-            kw["next_colck"] = self.colck[nxt]
         return kw
 
     def forward(self, x=None) -> object:
@@ -127,9 +126,6 @@ class ProtectedChain:
         if x is not None:
             self.x.copy_(x, non_blocking=True)
         kernels.zero(self.scratch)
-        if self.layers and self.layers[0].scheme is Scheme.GLOBAL_ABFT:
-            kernels.colsum(self.x, self.batch, self.layers[0].k, self.x.stride(0), self.dtype, self.colck[0],
-                           accumulate=True)
         a = self.x
         for i, L in enumerate(self.layers):
             kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype, self.numeric,

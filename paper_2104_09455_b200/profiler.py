@@ -8,10 +8,8 @@ rather than from a T4-calibrated model:
 
   T_o     the layer's GEMM alone (CUDA-graph replayed, CUDA events)
   T_one   GEMM with the checksum N-slice and the per-row compare (flags mode)
-  T_glob  GEMM with the output summation
-          + the cost of producing this layer's activation checksum: the standalone
-            abft_colsum for the first layer, otherwise the extra time the previous
-            layer's epilogue spends fusing it
+  T_glob  GEMM with the output summation and the activation checksum accumulated
+          from the staged A tiles (both inside the one kernel)
           + this layer's share of the one batched verification launch
 """
 
@@ -60,36 +58,20 @@ def profile_layers(weights: Sequence, batch: int, dtype: DType = BINARY16,
     chains = {s: ProtectedChain(weights, batch, [s] * n, dtype, tiling) for s in
               (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED)}
     entries = {}
-    t_plain, t_fused = [], []
     for i in range(n):
         for s, ch in chains.items():
             L = ch.layers[i]
             a = ch.x if i == 0 else ch.acts[i - 1]
             kw = ch._gemm_kwargs(i, L)
-            kw.pop("next_colck", None)
-            us = graph_time_us(lambda: kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, batch, L.n, L.k, dtype,
-                                                    ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw), iters)
-            entries[(i, s)] = us
-            if s is Scheme.UNPROTECTED:
-                t_plain.append(us)
-        # the same GEMM when it also emits the next layer's activation checksum
-        ch = chains[Scheme.GLOBAL_ABFT]
-        L = ch.layers[i]
-        a = ch.x if i == 0 else ch.acts[i - 1]
-        kw = ch._gemm_kwargs(i, L)
-        kw.pop("out_sum", None)
-        kw["next_colck"] = ch.colck[min(i + 1, n - 1)]
-        t_fused.append(graph_time_us(lambda: kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, batch, L.n, L.k,
-                                                          dtype, ch.numeric, Scheme.UNPROTECTED, **kw), iters))
+            entries[(i, s)] = graph_time_us(lambda: kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, batch, L.n, L.k,
+                                                                 dtype, ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw),
+                                            iters)
     g = chains[Scheme.GLOBAL_ABFT]
-    t_colsum = graph_time_us(lambda: kernels.colsum(g.x, batch, g.layers[0].k, g.x.stride(0), dtype, g.colck[0],
-                                                    accumulate=True), iters)
     t_verify = graph_time_us(lambda: kernels.global_verify(g._tasks, len(g.global_ids), g.numeric, g._gsums,
                                                            out=g.verdict_buf, detected_count=g.counters[1:2]), iters)
     out = {}
     for i in range(n):
-        colck_cost = t_colsum if i == 0 else max(t_fused[i - 1] - t_plain[i - 1], 0.0)
         out[(i, Scheme.UNPROTECTED)] = entries[(i, Scheme.UNPROTECTED)] * 1e-6
-        out[(i, Scheme.GLOBAL_ABFT)] = (entries[(i, Scheme.GLOBAL_ABFT)] + colck_cost + t_verify / n) * 1e-6
+        out[(i, Scheme.GLOBAL_ABFT)] = (entries[(i, Scheme.GLOBAL_ABFT)] + t_verify / n) * 1e-6
         out[(i, Scheme.THREAD_ONE_SIDED)] = entries[(i, Scheme.THREAD_ONE_SIDED)] * 1e-6
     return MeasuredTimings(entries=out)
