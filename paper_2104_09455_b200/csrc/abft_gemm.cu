@@ -40,9 +40,9 @@ namespace abft {
 
 constexpr int BM = 128;            // UMMA M (one TMEM lane per output row)
 constexpr int BK = 64;             // 64 fp16 = 128 B = one SW128 row
-constexpr int NUM_THREADS = 320;   // 10 warps
-constexpr int EPI_WARP0 = 2;
-constexpr int CK_WARP0 = 6;
+constexpr int NUM_THREADS = 448;   // 14 warps
+constexpr int EPI_WARP0 = 2;       // warps 2-9: epilogue (two per TMEM lane quadrant)
+constexpr int CK_WARP0 = 10;       // warps 10-13: checksum rows / A-column checksum
 constexpr int COLCK_SMEM_MAX = 4096;
 
 enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
@@ -68,6 +68,7 @@ struct GemmParams {
   uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_out, off_acolck, off_bar;
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
+  int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
   int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);    // one arrival per epilogue warp
+      ptx::mbar_init(&tempty[a], 8);    // one arrival per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
-    for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 128) colck_s[i] = 0.f;
+    for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 256) colck_s[i] = 0.f;
   }
   if (warp >= CK_WARP0 && p.acolck_in_smem) {
     for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128) acolck_s[i] = 0.f;
@@ -589,14 +590,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int et = threadIdx.x - EPI_WARP0 * 32;   // 0..127 (named-barrier rank)
-    const int q = warp & 3;                         // TMEM lane quadrant of this warp
-    const int row = q * 32 + lane;                  // tile row == TMEM lane
+    // Two warps per TMEM lane quadrant (warps 2-5: h = 0, warps 6-9: h = 1) split the
+    // tile's 32-column chunks round-robin, so each SM sub-partition has two independent
+    // epilogue instruction streams.  Thread-level epilogues whose checks need a whole row
+    // (generic Nt, smem verdict records) run on the h = 0 warps only.
+    const int et = threadIdx.x - EPI_WARP0 * 32;    // 0..255
+    const int q = warp & 3;                          // TMEM lane quadrant of this warp
+    const int h = (warp - EPI_WARP0) >> 2;           // chunk parity handled by this warp
+    const int row = q * 32 + lane;                   // tile row == TMEM lane
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const bool split = p.epi_split != 0;
+    const int c_first = split ? h * 32 : (h == 0 ? 0 : 0x7fffffff);
+    const int c_step = split ? 64 : 32;
     double rhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
-    int sbuf = 0;                                   // output staging buffer of this warp (double-buffered)
-    uint8_t* my_stage = out_stage + q * 8192;
+    int sbuf = 0;
+    uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * 4096;
     int t_local = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
@@ -619,16 +628,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][2] = gtimer();
       const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * p.cols_per_acc);
 
-      if (has_ck && !(p.debug & 2)) {
-        // checksum column per (row, group) -> cks[g][row] (groups <= 32)
+      if (has_ck && !(p.debug & 2) && c_first < p.bn_eff) {
+        // checksum column per (row, group) of the groups this warp handles -> cks[slot][row]
         float hi[32], lo[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + bn, hi);
         if (p.split) ptx::tmem_ld32(tacc + bn + p.groups, lo);
         ptx::tmem_ld_wait();
+        if (split) {
+          constexpr int GPC = NT > 0 ? 32 / NT : 1;    // groups per 32-column chunk
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < p.groups) cks[j * BM + row] = p.split ? hi[j] + lo[j] : hi[j];
+          for (int j = 0; j < 32; ++j) {
+            const int chunk = j / GPC;
+            if (j < p.groups && (chunk & 1) == h)
+              cks[(h * 16 + (chunk >> 1) * GPC + j % GPC) * BM + row] = p.split ? hi[j] + lo[j] : hi[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < p.groups) cks[j * BM + row] = p.split ? hi[j] + lo[j] : hi[j];
+        }
+        __syncwarp();
       }
 
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
@@ -640,7 +660,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int cnt = 0, g = 0;
       float tsum = 0.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < p.bn_eff; c0 += 32) {
+      for (int c0 = c_first; c0 < p.bn_eff; c0 += c_step) {
+        if (p.debug & 32768) break;      // bring-up: epilogue does nothing but hand TMEM back
         float v[32], sh[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
@@ -653,15 +674,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.debug & 16) {
         } else if constexpr (thread_level && NT > 0) {
           // static group structure: 32 / NT complete groups per chunk (NT divides 32 and bn_eff)
+          constexpr int GPC = 32 / NT;
+          const int slot0 = split ? h * 16 + (c0 >> 6) * GPC : c0 / NT;
 #pragma unroll
-          for (int gi = 0; gi < 32 / NT; ++gi) {
+          for (int gi = 0; gi < GPC; ++gi) {
             if (gi * NT < cmax) {
               const int gg = c0 / NT + gi;
               float x, y = 0.f;
               if constexpr (has_ck) {
 #pragma unroll
                 for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
-                x = cks[gg * BM + row];
+                x = cks[(slot0 + gi) * BM + row];
               } else {
                 if (p.scheme == ABFT_REPL_FULL) {
                   float bk = -FLT_MAX;
@@ -721,7 +744,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
         }
-        if (p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) {
+        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
           // ReLU + rounding to the storage grid (checksum.py:235 storage_array(activation(c)))
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -729,22 +752,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             v[j] = round_out(y, p.out_dtype);
           }
           if (p.tma_store) {
-            // stage 128-byte row segments (32 fp32 or 64 16-bit columns) in SW128 order, then one
-            // elected lane writes the [32 rows x 128 B] box with a bulk tensor store
-            const bool f32 = p.out_dtype == ABFT_OUT_F32;
-            const int half = f32 ? 0 : ((c0 >> 5) & 1);
-            uint8_t* buf = my_stage + sbuf * 4096;
-            if (half == 0) {
-              if (lane == 0) ptx::bulk_wait_read<1>();
+            // stage the warp's [32 rows x 32 columns] in the TMA swizzle order (fp32: 128-byte
+            // rows, SW128; 16-bit: 64-byte rows, SW64), then one lane issues the bulk store
+            if (p.out_dtype == ABFT_OUT_F32) {
+              if (lane == 0) ptx::bulk_wait_read<0>();
               __syncwarp();
-            }
-            uint8_t* rowp = buf + lane * 128;
-            if (f32) {
+              uint8_t* rowp = my_stage + lane * 128;
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
+              if (lane == 0) ptx::bulk_wait_read<1>();
+              __syncwarp();
+              uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 uint4 u;
@@ -752,21 +773,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
                 u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
                 u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
-                *reinterpret_cast<uint4*>(rowp + (((half * 4 + j) ^ (lane & 7)) << 4)) = u;
+                *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
               }
             }
-            if (f32 || half == 1) {
-              ptx::fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_2d(&tmC, buf, gc0 - (f32 ? 0 : 32), m0 + q * 32);
-                ptx::bulk_commit();
-              }
-              sbuf ^= 1;
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0, m0 + q * 32);
+              ptx::bulk_commit();
             }
-          } else {
-          const bool full_chunk = (cmax >= 32) && (gc0 + 32 <= p.N);
-          if (row_store && p.out_dtype != ABFT_OUT_NONE) {
+            sbuf ^= 1;
+          } else if (row_store && p.out_dtype != ABFT_OUT_NONE) {
+            const bool full_chunk = (cmax >= 32) && (gc0 + 32 <= p.N);
             if (p.out_dtype == ABFT_OUT_F32) {
               float* dst = reinterpret_cast<float*>(p.C) + (long long)gm * p.ldc + gc0;
               if (full_chunk && (p.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -796,7 +814,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   if (j < cmax && gc0 + j < p.N) dst[j] = TR::from_f(v[j]);
               }
             }
-          }
           }
           if (p.next_colck != nullptr) {
 #pragma unroll
@@ -830,7 +847,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       if (row_in_tile) rhs_acc += (double)tsum;
 
-      if (thread_level && !p.shuffle_verdicts) {
+      if (thread_level && !p.shuffle_verdicts && h == 0) {
         ptx::named_bar_sync(1, 128);
         tile_verdicts_smem(p, rec, et, m0, n0);
         ptx::named_bar_sync(1, 128);
@@ -843,13 +860,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       if (lane == 0) red_d[et >> 5] = x;
-      ptx::named_bar_sync(1, 128);
-      if (et == 0) atomicAdd(p.out_sum, red_d[0] + red_d[1] + red_d[2] + red_d[3]);
+      ptx::named_bar_sync(3, 256);
+      if (et == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 8; ++w) tot += red_d[w];
+        atomicAdd(p.out_sum, tot);
+      }
     }
     if (p.tma_store && lane == 0) ptx::bulk_wait_all();
     if (p.next_colck != nullptr && p.colck_in_smem) {
-      ptx::named_bar_sync(1, 128);
-      for (int i = col_lo + et; i < col_hi; i += 128) {
+      ptx::named_bar_sync(3, 256);
+      for (int i = col_lo + et; i < col_hi; i += 256) {
         const float x = colck_s[i];
         if (x != 0.f) atomicAdd(&p.next_colck[i], x);
       }
@@ -950,7 +971,8 @@ int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb,
   return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, mo, p, smem, grid, st);
 }
 
-// output map for the bulk tensor stores: dims {N, M}, box {128 B of columns, 32 rows}, SW128
+// output map for the bulk tensor stores: dims {N, M}, box {32 columns, 32 rows}; fp32 rows are
+// 128 B (SW128), 16-bit rows 64 B (SW64)
 int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a) {
   auto enc = get_encode_fn();
   if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -960,10 +982,11 @@ int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a) {
                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   cuuint64_t dims[2] = {(cuuint64_t)a->N, (cuuint64_t)a->M};
   cuuint64_t strides[1] = {(cuuint64_t)(a->ldc * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+  cuuint32_t box[2] = {32u, 32u};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, a->C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled(C) failed with CUresult " + std::to_string((int)r));
   return ABFT_OK;
 }
@@ -1106,12 +1129,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     // bulk tensor stores of the output: whole 128-row tiles, 128-byte row units (32 fp32 / 64
     // 16-bit columns) that tile bn_eff exactly, 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
-    const int unit = 128 / esz;
-    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % unit == 0 &&
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 32 == 0 &&
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
                    !(dbg_env & 8192)) ? 1 : 0;
   }
-  const uint32_t out_bytes = p.tma_store ? 4u * 8192u : 0u;
+  const uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
+  // chunks split across both warps of a quadrant unless a check needs whole rows in one warp
+  p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) && !(dbg_env & 65536) ? 1 : 0;
   p.a_colck = (a->scheme == ABFT_GLOBAL || as_plain) ? a->a_colck : nullptr;
   if (p.a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;

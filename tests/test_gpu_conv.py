@@ -95,9 +95,9 @@ def test_conv_binary16_outputs_and_flags(P, case):
         rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme),
                        faults=[P.OutputFault(row=row, col=col, delta=delta)], dtype=P.BINARY16)
         _, ref_v = O.execute(cols, wmat, O.Tiling(), scheme, [("output", row, col, delta)], "binary16")
-        # the reference's tau = 2^-10 * K * max(|lhs|, |rhs|, 1) can never fire for K >= 1024
+        # the reference tau 2^-10 * K * max(|lhs|, |rhs|, 1) (global AND per-row) cannot fire for K >= 1024
         assert rep.detected == any(v.detected for v in ref_v)
-        if scheme == "thread-one-sided" or c * r * s < 1024:
+        if c * r * s < 1024:
             assert rep.detected is True
         if scheme == "thread-one-sided":
             assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \

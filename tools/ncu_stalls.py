@@ -1,0 +1,32 @@
+"""Stall-reason breakdown of the SASS lines executed exactly `ex` times (one code region) in an ncu report.
+usage: python tools/ncu_stalls.py REP [ex ...]   (no ex: list the most-sampled execution counts)"""
+import csv, subprocess, sys
+from collections import defaultdict
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr = rows[1]
+body = [r for r in rows[2:] if len(r) == len(hdr)]
+iex, ist, isrc = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
+stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+if len(sys.argv) == 2:
+    agg = defaultdict(lambda: [0, 0])
+    for r in body:
+        agg[int(r[iex] or 0)][0] += int(r[ist] or 0)
+        agg[int(r[iex] or 0)][1] += 1
+    for ex, (st, n) in sorted(agg.items(), key=lambda x: -x[1][0])[:12]:
+        print(f"ex={ex:9d} samples={st:6d} instructions={n}")
+    sys.exit()
+for ex in map(int, sys.argv[2:]):
+    tot = defaultdict(int)
+    top = []
+    for r in body:
+        if int(r[iex] or 0) != ex:
+            continue
+        for i in stall_cols:
+            tot[hdr[i]] += int(r[i] or 0)
+        top.append((int(r[ist] or 0), r[isrc][:80]))
+    print(f"ex={ex}: " + ", ".join(f"{k[6:]}={v}" for k, v in sorted(tot.items(), key=lambda x: -x[1]) if v))
+    for st, src in sorted(top, reverse=True)[:12]:
+        print(f"   {st:5d}  {src}")
