@@ -106,6 +106,12 @@ struct ElemTraits<__half> {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+  // round-to-nearest pack with the ReLU clamp folded into the conversion
+  static __device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
+  }
 };
 template <>
 struct ElemTraits<__nv_bfloat16> {
@@ -117,6 +123,11 @@ struct ElemTraits<__nv_bfloat16> {
   static __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
   }
 };
 
@@ -745,16 +756,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
         }
         if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
-          // ReLU + rounding to the storage grid (checksum.py:235 storage_array(activation(c)))
+          // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
+          // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
+          const bool relu_in_pack = p.relu && p.tma_store && p.out_dtype != ABFT_OUT_F32;
+          if (p.relu && !relu_in_pack) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float y = p.relu ? fmaxf(v[j], 0.f) : v[j];
-            v[j] = round_out(y, p.out_dtype);
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+          }
+          if (p.next_colck != nullptr && p.out_dtype != ABFT_OUT_F32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = round_out(v[j], p.out_dtype);
           }
           if (p.tma_store) {
             // stage the warp's [32 rows x 32 columns] in the TMA swizzle order (fp32: 128-byte
             // rows, SW128; 16-bit: 64-byte rows, SW64), then one lane issues the bulk store
-            if (p.out_dtype == ABFT_OUT_F32) {
+            if (p.debug & 131072) {
+              // bring-up: no staging, no store
+            } else if (p.out_dtype == ABFT_OUT_F32) {
               if (lane == 0) ptx::bulk_wait_read<0>();
               __syncwarp();
               uint8_t* rowp = my_stage + lane * 128;
@@ -766,21 +784,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (lane == 0) ptx::bulk_wait_read<1>();
               __syncwarp();
               uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
+              if (relu_in_pack) {
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                uint4 u;
-                u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
-                u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
-                u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
-                u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
-                *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+                for (int j = 0; j < 4; ++j) {
+                  uint4 u;
+                  u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
+                  u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
+                  u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
+                  u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
+                  *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  uint4 u;
+                  u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+                  u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+                  u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+                  u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+                  *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+                }
               }
             }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0, m0 + q * 32);
-              ptx::bulk_commit();
+            if (!(p.debug & (131072 | 262144))) {
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0,
+                                  m0 + q * 32);
+                ptx::bulk_commit();
+              }
             }
             sbuf ^= 1;
           } else if (row_store && p.out_dtype != ABFT_OUT_NONE) {
