@@ -68,6 +68,10 @@ struct GemmParams {
   uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_out, off_acolck, off_bar;
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
+  int acolck_mode;       // 1: column sums on the tensor cores (ones x A-tile MMA into TMEM), 2: CUDA cores
+  int dck_col;           // TMEM column of the two 64-column column-sum buffers (mode 1)
+  uint32_t off_ones;     // smem [64 x 128 B] tile of ones (mode 1)
+  uint32_t idesc_ones;
   int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
   int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
@@ -316,7 +320,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = bars + 2 * p.stages;
   uint64_t* tfull = bars + 3 * p.stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* dfull = tempty + 2;     // column-sum TMEM buffers (acolck_mode 1)
+  uint64_t* dempty = dfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
   double* red_d = reinterpret_cast<double*>(tmem_holder + 4);
 
   const int warp = threadIdx.x >> 5;
@@ -334,9 +340,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < p.stages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
-      ptx::mbar_init(&empty[s], p.a_colck != nullptr ? 5 : 1);   // + one arrival per A-checksum warp
+      ptx::mbar_init(&empty[s], p.acolck_mode == 2 ? 5 : 1);   // + one arrival per CUDA-core A-checksum warp
     }
     for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&dfull[a], 1);
+      ptx::mbar_init(&dempty[a], 1);
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 8);    // one arrival per epilogue warp
     }
@@ -354,6 +362,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp >= CK_WARP0 && p.acolck_in_smem) {
     for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128) acolck_s[i] = 0.f;
+  }
+  if (warp >= CK_WARP0 && p.acolck_mode == 1) {
+    // [64 x 64] ones operand of the column-sum MMA (any layout reads as all ones)
+    const uint32_t one2 = ElemTraits<T>::pack2(1.f, 1.f);
+    uint4* o = reinterpret_cast<uint4*>(smem + p.off_ones);
+    for (int i = threadIdx.x - CK_WARP0 * 32; i < 512; i += 128) o[i] = make_uint4(one2, one2, one2, one2);
+    ptx::fence_proxy_async_smem();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -427,8 +442,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int s = 0, ps = 0;
       uint32_t ph = 0, pph = 0;
+      int db = 0;
+      uint32_t dph = 0;
       int t_local = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+        const bool count_tile = (tile % p.num_n_blocks) == 0;
         const int acc = t_local % p.acc_stages;
         const uint32_t aph = (uint32_t)(t_local / p.acc_stages) & 1u;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -449,6 +467,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mma_f16_ss(d, adesc, bdesc, p.idesc_main, accum);
             if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
             if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
+          }
+          if (p.acolck_mode == 1 && count_tile) {
+            // colck[kb*64 + j] += sum_rows A_tile[row][j]: ones[64 x 128 rows] x A_tile (MN-major B)
+            ptx::mbar_wait(&dempty[db], dph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t dd = tmem_base + (uint32_t)(p.dck_col + db * 64);
+            const uint64_t odesc = ptx::desc_kmajor_sw128(ptx::smem_u32(smem + p.off_ones));
+#pragma unroll
+            for (int r = 0; r < BM / 16; ++r) {
+              const uint64_t bdesc2 = a_none ? ptx::desc_mnmajor_none(a_addr + r * 256, 128, 2048)
+                                             : ptx::desc_mnmajor_sw128(a_addr + r * 2048, 1024);
+              ptx::mma_f16_ss(dd, odesc, bdesc2, p.idesc_ones, r > 0 ? 1u : 0u);
+            }
+            ptx::mma_commit(&dfull[db]);
+            db ^= 1;
+            if (db == 0) dph ^= 1;
           }
           if (ck_onchip) {
             if (kb > 0) {
@@ -538,6 +572,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) ptx::mbar_arrive(&ckfull[s]);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
+      }
+    } else if (p.acolck_mode == 1) {
+      // ------------------- global: activation column checksum, tensor-core partials
+      // warp 12 (TMEM lane quadrant 0) drains each k-block's 64 column sums from TMEM
+      if (warp == CK_WARP0 + 2) {
+        int db = 0;
+        uint32_t dph = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+          if ((tile % p.num_n_blocks) != 0) continue;
+#pragma unroll 1
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            ptx::mbar_wait(&dfull[db], dph);
+            ptx::tc_fence_after();
+            float c0v[32], c1v[32];
+            const uint32_t ta = tmem_base + (uint32_t)(p.dck_col + db * 64);
+            ptx::tmem_ld32(ta, c0v);
+            ptx::tmem_ld32(ta + 32, c1v);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&dempty[db]);
+            if (lane == 0) {
+              // every row of the ones-product holds the same sums: lane 0's row is enough
+              const int k0 = kb * BK;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (k0 + j < p.K && c0v[j] != 0.f) {
+                  if (p.acolck_in_smem) acolck_s[k0 + j] += c0v[j];
+                  else atomicAdd(&p.a_colck[k0 + j], c0v[j]);
+                }
+                if (k0 + 32 + j < p.K && c1v[j] != 0.f) {
+                  if (p.acolck_in_smem) acolck_s[k0 + 32 + j] += c1v[j];
+                  else atomicAdd(&p.a_colck[k0 + 32 + j], c1v[j]);
+                }
+              }
+            }
+            db ^= 1;
+            if (db == 0) dph ^= 1;
+          }
+        }
+        __syncwarp();
+        if (p.acolck_in_smem)
+          for (int i = lane; i < p.K; i += 32)
+            if (acolck_s[i] != 0.f) atomicAdd(&p.a_colck[i], acolck_s[i]);
       }
     } else if (p.a_colck != nullptr) {
       // ------------------------------------- global: activation column checksum
@@ -758,7 +836,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
-          const bool relu_in_pack = p.relu && p.tma_store && p.out_dtype != ABFT_OUT_F32;
+          const bool relu_in_pack = p.relu && p.tma_store && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr;
           if (p.relu && !relu_in_pack) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
@@ -1066,6 +1144,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
       return fail(ABFT_E_SHAPE, "m_ext/n_ext must cover M/N and be multiples of the thread tile");
   }
   const int split = (has_ck && a->ck_split) ? 1 : 0;
+  // global scheme with the activation checksum: 2 x 64 TMEM columns for the column-sum MMA
+  const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
+  const int extra_cols = want_acolck ? 128 : 0;
   const int sms = a->num_sms > 0 ? a->num_sms : num_sms();
   const int bm_eff = (BM / mt) * mt;
   const int m_blocks = ceil_div(m_ext, bm_eff);
@@ -1082,8 +1163,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
         if (cand > 32 && cand / 2 >= round_up(n_ext, 32) && cand != 64) continue;   // far wider than needed
         if (cand == 32 && n_ext > 32 && nt <= 64 && cand * 2 <= 32 * nt) continue;  // 64 is the narrowest efficient tile
         const int cols = tile_cols(cand, nt, has_ck, has_shadow, split);
-        if (cols > 512) continue;
-        if (pass == 0 && 2 * cols > 512) continue;                                   // pass 0: double-buffered only
+        if (cols + extra_cols > 512) continue;
+        if (pass == 0 && 2 * cols + extra_cols > 512) continue;                      // pass 0: double-buffered only
         const int eff = (cand / nt) * nt;
         if (best == 0 && (long long)m_blocks * ceil_div(n_ext, eff) >= sms) best = cand;
         smallest = cand;
@@ -1116,8 +1197,11 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split);
   p.shadow_off = bn + p.nck_pad;
   if (p.cols_per_acc > 512) return fail(ABFT_E_UNSUPPORTED, "TMEM budget exceeded");
-  p.acc_stages = (2 * p.cols_per_acc <= 512) ? 2 : 1;
-  p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
+  p.acc_stages = (2 * p.cols_per_acc + extra_cols <= 512) ? 2 : 1;
+  p.acolck_mode = 0;
+  if (want_acolck) p.acolck_mode = (p.acc_stages * p.cols_per_acc + extra_cols <= 512) ? 1 : 2;
+  p.dck_col = p.acc_stages * p.cols_per_acc;
+  p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc + (p.acolck_mode == 1 ? 128 : 0)));
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
   p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : 0;
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
@@ -1134,6 +1218,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = has_ck ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
+  p.idesc_ones = ptx::idesc_f16(fmt, 64, 64) | (1u << 16);   // M=64, N=64, B MN-major
   {
     const char* dbg = getenv("ABFT_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
@@ -1169,13 +1254,14 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
   // chunks split across both warps of a quadrant unless a check needs whole rows in one warp
   p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) && !(dbg_env & 65536) ? 1 : 0;
+  if (a->a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
   p.a_colck = (a->scheme == ABFT_GLOBAL || as_plain) ? a->a_colck : nullptr;
-  if (p.a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
   const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : 0u;
+  const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
   const uint32_t extras =
-      cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + out_bytes + acolck_bytes + bar_bytes;
+      cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + out_bytes + acolck_bytes + ones_bytes + bar_bytes;
   const uint32_t stage_bytes = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes;
   int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
   if (const char* cap = getenv("ABFT_SMEM_CAP")) budget = std::min(budget, atoi(cap) * 1024 - (int)extras);
@@ -1190,7 +1276,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.off_stage = p.off_rec + rec_bytes;
   p.off_colck = p.off_stage + stage_bytes_ep;
   p.off_out = p.off_colck + colck_bytes;
-  p.off_acolck = p.off_out + out_bytes;
+  p.off_ones = p.off_out + out_bytes;                 // 1024-aligned (all earlier sizes are)
+  p.off_acolck = p.off_ones + ones_bytes;
   p.off_bar = p.off_acolck + acolck_bytes;
   out.smem = (size_t)p.off_bar + bar_bytes + 1024;
   out.grid = std::min(p.num_tiles, sms);

@@ -175,6 +175,40 @@ def make_select_cases(cost, shapes, tiled):
     return out
 
 
+def make_campaign_cases(shapes, tiled):
+    """Per-trial outcomes of the reference campaign (campaign.py:227-259) for parity of the
+    GPU campaign: the trial draws (shape, delta, fault) and detected / masked / missed."""
+    sys.path.insert(0, REF)
+    from abft_guard import campaign as C
+    out = []
+    schemes = tuple(s for s in tiled.Scheme if s is not tiled.Scheme.UNPROTECTED)
+    for dtype, delta, seed, ntr in ((shapes.EXACT_INT, C.INT_DELTAS, 20240601, 40),
+                                    (shapes.BINARY16, C.FP_DELTAS, 7, 40)):
+        cfg = C.CampaignConfig(trials=ntr, seed=seed, gemm_min=8, gemm_max=24, schemes=schemes, dtype=dtype,
+                               delta=delta, control_trials=ntr)
+        for si, sch in enumerate(schemes):
+            for t in range(ntr):
+                rng = C._trial_rng(seed, si, 0, t)
+                shape = shapes.GemmShape(m=int(rng.integers(8, 25)), n=int(rng.integers(8, 25)),
+                                        k=int(rng.integers(8, 25)))
+                a, b = C.random_matrices(rng, shape, dtype)
+                d = delta.sample(rng)
+                site = C.SITE_OUTPUT if rng.integers(2) else C.SITE_THREAD_MMA
+                f = (tiled.random_output_fault(rng, shape, d) if site == C.SITE_OUTPUT
+                     else tiled.random_thread_mma_fault(rng, shape, cfg.tiling, d))
+                rep = tiled.execute(a, b, cfg.tiling, sch, faults=[f], dtype=dtype)
+                tau = C._fault_tolerance(rep, f, cfg.tiling)
+                detected, masked = C._run_injected_trial(cfg, sch, si, t)
+                outcome = "detected" if detected else ("masked" if masked else "missed")
+                fdesc = (["output", f.row, f.col, float(f.delta)] if isinstance(f, tiled.OutputFault) else
+                         ["thread-mma", f.thread_row, f.thread_col, f.step, f.local_index, float(f.delta)])
+                out.append(dict(dtype=dtype.tag.value, seed=seed, scheme=sch.value, scheme_index=si, trial=t,
+                                shape=[shape.m, shape.n, shape.k], delta=float(d), fault=fdesc,
+                                outcome=outcome, tau=float(tau),
+                                control_flagged=bool(C._run_control_trial(cfg, sch, si, t))))
+    return out
+
+
 def _save(cases, path):
     arrays, metas = {}, []
     for i, (meta, arrs) in enumerate(cases):
@@ -192,6 +226,8 @@ def main():
     _save(make_pipeline_cases(checksum, shapes), os.path.join(HERE, "pipeline_cases"))
     with open(os.path.join(HERE, "select_cases.json"), "w") as fh:
         json.dump(make_select_cases(cost, shapes, tiled), fh, indent=0, sort_keys=True)
+    with open(os.path.join(HERE, "campaign_cases.json"), "w") as fh:
+        json.dump(make_campaign_cases(shapes, tiled), fh, indent=0, sort_keys=True)
     print("golden fixtures written to", HERE)
 
 

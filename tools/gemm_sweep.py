@@ -26,6 +26,7 @@ def run(m, n, k):
     pw = D.prepare_weight(b, P.BINARY16)
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
     osum = torch.zeros(1, dtype=torch.float64, device="cuda")
+    acol = torch.zeros(k, dtype=torch.float32, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     base = dict(out=out, ldc=n, out_kind="f16", relu=True)
     one = dict(base, fired_count=cnt, m_ext=-(-m // 16) * 16, n_ext=-(-n // 8) * 8)
@@ -39,7 +40,7 @@ def run(m, n, k):
     res["unprot"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                        P.Scheme.UNPROTECTED, **base), it)
     res["global"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
-                                                       P.Scheme.GLOBAL_ABFT, out_sum=osum, **base), it)
+                                                       P.Scheme.GLOBAL_ABFT, out_sum=osum, a_colck=acol, **base), it)
     res["one_chip"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                          P.Scheme.THREAD_ONE_SIDED, **one), it)
     res["one_off"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
