@@ -81,7 +81,7 @@ typedef struct {
   int32_t* fired_count;                 /* optional: number of thread tiles whose check fired */
   int32_t* fired;                       /* optional [fired_cap x 2] (t_row, t_col) of fired tiles */
   int32_t fired_cap;
-  int32_t tile_n;                       /* CTA N tile: 0 = auto, else 32/64/128/192/256 */
+  int32_t tile_n;                       /* CTA N tile: 0 = auto, else 32/64/128/192/224/256 */
   int32_t num_sms;                      /* persistent grid size cap: 0 = all SMs */
   /* optional checksum rows prepared offline by abft_ck_rows for THIS call's plan; when null the
    * checksum warps generate them on chip from each B^T tile (one-sided / two-sided only) */

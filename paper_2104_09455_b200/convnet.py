@@ -62,14 +62,18 @@ class LayerRunner:
         self.offline_ck = offline_ck
         for s in (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED):
             self._args[s] = self._make_args(s)
+        # global scheme with the activation checksum from a separate pass instead of in-kernel
+        self._args["global-standalone"] = self._make_args(Scheme.GLOBAL_ABFT, fused_colck=False)
+        self.global_variant = "fused"
 
-    def _make_args(self, scheme: Scheme):
+    def _make_args(self, scheme: Scheme, fused_colck: bool = True):
         t = self.tiling
         kw = dict(out=self.out, ldc=self.n8, out_kind="bf16" if self.out.dtype == D.torch().bfloat16 else "f16",
                   relu=True)
         if scheme is Scheme.GLOBAL_ABFT:
             kw["out_sum"] = self.rhs
-            kw["a_colck"] = self.colck
+            if fused_colck:
+                kw["a_colck"] = self.colck
         elif scheme is Scheme.THREAD_ONE_SIDED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-self.m // t.thread_m) * t.thread_m,
                       n_ext=-(-self.spec.oc // t.thread_n) * t.thread_n,
@@ -88,11 +92,27 @@ class LayerRunner:
     def flops(self) -> int:
         return 2 * self.m * self.spec.oc * self.k_ref
 
-    def conv(self, scheme: Scheme) -> None:
+    def conv(self, scheme) -> None:
         kernels.conv2d(self._args[scheme])
 
+    def global_standalone(self) -> None:
+        """Global ABFT with the standalone checksum pass (the other measured variant)."""
+        self.colck_pass()
+        kernels.conv2d(self._args["global-standalone"])
+
+    @property
+    def pointwise(self) -> bool:
+        sp = self.spec
+        return sp.r == 1 and sp.s == 1 and sp.stride_h == 1 and sp.stride_w == 1 and sp.pad_h == 0 and sp.pad_w == 0
+
     def colck_pass(self) -> None:
-        kernels.conv_colck(self.x, self.geom, self.dtype, self.colck)
+        """Standalone activation checksum (one extra read of the input): the plain column
+        sum for a pointwise conv (its A is the NHWC matrix itself), the windowed one otherwise."""
+        if self.pointwise:
+            c8 = self.x.shape[3]
+            kernels.colsum(self.x, self.spec.n * self.spec.h * self.spec.w, c8, c8, self.dtype, self.colck)
+        else:
+            kernels.conv_colck(self.x, self.geom, self.dtype, self.colck)
 
     def verify(self) -> None:
         kernels.global_verify(self.task, 1, self.numeric, self.sums, out=self.verdict,
@@ -102,8 +122,11 @@ class LayerRunner:
         """One protected execution of the layer (verification included for global)."""
         if scheme is Scheme.GLOBAL_ABFT:
             kernels.zero(self.scratch)
-            kernels.zero(self.colck)
-            self.conv(scheme)
+            if self.global_variant == "fused":
+                kernels.zero(self.colck)
+                self.conv(scheme)
+            else:
+                self.global_standalone()
             self.verify()
         else:
             self.conv(scheme)

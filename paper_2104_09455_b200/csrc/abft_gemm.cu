@@ -44,6 +44,7 @@ constexpr int NUM_THREADS = 448;   // 14 warps
 constexpr int EPI_WARP0 = 2;       // warps 2-9: epilogue (two per TMEM lane quadrant)
 constexpr int CK_WARP0 = 10;       // warps 10-13: checksum rows / A-column checksum
 constexpr int COLCK_SMEM_MAX = 4096;
+constexpr int DCK_BUFS = 4;        // column-sum MMA results in flight (8 TMEM columns each)
 
 enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
 
@@ -320,9 +321,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = bars + 2 * p.stages;
   uint64_t* tfull = bars + 3 * p.stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* dfull = tempty + 2;     // column-sum TMEM buffers (acolck_mode 1)
-  uint64_t* dempty = dfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* dfull = tempty + 2;     // column-sum TMEM buffers (acolck_mode 1), DCK_BUFS deep
+  uint64_t* dempty = dfull + DCK_BUFS;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + DCK_BUFS);
   double* red_d = reinterpret_cast<double*>(tmem_holder + 4);
 
   const int warp = threadIdx.x >> 5;
@@ -342,9 +343,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
       ptx::mbar_init(&empty[s], p.acolck_mode == 2 ? 5 : 1);   // + one arrival per CUDA-core A-checksum warp
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < DCK_BUFS; ++a) {
       ptx::mbar_init(&dfull[a], 1);
-      ptx::mbar_init(&dempty[a], 1);
+      ptx::mbar_init(&dempty[a], 4);    // one arrival per checksum warp
+    }
+    for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 8);    // one arrival per epilogue warp
     }
@@ -469,20 +472,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
           }
           if (p.acolck_mode == 1 && count_tile) {
-            // colck[kb*64 + j] += sum_rows A_tile[row][j]: ones[64 x 128 rows] x A_tile (MN-major B)
+            // colck[kb*64 + j] += sum_rows A_tile[row][j] on the tensor cores:
+            // D'[64 x 8] = A_tile^T (M = the 64 columns, MN-major) x ones[8 x 128 rows]
             ptx::mbar_wait(&dempty[db], dph ^ 1);
             ptx::tc_fence_after();
-            const uint32_t dd = tmem_base + (uint32_t)(p.dck_col + db * 64);
+            const uint32_t dd = tmem_base + (uint32_t)(p.dck_col + db * 8);
             const uint64_t odesc = ptx::desc_kmajor_sw128(ptx::smem_u32(smem + p.off_ones));
 #pragma unroll
             for (int r = 0; r < BM / 16; ++r) {
-              const uint64_t bdesc2 = a_none ? ptx::desc_mnmajor_none(a_addr + r * 256, 128, 2048)
+              const uint64_t adesc2 = a_none ? ptx::desc_mnmajor_none(a_addr + r * 256, 128, 2048)
                                              : ptx::desc_mnmajor_sw128(a_addr + r * 2048, 1024);
-              ptx::mma_f16_ss(dd, odesc, bdesc2, p.idesc_ones, r > 0 ? 1u : 0u);
+              ptx::mma_f16_ss(dd, adesc2, odesc, p.idesc_ones, r > 0 ? 1u : 0u);
             }
             ptx::mma_commit(&dfull[db]);
-            db ^= 1;
-            if (db == 0) dph ^= 1;
+            if (++db == DCK_BUFS) { db = 0; dph ^= 1; }
           }
           if (ck_onchip) {
             if (kb > 0) {
@@ -575,47 +578,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     } else if (p.acolck_mode == 1) {
       // ------------------- global: activation column checksum, tensor-core partials
-      // warp 12 (TMEM lane quadrant 0) drains each k-block's 64 column sums from TMEM
-      if (warp == CK_WARP0 + 2) {
-        int db = 0;
-        uint32_t dph = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-          if ((tile % p.num_n_blocks) != 0) continue;
+      // D'[64 x 8] rows (= the k-block's 64 columns) sit in lanes 16q..16q+15 of quadrant q
+      // (the M=64 data-path layout); each checksum warp drains its quadrant's 16 rows.
+      const int q = warp & 3;
+      int db = 0;
+      uint32_t dph = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        if ((tile % p.num_n_blocks) != 0) continue;
 #pragma unroll 1
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            ptx::mbar_wait(&dfull[db], dph);
-            ptx::tc_fence_after();
-            float c0v[32], c1v[32];
-            const uint32_t ta = tmem_base + (uint32_t)(p.dck_col + db * 64);
-            ptx::tmem_ld32(ta, c0v);
-            ptx::tmem_ld32(ta + 32, c1v);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&dempty[db]);
-            if (lane == 0) {
-              // every row of the ones-product holds the same sums: lane 0's row is enough
-              const int k0 = kb * BK;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (k0 + j < p.K && c0v[j] != 0.f) {
-                  if (p.acolck_in_smem) acolck_s[k0 + j] += c0v[j];
-                  else atomicAdd(&p.a_colck[k0 + j], c0v[j]);
-                }
-                if (k0 + 32 + j < p.K && c1v[j] != 0.f) {
-                  if (p.acolck_in_smem) acolck_s[k0 + 32 + j] += c1v[j];
-                  else atomicAdd(&p.a_colck[k0 + 32 + j], c1v[j]);
-                }
-              }
-            }
-            db ^= 1;
-            if (db == 0) dph ^= 1;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          ptx::mbar_wait(&dfull[db], dph);
+          ptx::tc_fence_after();
+          const float x = ptx::tmem_ld1(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(p.dck_col + db * 8));
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&dempty[db]);
+          const int k = kb * BK + q * 16 + lane;
+          if (lane < 16 && k < p.K && x != 0.f) {
+            if (p.acolck_in_smem) acolck_s[k] += x;
+            else atomicAdd(&p.a_colck[k], x);
           }
+          if (++db == DCK_BUFS) { db = 0; dph ^= 1; }
         }
-        __syncwarp();
-        if (p.acolck_in_smem)
-          for (int i = lane; i < p.K; i += 32)
-            if (acolck_s[i] != 0.f) atomicAdd(&p.a_colck[i], acolck_s[i]);
+      }
+      if (p.acolck_in_smem) {
+        ptx::named_bar_sync(2, 128);
+        for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128)
+          if (acolck_s[i] != 0.f) atomicAdd(&p.a_colck[i], acolck_s[i]);
       }
     } else if (p.a_colck != nullptr) {
       // ------------------------------------- global: activation column checksum
@@ -1146,7 +1136,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const int split = (has_ck && a->ck_split) ? 1 : 0;
   // global scheme with the activation checksum: 2 x 64 TMEM columns for the column-sum MMA
   const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
-  const int extra_cols = want_acolck ? 128 : 0;
+  const int extra_cols = want_acolck ? 32 : 0;
   const int sms = a->num_sms > 0 ? a->num_sms : num_sms();
   const int bm_eff = (BM / mt) * mt;
   const int m_blocks = ceil_div(m_ext, bm_eff);
@@ -1158,7 +1148,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     // Thread-level schemes keep <= 32 checksum groups per tile.
     int best = 0, smallest = 0;
     for (int pass = 0; pass < 2 && best == 0; ++pass) {
-      for (int cand : {256, 192, 128, 64, 32}) {
+      for (int cand : {256, 224, 192, 128, 64, 32}) {
         if (cand < nt || (thread_level && cand / nt > 32)) continue;
         if (cand > 32 && cand / 2 >= round_up(n_ext, 32) && cand != 64) continue;   // far wider than needed
         if (cand == 32 && n_ext > 32 && nt <= 64 && cand * 2 <= 32 * nt) continue;  // 64 is the narrowest efficient tile
@@ -1174,8 +1164,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     bn = best;
     if (bn == 0) return fail(ABFT_E_UNSUPPORTED, "no CTA tile fits this thread tile");
   }
-  if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 256)
-    return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/192/256");
+  if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 224 && bn != 256)
+    return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/192/224/256");
   if (bn < nt) return fail(ABFT_E_UNSUPPORTED, "thread_n larger than the CTA tile");
 
   GemmParams& p = out.p;
@@ -1201,7 +1191,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.acolck_mode = 0;
   if (want_acolck) p.acolck_mode = (p.acc_stages * p.cols_per_acc + extra_cols <= 512) ? 1 : 2;
   p.dck_col = p.acc_stages * p.cols_per_acc;
-  p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc + (p.acolck_mode == 1 ? 128 : 0)));
+  p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc + (p.acolck_mode == 1 ? 32 : 0)));
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
   p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : 0;
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
@@ -1218,7 +1208,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = has_ck ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
-  p.idesc_ones = ptx::idesc_f16(fmt, 64, 64) | (1u << 16);   // M=64, N=64, B MN-major
+  p.idesc_ones = ptx::idesc_f16(fmt, 64, 8) | (1u << 15);    // M=64, N=8, A MN-major
   {
     const char* dbg = getenv("ABFT_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
