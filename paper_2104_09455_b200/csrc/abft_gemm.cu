@@ -1143,23 +1143,25 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
 
   int bn = a->tile_n;
   if (bn == 0) {
-    // largest tile that still gives >= one tile per SM, preferring TMEM double buffering;
-    // otherwise the narrowest efficient tile (max parallelism for bandwidth-bound layers).
+    // Wave-quantised cost model over the legal tiles (TMEM double buffering required unless no
+    // tile allows it): waves x per-tile cost, a tile costing its operand bytes per k-block
+    // (128 A rows + bn B rows + checksum rows) and its epilogue (~bn); ties go to the wider tile.
     // Thread-level schemes keep <= 32 checksum groups per tile.
-    int best = 0, smallest = 0;
+    int best = 0;
     for (int pass = 0; pass < 2 && best == 0; ++pass) {
+      long long best_cost = 0;
       for (int cand : {256, 224, 192, 128, 64, 32}) {
         if (cand < nt || (thread_level && cand / nt > 32)) continue;
-        if (cand > 32 && cand / 2 >= round_up(n_ext, 32) && cand != 64) continue;   // far wider than needed
-        if (cand == 32 && n_ext > 32 && nt <= 64 && cand * 2 <= 32 * nt) continue;  // 64 is the narrowest efficient tile
         const int cols = tile_cols(cand, nt, has_ck, has_shadow, split);
         if (cols + extra_cols > 512) continue;
         if (pass == 0 && 2 * cols + extra_cols > 512) continue;                      // pass 0: double-buffered only
         const int eff = (cand / nt) * nt;
-        if (best == 0 && (long long)m_blocks * ceil_div(n_ext, eff) >= sms) best = cand;
-        smallest = cand;
+        const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
+        const long long waves = (tiles + sms - 1) / sms;
+        const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : 0;
+        const long long cost = waves * (128 + 2LL * cand + nck);
+        if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
       }
-      if (best == 0 && pass == 0 && smallest != 0) best = smallest;
     }
     bn = best;
     if (bn == 0) return fail(ABFT_E_UNSUPPORTED, "no CTA tile fits this thread tile");
