@@ -173,15 +173,26 @@ typedef struct {
   abft_gemm_args_t gemm;
   int32_t n, h, w, c;
   int32_t r, s, stride_h, stride_w, pad_h, pad_w;
+  int32_t c_real;          /* the model's input channels (<= c; 0 = c) */
+  void* workspace;         /* explicit-im2col mode only: >= plan out[6] bytes, 16-byte aligned */
+  int64_t ws_bytes;
 } abft_conv_args_t;
 
 int abft_conv2d(const abft_conv_args_t* args, void* stream);
-/* out[0] A-load mode (0 GEMM, 1 im2col 64-channel chunks, 2 im2col 8-channel chunks),
- * [1] packed-weight channel stride, [2] P, [3] Q, [4] K = r*s*c, [5] M = n*P*Q */
-int abft_conv_plan(const abft_conv_args_t* args, int32_t* out /*[6]*/);
-/* torch-layout weight [OC][cin][r][s] -> K-major [OC][(r, s, ck)], channels >= cin zero */
+/* The kernel plan of a conv (no launch):
+ *   out[0] A-load mode: 0 = plain GEMM of the NHWC matrix (1x1, stride 1, pad 0);
+ *          1 = TMA im2col, 64-channel columns (channels zero-padded to a multiple of 64);
+ *          2 = TMA im2col, 8-channel columns;
+ *          3 = explicit im2col into the workspace, then the plain GEMM (few input channels,
+ *              e.g. network stems, where K = r*s*c_real is packed densely)
+ *   out[1] packed-weight channel stride ck, out[2] P, out[3] Q,
+ *   out[4] K of the GEMM (r*s*ck, or round8(r*s*c_real) in mode 3), out[5] M = n*P*Q,
+ *   out[6] workspace bytes (mode 3) */
+int abft_conv_plan(const abft_conv_args_t* args, int32_t* out /*[8]*/);
+/* torch-layout weight [OC][cin][r][s] -> K-major [OC][ldo] with element (r, s, c) at
+ * (r*s_ + s)*ck + c, channels >= cin and columns >= r*s*ck zero (ldo >= r*s*ck) */
 int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin, int32_t r, int32_t s, int32_t ck, void* out,
-                          void* stream);
+                          int64_t ldo, void* stream);
 /* windowed activation checksum of the conv's im2col matrix, out[(ri*s + si)*c + ch]
  * (column_checksum of the lowered A, checksum.py:90-96), fp32; accumulate != 0 adds */
 int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w, int32_t c, int32_t r, int32_t s,

@@ -96,7 +96,8 @@ class ConvArgs(ctypes.Structure):
     _fields_ = [("gemm", GemmArgs),
                 ("n", ctypes.c_int32), ("h", ctypes.c_int32), ("w", ctypes.c_int32), ("c", ctypes.c_int32),
                 ("r", ctypes.c_int32), ("s", ctypes.c_int32), ("stride_h", ctypes.c_int32),
-                ("stride_w", ctypes.c_int32), ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32)]
+                ("stride_w", ctypes.c_int32), ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32),
+                ("c_real", ctypes.c_int32), ("workspace", ctypes.c_void_p), ("ws_bytes", ctypes.c_int64)]
 
 
 class GlobalTask(ctypes.Structure):
@@ -123,7 +124,7 @@ def _declare(lib):
     lib.abft_verify_sums.argtypes = [vp, vp, i32, i32, vp, vp, vp]
     lib.abft_conv2d.argtypes = [ctypes.POINTER(ConvArgs), vp]
     lib.abft_conv_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]
-    lib.abft_conv_pack_weight.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp]
+    lib.abft_conv_pack_weight.argtypes = [vp, i32, i32, i32, i32, i32, vp, i64, vp]
     lib.abft_conv_colck.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, i32, vp]
     lib.abft_last_error.restype = ctypes.c_char_p
     for name in EXPORTED_SYMBOLS:

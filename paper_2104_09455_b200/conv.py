@@ -36,31 +36,43 @@ def _up(x: int, q: int) -> int:
 class PreparedConv:
     """A conv weight in the kernel layout plus its offline row checksum (checksum.py:175-187)."""
 
-    bt: object          # [OC x r*s*ck] K-major
-    rowck: object       # [r*s*ck] fp32
+    bt: object          # [OC x K] K-major, element (r, s, c) at (r*S + s)*ck + c
+    rowck: object       # [K] fp32
     oc: int
     cin: int            # the model's input channels (K = cin*r*s in the reference lowering)
-    ck: int             # physical channels of the NHWC input (multiple of 8)
+    ck: int             # channel stride of the packed weight (plan out[1])
     r: int
     s: int
     dtype: DType
 
 
-def prepare_conv_weight(weight, dtype: DType, ck: int | None = None) -> PreparedConv:
-    """torch-layout weight [OC, C, R, S] (numpy or torch) -> PreparedConv on the device."""
+def geometry(x_dev, r: int, s: int, stride, padding, cin: int) -> dict:
+    sh, sw = (stride, stride) if np.isscalar(stride) else stride
+    ph, pw = (padding, padding) if np.isscalar(padding) else padding
+    n, h, w, c = (int(v) for v in x_dev.shape)
+    if cin > c:
+        raise ShapeMismatchError(f"weights have {cin} input channels, the activation only {c}")
+    return dict(n=n, h=h, w=w, c=c, r=int(r), s=int(s), stride_h=int(sh), stride_w=int(sw), pad_h=int(ph),
+                pad_w=int(pw), c_real=int(cin))
+
+
+def plan(x_dev, geom: dict, oc: int, dtype: DType) -> dict:
+    """abft_conv_plan for this input / geometry: A-load mode, packed-weight layout, workspace."""
+    return kernels.conv_plan(kernels.conv_args(x_dev, geom, None, oc, dtype, D.numeric_code(dtype)))
+
+
+def prepare_conv_weight(weight, dtype: DType, ck: int, k_pitch: int) -> PreparedConv:
+    """torch-layout weight [OC, C, R, S] (numpy or torch) -> PreparedConv with the plan's layout."""
     t = D.torch()
     if len(tuple(weight.shape)) != 4:
         raise ShapeMismatchError(f"conv weight must be [OC, C, R, S], got {tuple(weight.shape)}")
     oc, cin, r, s = (int(v) for v in weight.shape)
-    ck = ck or D.round8(cin)
-    if ck < cin or ck % 8:
-        raise ShapeMismatchError(f"physical channels {ck} must cover {cin} and be a multiple of 8")
     sd = D.torch_storage_dtype(dtype)
     if D.is_torch(weight):
         w = weight.to(device="cuda", dtype=sd).contiguous()
     else:
         w = t.from_numpy(np.ascontiguousarray(np.asarray(weight).astype(np.float32))).to("cuda").to(sd)
-    bt = kernels.conv_pack_weight(w, ck)
+    bt = kernels.conv_pack_weight(w, ck, k_pitch)
     rowck = t.empty(bt.shape[1], dtype=t.float32, device="cuda")
     kernels.colsum(bt, oc, bt.shape[1], bt.stride(0), dtype, rowck)
     return PreparedConv(bt=bt, rowck=rowck, oc=oc, cin=cin, ck=ck, r=r, s=s, dtype=dtype)
@@ -83,14 +95,24 @@ def upload_nhwc(x, dtype: DType):
     return out
 
 
-def geometry(x_dev, pc: PreparedConv, stride, padding) -> dict:
-    sh, sw = (stride, stride) if np.isscalar(stride) else stride
-    ph, pw = (padding, padding) if np.isscalar(padding) else padding
-    n, h, w, c = (int(v) for v in x_dev.shape)
-    if c != pc.ck:
-        raise ShapeMismatchError(f"input has {c} physical channels, weights were packed for {pc.ck}")
-    return dict(n=n, h=h, w=w, c=c, r=pc.r, s=pc.s, stride_h=int(sh), stride_w=int(sw), pad_h=int(ph),
-                pad_w=int(pw))
+def standalone_colck(x_dev, geom: dict, pl: dict, dtype: DType, out) -> None:
+    """The layer's activation checksum by a separate pass over the input (abft_colsum for a
+    pointwise conv, abft_conv_colck otherwise); layout = the packed weight's K (plan)."""
+    t = D.torch()
+    n, h, w, c = geom["n"], geom["h"], geom["w"], geom["c"]
+    if pl["a_mode"] == 0:
+        kernels.colsum(x_dev, n * h * w, c, c, dtype, out)
+        return
+    r, s = geom["r"], geom["s"]
+    if pl["ck"] == c:
+        kernels.conv_colck(x_dev, geom, dtype, out)
+        return
+    # repack the [(r, s, c)] windowed sums into the plan's (r, s, ck) layout
+    tmp = t.empty(r * s * c, dtype=t.float32, device="cuda")
+    kernels.conv_colck(x_dev, geom, dtype, tmp)
+    out.zero_()
+    cc = min(c, pl["ck"])
+    out[: r * s * pl["ck"]].view(r * s, pl["ck"])[:, :cc] = tmp.view(r * s, c)[:, :cc]
 
 
 def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig(),
@@ -114,12 +136,12 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     if dtype.is_exact:
         D.guard_exact(x, weight, int(weight.shape[1]) * int(weight.shape[2]) * int(weight.shape[3]))
     x_dev = upload_nhwc(x, dtype)
-    pc = prepare_conv_weight(weight, dtype, ck=int(x_dev.shape[3]))
-    geom = geometry(x_dev, pc, stride, padding)
+    oc, cin, kr, ks = (int(v) for v in weight.shape)
+    geom = geometry(x_dev, kr, ks, stride, padding, cin)
     numeric = D.numeric_code(dtype)
-    probe = kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric)
-    plan = kernels.conv_plan(probe)
-    m, P, Q = plan["m"], plan["p"], plan["q"]
+    pl = plan(x_dev, geom, oc, dtype)
+    pc = prepare_conv_weight(weight, dtype, pl["ck"], pl["k"])
+    m, P, Q = pl["m"], pl["p"], pl["q"]
     k_ref = pc.cin * pc.r * pc.s
     shape = GemmShape(m=m, n=pc.oc, k=k_ref)
     validate_faults(faults, shape, tiling)
@@ -127,6 +149,7 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     cells = [fault_cell(f, tiling) for f in faults]
     f_dev, nf = D.faults_tensor(cells)
     out = t.empty((m, pc.oc), dtype=t.float32, device="cuda")
+    ws = t.empty(max(pl["ws"], 16), dtype=t.uint8, device="cuda") if pl["ws"] else None
     thread_level = scheme in THREAD_LEVEL_SCHEMES
     verdicts = None
     if thread_level:
@@ -137,14 +160,15 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     out_sum = t.zeros(1, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
     colck = t.zeros(pc.bt.shape[1], dtype=t.float32, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
     fused = colck if colck_source == "fused" else None
-    args = kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, out=out, ldc=pc.oc, out_kind="f32",
+    args = kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, workspace=ws, out=out, ldc=pc.oc,
+                             out_kind="f32",
                              thread_m=tiling.thread_m, thread_n=tiling.thread_n, m_ext=padded.m, n_ext=padded.n,
                              tol_k=padded.k, faults=f_dev, nfaults=nf, out_sum=out_sum, verdicts=verdicts,
                              ck_split=not dtype.is_exact, a_colck=fused)
     kernels.conv2d(args)
     if scheme is Scheme.GLOBAL_ABFT:
         if colck_source == "standalone":
-            kernels.conv_colck(x_dev, geom, dtype, colck)
+            standalone_colck(x_dev, geom, pl, dtype, colck)
         sums = t.empty(2, dtype=t.float64, device="cuda")
         vbuf = t.empty(32, dtype=t.uint8, device="cuda")
         kernels.global_verify(kernels.global_tasks([(colck, pc.rowck, out_sum, pc.bt.shape[1], k_ref)]), 1,

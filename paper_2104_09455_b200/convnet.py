@@ -24,7 +24,8 @@ from typing import Dict
 
 from . import device as D
 from . import kernels
-from .conv import PreparedConv, geometry, prepare_conv_weight
+from .conv import PreparedConv, geometry, prepare_conv_weight, standalone_colck
+from .conv import plan as conv_plan
 from .networks import LayerSpec
 from .schemes import Scheme, TilingConfig
 from .shapes import BINARY16, DType
@@ -44,8 +45,11 @@ class LayerRunner:
         self.x[..., :spec.cin] = (t.rand((spec.n, spec.h, spec.w, spec.cin), generator=g, device="cuda") * 2 - 1).to(sd)
         bound = 1.0 / (spec.cin * spec.r * spec.s) ** 0.5
         w = ((t.rand((spec.oc, spec.cin, spec.r, spec.s), generator=g, device="cuda") * 2 - 1) * bound).to(sd)
-        self.pc: PreparedConv = prepare_conv_weight(w, dtype, ck=c8)
-        self.geom = geometry(self.x, self.pc, (spec.stride_h, spec.stride_w), (spec.pad_h, spec.pad_w))
+        self.geom = geometry(self.x, spec.r, spec.s, (spec.stride_h, spec.stride_w), (spec.pad_h, spec.pad_w),
+                             spec.cin)
+        self.plan = conv_plan(self.x, self.geom, spec.oc, dtype)
+        self.pc: PreparedConv = prepare_conv_weight(w, dtype, self.plan["ck"], self.plan["k"])
+        self.ws = t.empty(self.plan["ws"], dtype=t.uint8, device="cuda") if self.plan["ws"] else None
         self.m = spec.n * spec.p * spec.q
         self.n8 = D.round8(spec.oc)
         self.out = t.empty((self.m, self.n8), dtype=sd, device="cuda")
@@ -78,7 +82,8 @@ class LayerRunner:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-self.m // t.thread_m) * t.thread_m,
                       n_ext=-(-self.spec.oc // t.thread_n) * t.thread_n,
                       tol_k=-(-self.k_ref // t.k_step) * t.k_step, fired_count=self.counters)
-        args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric, scheme, **kw)
+        args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric, scheme,
+                                 workspace=self.ws, **kw)
         if scheme is Scheme.THREAD_ONE_SIDED and self.offline_ck:
             plan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
                                 self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, **kw)
@@ -86,7 +91,7 @@ class LayerRunner:
                 self.ck_rows = kernels.ck_rows(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype, plan,
                                                t.thread_n, False)
                 args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric,
-                                         scheme, ck_rows=self.ck_rows, **kw)
+                                         scheme, ck_rows=self.ck_rows, workspace=self.ws, **kw)
         return args
 
     def flops(self) -> int:
@@ -100,19 +105,10 @@ class LayerRunner:
         self.colck_pass()
         kernels.conv2d(self._args["global-standalone"])
 
-    @property
-    def pointwise(self) -> bool:
-        sp = self.spec
-        return sp.r == 1 and sp.s == 1 and sp.stride_h == 1 and sp.stride_w == 1 and sp.pad_h == 0 and sp.pad_w == 0
-
     def colck_pass(self) -> None:
         """Standalone activation checksum (one extra read of the input): the plain column
         sum for a pointwise conv (its A is the NHWC matrix itself), the windowed one otherwise."""
-        if self.pointwise:
-            c8 = self.x.shape[3]
-            kernels.colsum(self.x, self.spec.n * self.spec.h * self.spec.w, c8, c8, self.dtype, self.colck)
-        else:
-            kernels.conv_colck(self.x, self.geom, self.dtype, self.colck)
+        standalone_colck(self.x, self.geom, self.plan, self.dtype, self.colck)
 
     def verify(self) -> None:
         kernels.global_verify(self.task, 1, self.numeric, self.sums, out=self.verdict,

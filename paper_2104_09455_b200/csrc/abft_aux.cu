@@ -182,15 +182,56 @@ __global__ void verify_kernel(const double* __restrict__ sums, const int* __rest
 // Weight [OC][Cin][R][S] (torch layout) -> K-major [OC][(r, s, c)] with c padded to ck (zeros):
 // the B^T operand of the implicit-GEMM conv, K ordered like the im2col columns.
 __global__ void conv_pack_weight_kernel(const uint16_t* __restrict__ w, int oc, int cin, int r, int s, int ck,
-                                        uint16_t* __restrict__ out) {
+                                        uint16_t* __restrict__ out, long long ldo) {
   const long long kk = (long long)r * s * ck;
-  const long long total = (long long)oc * kk;
+  const long long total = (long long)oc * ldo;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int o = (int)(i / kk);
-    const int k = (int)(i - (long long)o * kk);
-    const int tap = k / ck, c = k - tap * ck;
-    const int ri = tap / s, si = tap - ri * s;
-    out[i] = c < cin ? w[(((long long)o * cin + c) * r + ri) * s + si] : (uint16_t)0;
+    const int o = (int)(i / ldo);
+    const long long k = i - (long long)o * ldo;
+    uint16_t v = 0;
+    if (k < kk) {
+      const int tap = (int)(k / ck), c = (int)(k - (long long)tap * ck);
+      const int ri = tap / s, si = tap - ri * s;
+      if (c < cin) v = w[(((long long)o * cin + c) * r + ri) * s + si];
+    }
+    out[i] = v;
+  }
+}
+
+// Explicit im2col of an NHWC input into A [M x ld] (row m = (n*P + p)*Q + q, column
+// (ri*S + si)*cr + c over the cr real channels, zero for padding / columns >= R*S*cr):
+// the lowering of shapes.py:169-177, used for convs with few input channels.
+__global__ void __launch_bounds__(256) im2col_kernel(const uint16_t* __restrict__ x, int H, int W, int C, int cr,
+                                                     int R, int S, int sh, int sw, int ph, int pw, int P, int Q,
+                                                     long long M, int K, int ld, uint16_t* __restrict__ out) {
+  const int vpr = ld / 8;                       // 16-byte vectors per row
+  const long long total = M * vpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long m = i / vpr;
+    const int v = (int)(i - m * vpr);
+    const int pq = P * Q;
+    const int n = (int)(m / pq);
+    const int rem = (int)(m - (long long)n * pq);
+    const int p = rem / Q, q = rem - p * Q;
+    uint16_t e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = v * 8 + j;
+      uint16_t val = 0;
+      if (k < K) {
+        const int tap = k / cr, c = k - tap * cr;
+        const int ri = tap / S, si = tap - ri * S;
+        const int hh = p * sh - ph + ri, ww = q * sw - pw + si;
+        if (hh >= 0 && hh < H && ww >= 0 && ww < W) val = __ldg(x + (((long long)n * H + hh) * W + ww) * C + c);
+      }
+      e[j] = val;
+    }
+    uint4 u;
+    u.x = e[0] | ((uint32_t)e[1] << 16);
+    u.y = e[2] | ((uint32_t)e[3] << 16);
+    u.z = e[4] | ((uint32_t)e[5] << 16);
+    u.w = e[6] | ((uint32_t)e[7] << 16);
+    *reinterpret_cast<uint4*>(out + m * ld + v * 8) = u;
   }
 }
 
@@ -265,13 +306,27 @@ using namespace abft;
 
 extern "C" __attribute__((visibility("default"))) int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin,
                                                                            int32_t r, int32_t s, int32_t ck,
-                                                                           void* out, void* stream) {
-  if (oc < 1 || cin < 1 || r < 1 || s < 1 || ck < cin || ck % 8) return fail(ABFT_E_SHAPE, "conv_pack_weight: bad extents");
-  const long long total = (long long)oc * r * s * ck;
+                                                                           void* out, int64_t ldo, void* stream) {
+  if (oc < 1 || cin < 1 || r < 1 || s < 1 || ck < cin || ldo < (int64_t)r * s * ck || ldo % 8)
+    return fail(ABFT_E_SHAPE, "conv_pack_weight: bad extents");
+  const long long total = (long long)oc * ldo;
   int blocks = (int)std::min<long long>((total + 255) / 256, 8LL * num_sms());
-  conv_pack_weight_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const uint16_t*)w, oc, cin, r, s, ck, (uint16_t*)out);
+  conv_pack_weight_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const uint16_t*)w, oc, cin, r, s, ck, (uint16_t*)out,
+                                                                 ldo);
   return cuda_check(cudaGetLastError(), "conv_pack_weight launch");
 }
+
+namespace abft {
+int launch_im2col(const void* x, int n, int h, int w, int c, int cr, int r, int s, int sh, int sw, int ph, int pw,
+                  int P, int Q, int K, int ld, void* out, cudaStream_t st) {
+  const long long M = (long long)n * P * Q;
+  const long long total = M * (ld / 8);
+  int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
+  im2col_kernel<<<blocks, 256, 0, st>>>((const uint16_t*)x, h, w, c, cr, r, s, sh, sw, ph, pw, P, Q, M, K, ld,
+                                        (uint16_t*)out);
+  return cuda_check(cudaGetLastError(), "im2col launch");
+}
+}  // namespace abft
 
 extern "C" __attribute__((visibility("default"))) int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w,
                                                                      int32_t c, int32_t r, int32_t s, int32_t stride_h,

@@ -36,4 +36,8 @@ __host__ __device__ inline double tolerance(double r, int k, double lhs, double 
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// explicit im2col (abft_aux.cu) for the few-channel conv mode
+int launch_im2col(const void* x, int n, int h, int w, int c, int cr, int r, int s, int sh, int sw, int ph, int pw,
+                  int P, int Q, int K, int ld, void* out, cudaStream_t st);
+
 }  // namespace abft

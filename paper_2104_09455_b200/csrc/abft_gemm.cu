@@ -1403,7 +1403,8 @@ PFN_cuTensorMapEncodeIm2col_v12000 get_im2col_fn() {
 }
 
 struct ConvGeom {
-  int a_mode, ck, P, Q, K;
+  int a_mode, ck, P, Q, K, cr;
+  long long ws;
 };
 
 int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
@@ -1418,9 +1419,24 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   g.Q = (c->w + 2 * c->pad_w - c->s) / c->stride_w + 1;
   if (g.P < 1 || g.Q < 1) return fail(ABFT_E_SHAPE, "conv output extent is not positive");
   const bool pointwise = c->r == 1 && c->s == 1 && c->stride_h == 1 && c->stride_w == 1 && c->pad_h == 0 && c->pad_w == 0;
-  g.a_mode = pointwise ? 0 : (c->c % 64 == 0 ? 1 : 2);
-  g.ck = c->c;
-  g.K = c->r * c->s * c->c;
+  g.cr = c->c_real > 0 ? c->c_real : c->c;
+  if (g.cr > c->c) return fail(ABFT_E_SHAPE, "c_real exceeds the physical channel count");
+  const char* force = getenv("ABFT_CONV_MODE");     // bring-up / measurement override
+  int mode = pointwise ? 0 : (c->c % 64 == 0 ? 1 : (c->c >= 48 ? 1 : 3));
+  if (force && !pointwise) mode = atoi(force);
+  g.a_mode = mode;
+  g.ws = 0;
+  if (mode == 0 || mode == 2) {
+    g.ck = c->c;
+    g.K = c->r * c->s * c->c;
+  } else if (mode == 1) {
+    g.ck = (c->c + 63) / 64 * 64;            // channels past c arrive as zeros from the TMA
+    g.K = c->r * c->s * g.ck;
+  } else {
+    g.ck = g.cr;                              // dense (r, s, c_real) columns
+    g.K = (c->r * c->s * g.cr + 7) / 8 * 8;
+    g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
+  }
   return ABFT_OK;
 }
 
@@ -1484,6 +1500,8 @@ extern "C" __attribute__((visibility("default"))) int abft_conv_plan(const abft_
   if (rc != ABFT_OK) return rc;
   out[0] = g.a_mode; out[1] = g.ck; out[2] = g.P; out[3] = g.Q; out[4] = g.K;
   out[5] = (int32_t)std::min<long long>((long long)c->n * g.P * g.Q, 0x7fffffffLL);
+  out[6] = (int32_t)std::min<long long>(g.ws, 0x7fffffffLL);
+  out[7] = 0;
   return ABFT_OK;
 }
 
@@ -1503,11 +1521,25 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
   rc = make_plan(&ga, pl);
   if (rc != ABFT_OK) return rc;
   GemmParams& p = pl.p;
+  if (g.a_mode == 3) {
+    // explicit im2col into the caller's workspace, then the plain GEMM on it
+    if (c->workspace == nullptr || c->ws_bytes < g.ws || (reinterpret_cast<uintptr_t>(c->workspace) & 15))
+      return fail(ABFT_E_VALUE, "explicit-im2col conv needs a 16-byte aligned workspace of abft_conv_plan out[6] bytes");
+    rc = launch_im2col(c->gemm.A, c->n, c->h, c->w, c->c, g.cr, c->r, c->s, c->stride_h, c->stride_w, c->pad_h,
+                       c->pad_w, g.P, g.Q, c->r * c->s * g.cr, g.K, c->workspace, as_stream(stream));
+    if (rc != ABFT_OK) return rc;
+    ga.A = c->workspace;
+    ga.lda = g.K;
+    CUtensorMap ma;
+    rc = cached_map(&ma, ga.A, ga.dtype, ga.K, ga.M, ga.lda, BM);
+    if (rc != ABFT_OK) return rc;
+    return launch_with_a(&ga, pl, ma, stream);
+  }
   p.a_mode = g.a_mode;
   p.cv_P = g.P; p.cv_Q = g.Q; p.cv_S = c->s;
   p.cv_sh = c->stride_h; p.cv_sw = c->stride_w; p.cv_ph = c->pad_h; p.cv_pw = c->pad_w;
   p.cv_c = c->c;
-  p.cv_chunks = g.a_mode == 1 ? c->c / BK : c->c / 8;
+  p.cv_chunks = g.a_mode == 1 ? g.ck / BK : c->c / 8;
   p.cv_pairs = c->r * c->s * (c->c / 8);
   CUtensorMap ma;
   if (g.a_mode == 0) rc = cached_map(&ma, ga.A, ga.dtype, ga.K, ga.M, ga.lda, BM);

@@ -26,7 +26,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                num_sms: int = 0, ck_rows=None, a_colck=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
-    args.Bt, args.ldbt = bt.data_ptr(), ldbt
+    args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
     args.C, args.ldc = (out.data_ptr() if out is not None else None), (ldc or n)
     args.M, args.N, args.K = m, n, k
     args.m_ext, args.n_ext, args.tol_k = m_ext or m, n_ext or n, tol_k or k
@@ -64,22 +64,26 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
 
 
 def conv_args(x, geom: dict, bt, oc: int, dtype: DType, numeric: int, scheme: Scheme = Scheme.UNPROTECTED,
-              **kw):
-    """abft_conv_args_t for an NHWC input x [n, h, w, c] and packed weights bt [OC x r*s*c].
+              workspace=None, **kw):
+    """abft_conv_args_t for an NHWC input x [n, h, w, c] and packed weights bt [OC x K].
 
-    geom: n, h, w, c, r, s, stride_h, stride_w, pad_h, pad_w."""
-    g = _gemm_args(x, geom["c"], bt, bt.stride(0), 0, oc, 0, dtype, numeric, scheme, **kw)
+    geom: n, h, w, c, r, s, stride_h, stride_w, pad_h, pad_w (+ c_real, the model's channels)."""
+    g = _gemm_args(x, geom["c"], bt, bt.stride(0) if bt is not None else 8, 0, oc, 0, dtype, numeric, scheme, **kw)
     args = _lib.ConvArgs()
     args.gemm = g
     for f in ("n", "h", "w", "c", "r", "s", "stride_h", "stride_w", "pad_h", "pad_w"):
         setattr(args, f, int(geom[f]))
+    args.c_real = int(geom.get("c_real", 0))
+    if workspace is not None:
+        args.workspace, args.ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     return args
 
 
 def conv_plan(args) -> dict:
-    out = (ctypes.c_int32 * 6)()
+    """abft_conv_plan: A-load mode, packed-weight channel stride ck and K, P, Q, M, workspace bytes."""
+    out = (ctypes.c_int32 * 8)()
     _lib.check(_lib.load().abft_conv_plan(ctypes.byref(args), out))
-    return dict(a_mode=out[0], ck=out[1], p=out[2], q=out[3], k=out[4], m=out[5])
+    return dict(a_mode=out[0], ck=out[1], p=out[2], q=out[3], k=out[4], m=out[5], ws=out[6])
 
 
 def conv2d(args) -> None:
@@ -87,13 +91,14 @@ def conv2d(args) -> None:
     _lib.check(_lib.load().abft_conv2d(ctypes.byref(args), stream_handle()))
 
 
-def conv_pack_weight(w, ck: int):
-    """torch-layout weight [OC, cin, r, s] (CUDA fp16/bf16) -> packed K-major [OC, r*s*ck]."""
+def conv_pack_weight(w, ck: int, k_pitch: int = 0):
+    """torch-layout weight [OC, cin, r, s] (CUDA fp16/bf16) -> packed K-major [OC, k_pitch]."""
     t = torch()
     oc, cin, r, s = (int(v) for v in w.shape)
     w = w.contiguous()
-    out = t.empty((oc, r * s * ck), dtype=w.dtype, device="cuda")
-    _lib.call("abft_conv_pack_weight", ptr(w), oc, cin, r, s, ck, ptr(out), stream_handle())
+    k_pitch = k_pitch or -(-(r * s * ck) // 8) * 8
+    out = t.empty((oc, k_pitch), dtype=w.dtype, device="cuda")
+    _lib.call("abft_conv_pack_weight", ptr(w), oc, cin, r, s, ck, ptr(out), k_pitch, stream_handle())
     return out
 
 

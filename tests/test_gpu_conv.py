@@ -111,8 +111,7 @@ def test_conv_colck_is_the_im2col_column_sum(P):
         n, h, w, c, oc, r, s, st, pd = case
         x, wt, cols, _ = _data(case, exact=True, seed=2)
         xd = C.upload_nhwc(x, P.EXACT_INT)
-        pc = C.prepare_conv_weight(wt, P.EXACT_INT, ck=int(xd.shape[3]))
-        geom = C.geometry(xd, pc, st, pd)
+        geom = C.geometry(xd, r, s, st, pd, c)
         out = torch.empty(r * s * xd.shape[3], dtype=torch.float32, device="cuda")
         kernels.conv_colck(xd, geom, P.EXACT_INT, out)
         ref = O.colck(O.im2col_nhwc(np.pad(x, ((0, 0), (0, 0), (0, 0), (0, xd.shape[3] - c))), r, s, st, pd))
@@ -132,3 +131,23 @@ def test_conv_global_fused_and_standalone_checksums_agree(P, case):
         va, vb = a.verdicts[0], b.verdicts[0]
         assert (va.detected, va.lhs, va.rhs) == (vb.detected, vb.lhs, vb.rhs)
         assert va.detected == bool(faults)
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
+def test_conv_every_a_load_mode_bit_exact(P, mode, monkeypatch):
+    """Each A-load mode (64-channel TMA im2col, 8-channel TMA im2col, explicit im2col) on the
+    same non-pointwise cases gives the oracle's exact-int outputs and verdicts."""
+    monkeypatch.setenv("ABFT_CONV_MODE", mode)
+    for case in CASES:
+        n, h, w, c, oc, r, s, st, pd = case
+        if r == 1 and s == 1 and st == 1 and pd == 0:
+            continue
+        x, wt, cols, wmat = _data(case, exact=True, seed=4)
+        m = cols.shape[0]
+        for scheme in ("unprotected", "global-abft", "thread-one-sided"):
+            faults_ref = [("output", m - 1, 0, 9)] if scheme != "unprotected" else []
+            faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in faults_ref]
+            rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults)
+            out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, faults_ref)
+            assert np.array_equal(rep.output.reshape(m, oc), out), (mode, case, scheme)
+            assert rep.detected == any(v.detected for v in verdicts), (mode, case, scheme)
