@@ -90,6 +90,11 @@ typedef struct {
    * checksum of checksum.py:90-96 / :229 computed from the shared-memory A tiles the MMA consumes,
    * so the global scheme needs no extra pass over A; for a conv this is the windowed im2col sum) */
   float* a_colck;
+  /* optional [1] fp64, global scheme: += sum over rows of A . rowck(B-tile), i.e. the lhs
+   * colck(A) . rowck(B) of checksum.py:108-117 regrouped as 1^T (A (B 1)): one extra MMA
+   * N-slice per tile driven by the offline checksum rows (abft_ck_rows with nt = the plan's
+   * bn_eff, split hi/lo, nck_pad = 16) and a row sum in the epilogue.  Needs ck_rows. */
+  double* out_lhs;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);

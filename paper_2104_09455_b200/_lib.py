@@ -89,6 +89,7 @@ class GemmArgs(ctypes.Structure):
         ("num_sms", ctypes.c_int32),
         ("ck_rows", ctypes.c_void_p), ("ldck", ctypes.c_int64), ("ck_rows_n", ctypes.c_int32),
         ("a_colck", ctypes.c_void_p),
+        ("out_lhs", ctypes.c_void_p),
     ]
 
 

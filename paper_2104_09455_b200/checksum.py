@@ -187,9 +187,10 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
     """Global-ABFT layer chain with ReLU, deferred verdicts (checksum.py:198-237).
 
     Per layer one fused kernel: fp32 GEMM, faults into the raw accumulator,
-    output summation, ReLU + rounding to storage, and the next layer's
-    activation checksum of the stored values.  Verification of all layers is
-    one batched launch after the chain; the host reads the verdicts once.
+    output summation (rhs), ReLU + rounding to storage, and lhs = colck(a) .
+    rowck(w) regrouped as the row sum of the checksum column a . rowck(w tile)
+    from one extra MMA N-slice.  Verification of all layers is one batched
+    launch after the chain; the host reads the verdicts once.
     Only ReLU is fused; other activations are rejected.
     """
     if activation is not relu:
@@ -208,10 +209,11 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
     if mode.is_exact:
         D.guard_exact(a0)
     act = D.upload(a0, mode, "A0")
-    colck = D.colck_device(act, m, mode)
     numeric = D.numeric_code(mode)
-    sums = t.zeros((len(weights), 1), dtype=t.float64, device="cuda")
-    tasks, ks, outs = [], [], []
+    nl = len(weights)
+    if nl == 0:
+        return []
+    sums = t.zeros((nl, 2), dtype=t.float64, device="cuda")     # per layer (lhs, rhs)
     for idx, w in enumerate(weights):
         if mode.is_exact:
             D.guard_exact(w, act, dims[idx], f"layer {idx} accumulation")
@@ -220,27 +222,22 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
         nxt = t.empty((m, D.round8(n)), dtype=D.torch_storage_dtype(mode), device="cuda")
         if n % 8:
             nxt.zero_()
-        next_colck = t.zeros(D.round8(n), dtype=t.float32, device="cuda")
         f_dev, nf = D.faults_tensor(list(faults.get(idx, ())))
+        kw = dict(out=nxt, ldc=nxt.stride(0), out_kind="bf16" if mode.tag is DTypeTag.BFLOAT16 else "f16",
+                  relu=True, faults=f_dev, nfaults=nf, out_sum=sums[idx, 1:2], out_lhs=sums[idx, 0:1])
+        plan = kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
+                            plan_only=True, **kw)
+        ckr = kernels.global_ck_rows(pw.bt, n, dims[idx], mode, plan)
         kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
-                     out=nxt, ldc=nxt.stride(0), out_kind="bf16" if mode.tag is DTypeTag.BFLOAT16 else "f16",
-                     relu=True, faults=f_dev, nfaults=nf, out_sum=sums[idx], next_colck=next_colck)
-        tasks.append((colck, pw.rowck, sums[idx], dims[idx]))
-        ks.append(dims[idx])
-        outs.append(nxt)
+                     ck_rows=ckr, **kw)
         if mode.is_exact:
             # the next layer consumes these values exactly only inside the fp16 integer range
             if D.max_abs(nxt) > D.FP16_INT_MAX:
                 raise D.ExactOverflowError(f"layer {idx} activations leave the exact fp16 range")
-        act, colck = nxt, next_colck
-    nl = len(weights)
-    if nl == 0:
-        return []
-    lhs_rhs = t.empty((nl, 2), dtype=t.float64, device="cuda")
-    kernels.global_lhs(kernels.global_tasks(tasks), nl, lhs_rhs)
-    ks_dev = t.tensor(ks, dtype=t.int32, device="cuda")
+        act = nxt
+    ks_dev = t.tensor(dims[:-1], dtype=t.int32, device="cuda")
     vbuf = t.empty(nl * 32, dtype=t.uint8, device="cuda")
-    kernels.verify_sums(lhs_rhs, ks_dev, nl, numeric, out=vbuf)
+    kernels.verify_sums(sums, ks_dev, nl, numeric, out=vbuf)
     raw = vbuf.cpu().numpy().view(np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"),
                                             ("det", "<i4"), ("k", "<i4")]))
     verdicts = []

@@ -6,9 +6,11 @@ same ``execute`` / ``global_abft_check`` as any GEMM.  ``conv2d`` keeps exactly 
 contract — same schemes, tiling meaning, fault coordinates (row = output pixel index
 (n*P + p)*Q + q, col = output channel), verdict ordering and report type as ``execute``
 on the im2col matrix — but never builds the im2col matrix: the sm_100a kernel reads the
-NHWC activation through a TMA im2col map (implicit GEMM), and the global scheme's
-activation checksum — the column sum of the im2col matrix — is accumulated by the same
-kernel from the A tiles it stages (or by the standalone windowed pass ``abft_conv_colck``).
+NHWC activation through a TMA im2col map (implicit GEMM).  The global scheme's lhs
+colck(A) . rowck(B) is regrouped as 1^T (A (B 1)): one extra MMA N-slice against the
+weight tile's row sums, summed over rows in the same kernel, so the im2col matrix's
+column checksum is never needed (the standalone windowed pass ``abft_conv_colck`` is kept
+as the alternative and cross-check).
 
 K ordering is (r, s, c); input channels are zero-padded to a multiple of 8
 (the reference's x8 padding rule, shapes.py:187-195, also the TMA 16-byte pitch rule).
@@ -121,9 +123,9 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     """Protected NHWC convolution; returns the reference's ExecutionReport for the lowered GEMM.
 
     ``report.output`` is [n, P, Q, OC] fp32 (int64 in exact-int mode); ``report.shape`` is
-    the reference lowering GemmShape(n*P*Q, OC, C*R*S).  Global scheme: the windowed
-    activation checksum comes from the A tiles inside the conv kernel ("fused") or from the
-    standalone pass over the input ("standalone", abft_conv_colck)."""
+    the reference lowering GemmShape(n*P*Q, OC, C*R*S).  Global scheme: lhs comes from the
+    conv kernel's checksum N-slice, sum over rows of A . rowck(B tile) ("fused"), or from
+    colck(A) . rowck(B) with the windowed checksum of a standalone pass ("standalone")."""
     from .checksum import Verdict
     from .tiled import _TV_DTYPE, ExecutionReport, _counts, _thread_verdicts
 
@@ -157,22 +159,29 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
         verdicts = t.empty(ntr * ntc * _TV_DTYPE.itemsize, dtype=t.uint8, device="cuda")
     if colck_source not in ("fused", "standalone"):
         raise ValueError(f"colck_source must be 'fused' or 'standalone', got {colck_source!r}")
-    out_sum = t.zeros(1, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
-    colck = t.zeros(pc.bt.shape[1], dtype=t.float32, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
-    fused = colck if colck_source == "fused" else None
-    args = kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, workspace=ws, out=out, ldc=pc.oc,
-                             out_kind="f32",
-                             thread_m=tiling.thread_m, thread_n=tiling.thread_n, m_ext=padded.m, n_ext=padded.n,
-                             tol_k=padded.k, faults=f_dev, nfaults=nf, out_sum=out_sum, verdicts=verdicts,
-                             ck_split=not dtype.is_exact, a_colck=fused)
-    kernels.conv2d(args)
-    if scheme is Scheme.GLOBAL_ABFT:
-        if colck_source == "standalone":
-            standalone_colck(x_dev, geom, pl, dtype, colck)
-        sums = t.empty(2, dtype=t.float64, device="cuda")
+    glob = scheme is Scheme.GLOBAL_ABFT
+    sums = t.zeros(2, dtype=t.float64, device="cuda") if glob else None       # [lhs, rhs]
+    kw = dict(out=out, ldc=pc.oc, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
+              m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
+              out_sum=sums[1:2] if glob else None, verdicts=verdicts, ck_split=not dtype.is_exact)
+    colck = None
+    if glob and colck_source == "fused":
+        # lhs from the kernel's checksum slice: sum over rows of A . rowck(B tile)
+        kw["out_lhs"] = sums[0:1]
+        gplan = kernels.gemm(x_dev, 8, pc.bt, pc.bt.stride(0), m, pc.oc, pl["k"], dtype, numeric, scheme,
+                             plan_only=True, **kw)
+        kw["ck_rows"] = kernels.global_ck_rows(pc.bt, pc.oc, pl["k"], dtype, gplan)
+    kernels.conv2d(kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, workspace=ws, **kw))
+    if glob:
         vbuf = t.empty(32, dtype=t.uint8, device="cuda")
-        kernels.global_verify(kernels.global_tasks([(colck, pc.rowck, out_sum, pc.bt.shape[1], k_ref)]), 1,
-                              numeric, sums, out=vbuf)
+        if colck_source == "standalone":
+            # lhs = colck(A) . rowck(B) from a separate windowed pass over the input
+            colck = t.zeros(pc.bt.shape[1], dtype=t.float32, device="cuda")
+            standalone_colck(x_dev, geom, pl, dtype, colck)
+            kernels.global_verify(kernels.global_tasks([(colck, pc.rowck, sums[1:2], pc.bt.shape[1], k_ref)]), 1,
+                                  numeric, t.empty(2, dtype=t.float64, device="cuda"), out=vbuf)
+        else:
+            kernels.verify_sums(sums, t.tensor([k_ref], dtype=t.int32, device="cuda"), 1, numeric, out=vbuf)
         raw = vbuf.cpu().numpy().view(np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"),
                                                 ("det", "<i4"), ("k", "<i4")]))[0]
         lhs, rhs = float(raw["lhs"]), float(raw["rhs"])

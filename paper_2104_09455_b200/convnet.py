@@ -7,10 +7,12 @@ buffers (NHWC input, packed weight, checksums, output) and enqueues it under
 unprotected / global / one-sided ABFT:
 
   unprotected       implicit-GEMM conv (or GEMM), fp16 store
-  global-abft       the same kernel with the output summation in its epilogue and the
-                    layer's windowed activation checksum accumulated from the A tiles it
-                    stages (the input comes out of pooling / residual / BN glue, so it
-                    cannot be fused into the producer's epilogue)
+  global-abft       the same kernel with the output summation (rhs) in its epilogue and the
+                    lhs colck(A) . rowck(B) regrouped as sum_rows A . rowck(B tile): one
+                    extra MMA N-slice against the weight tile's row sums, summed in the
+                    epilogue (the input comes out of pooling / residual / BN glue, so a
+                    producer-fused activation checksum is not available; SURVEY H3);
+                    alternatively the windowed activation checksum by a standalone pass
                     + its share of the network's single batched verification
   thread-one-sided  checksum N-slice in the same MMA, per-row compares in the epilogue
 
@@ -53,11 +55,13 @@ class LayerRunner:
         self.m = spec.n * spec.p * spec.q
         self.n8 = D.round8(spec.oc)
         self.out = t.empty((self.m, self.n8), dtype=sd, device="cuda")
-        self.scratch = t.zeros(64, dtype=t.float64, device="cuda")     # [0] rhs, [1] counters
-        self.rhs = self.scratch[0:1]
-        self.counters = self.scratch[1:2].view(t.int32)
+        self.scratch = t.zeros(64, dtype=t.float64, device="cuda")     # [0] lhs, [1] rhs, [2] counters
+        self.lhs_rhs = self.scratch[0:2]
+        self.rhs = self.scratch[1:2]
+        self.counters = self.scratch[2:3].view(t.int32)
         self.colck = t.zeros(self.pc.bt.shape[1], dtype=t.float32, device="cuda")
         self.k_ref = spec.cin * spec.r * spec.s
+        self.ks = t.tensor([self.k_ref], dtype=t.int32, device="cuda")
         self.task = kernels.global_tasks([(self.colck, self.pc.rowck, self.rhs, self.pc.bt.shape[1], self.k_ref)])
         self.sums = t.zeros(2, dtype=t.float64, device="cuda")
         self.verdict = t.zeros(32, dtype=t.uint8, device="cuda")
@@ -77,7 +81,12 @@ class LayerRunner:
         if scheme is Scheme.GLOBAL_ABFT:
             kw["out_sum"] = self.rhs
             if fused_colck:
-                kw["a_colck"] = self.colck
+                # lhs from the kernel's checksum N-slice against the weight tile's row sums
+                kw["out_lhs"] = self.scratch[0:1]
+                gplan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
+                                     self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, **kw)
+                kw["ck_rows"] = kernels.global_ck_rows(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype,
+                                                       gplan)
         elif scheme is Scheme.THREAD_ONE_SIDED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-self.m // t.thread_m) * t.thread_m,
                       n_ext=-(-self.spec.oc // t.thread_n) * t.thread_n,
@@ -111,15 +120,18 @@ class LayerRunner:
         standalone_colck(self.x, self.geom, self.plan, self.dtype, self.colck)
 
     def verify(self) -> None:
-        kernels.global_verify(self.task, 1, self.numeric, self.sums, out=self.verdict,
-                              detected_count=self.counters)
+        if self.global_variant == "fused":
+            kernels.verify_sums(self.lhs_rhs, self.ks, 1, self.numeric, out=self.verdict,
+                                detected_count=self.counters)
+        else:
+            kernels.global_verify(self.task, 1, self.numeric, self.sums, out=self.verdict,
+                                  detected_count=self.counters)
 
     def run(self, scheme: Scheme) -> None:
         """One protected execution of the layer (verification included for global)."""
         if scheme is Scheme.GLOBAL_ABFT:
             kernels.zero(self.scratch)
             if self.global_variant == "fused":
-                kernels.zero(self.colck)
                 self.conv(scheme)
             else:
                 self.global_standalone()

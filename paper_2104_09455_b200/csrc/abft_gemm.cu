@@ -69,6 +69,8 @@ struct GemmParams {
   uint32_t off_b, off_ck, off_cks, off_rec, off_stage, off_colck, off_out, off_acolck, off_bar;
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
+  double* out_lhs;       // global: += sum_rows A . rowck(B tile) (one checksum N-slice per tile)
+  int gck;               // 1: the global checksum slice is active
   int acolck_mode;       // 1: column sums on the tensor cores (ones x A-tile MMA into TMEM), 2: CUDA cores
   int dck_col;           // TMEM column of the two 64-column column-sum buffers (mode 1)
   uint32_t off_ones;     // smem [64 x 128 B] tile of ones (mode 1)
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool has_shadow = CLASS == CLASS_REPLICA;
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
   const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
-  const bool ck_loaded = has_ck && p.ck_mode == 2 && !(p.debug & 8);
+  const bool ck_loaded = (has_ck || p.gck) && p.ck_mode == 2 && !(p.debug & 8);
   const int bn = p.bn;
   const bool stamp = (p.debug & 2048) && blockIdx.x < 160;
   if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][0] = gtimer();
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool split = p.epi_split != 0;
     const int c_first = split ? h * 32 : (h == 0 ? 0 : 0x7fffffff);
     const int c_step = split ? 64 : 32;
-    double rhs_acc = 0.0;
+    double rhs_acc = 0.0, lhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
     int sbuf = 0;
     uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * 4096;
@@ -730,6 +732,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
 
+      if (p.gck && h == 0) {
+        // global lhs: this row's A . rowck(B tile) = checksum column hi + lo
+        float ck_hi, ck_lo;
+        __syncwarp();
+        ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
+        ptx::tmem_ld_wait();
+        if (row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
+      }
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
       const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
       uint32_t fmask = 0;
@@ -968,6 +978,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         atomicAdd(p.out_sum, tot);
       }
     }
+    if (p.gck) {
+      double x = lhs_acc;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) red_d[8 + (et >> 5)] = x;
+      ptx::named_bar_sync(3, 256);
+      if (et == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 8; ++w) tot += red_d[8 + w];
+        atomicAdd(p.out_lhs, tot);
+      }
+    }
     if (p.tma_store && lane == 0) ptx::bulk_wait_all();
     if (p.next_colck != nullptr && p.colck_in_smem) {
       ptx::named_bar_sync(3, 256);
@@ -1133,6 +1155,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     if (m_ext < a->M || n_ext < a->N || m_ext % mt || n_ext % nt)
       return fail(ABFT_E_SHAPE, "m_ext/n_ext must cover M/N and be multiples of the thread tile");
   }
+  const bool gck = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && !as_plain;
   const int split = (has_ck && a->ck_split) ? 1 : 0;
   // global scheme with the activation checksum: 2 x 64 TMEM columns for the column-sum MMA
   const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
@@ -1152,13 +1175,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
       long long best_cost = 0;
       for (int cand : {256, 224, 192, 128, 64, 32}) {
         if (cand < nt || (thread_level && cand / nt > 32)) continue;
-        const int cols = tile_cols(cand, nt, has_ck, has_shadow, split);
+        const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
         if (cols + extra_cols > 512) continue;
         if (pass == 0 && 2 * cols + extra_cols > 512) continue;                      // pass 0: double-buffered only
         const int eff = (cand / nt) * nt;
         const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
         const long long waves = (tiles + sms - 1) / sms;
-        const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : 0;
+        const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
         const long long cost = waves * (128 + 2LL * cand + nck);
         if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
       }
@@ -1180,13 +1203,15 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.groups = thread_level ? p.bn_eff / nt : 0;
   if (thread_level && p.groups > 32) return fail(ABFT_E_UNSUPPORTED, "more than 32 checksum groups per CTA tile");
   p.split = split;
-  p.nck = has_ck ? p.groups * (split ? 2 : 1) : 0;
-  p.nck_pad = has_ck ? round_up(p.nck, 16) : 0;
+  p.nck = has_ck ? p.groups * (split ? 2 : 1) : (gck ? 2 : 0);
+  p.nck_pad = (has_ck || gck) ? round_up(p.nck, 16) : 0;
+  p.gck = gck ? 1 : 0;
+  p.out_lhs = gck ? a->out_lhs : nullptr;
   p.num_m_blocks = m_blocks;
   p.num_n_blocks = ceil_div(n_ext, p.bn_eff);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   p.nkb = ceil_div(a->K, BK);
-  p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split);
+  p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
   p.shadow_off = bn + p.nck_pad;
   if (p.cols_per_acc > 512) return fail(ABFT_E_UNSUPPORTED, "TMEM budget exceeded");
   p.acc_stages = (2 * p.cols_per_acc + extra_cols <= 512) ? 2 : 1;
@@ -1195,7 +1220,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.dck_col = p.acc_stages * p.cols_per_acc;
   p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc + (p.acolck_mode == 1 ? 32 : 0)));
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
-  p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : 0;
+  p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : (gck ? 2 : 0);
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
   p.rk = (float)(p.r * (double)p.tol_k);
@@ -1209,7 +1234,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.fired_count = a->fired_count; p.fired = a->fired; p.fired_cap = a->fired_cap;
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
-  p.idesc_ck = has_ck ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
+  p.idesc_ck = (has_ck || gck) ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
   p.idesc_ones = ptx::idesc_f16(fmt, 64, 8) | (1u << 15);    // M=64, N=8, A MN-major
   {
     const char* dbg = getenv("ABFT_DEBUG");
@@ -1365,9 +1390,11 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   int rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
   if (rc != ABFT_OK) return rc;
   if (p.ck_mode == 2) {
-    if (a->ck_rows_n != p.num_n_blocks * p.nck_pad || a->ldck < a->K || (a->ldck % 8) ||
+    if (a->ck_rows == nullptr || a->ck_rows_n != p.num_n_blocks * p.nck_pad || a->ldck < a->K || (a->ldck % 8) ||
         (reinterpret_cast<uintptr_t>(a->ck_rows) & 15))
-      return fail(ABFT_E_SHAPE, "ck_rows do not match this call's plan (see abft_gemm_plan)");
+      return fail(ABFT_E_SHAPE, p.gck ? "out_lhs needs the plan's global checksum rows (abft_ck_rows with nt = bn_eff, "
+                                        "split, nck_pad 16; see abft_gemm_plan)"
+                                      : "ck_rows do not match this call's plan (see abft_gemm_plan)");
     rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
     if (rc != ABFT_OK) return rc;
   } else {

@@ -23,7 +23,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-               num_sms: int = 0, ck_rows=None, a_colck=None):
+               num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -45,6 +45,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     if ck_rows is not None:
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
+    args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
     return args
 
 
@@ -117,6 +118,12 @@ def ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, split: 
     _lib.call("abft_ck_rows", ptr(bt), n, k, bt.stride(0), storage_code(dtype), plan["bn_eff"], thread_n,
               int(split), plan["nck_pad"], plan["n_blocks"], ptr(out), out.stride(0), stream_handle())
     return out
+
+
+def global_ck_rows(bt, n: int, k: int, dtype: DType, plan: dict):
+    """Checksum rows of the global scheme's lhs slice: per CTA N-tile, the hi/lo split of the
+    tile's weight row sums (abft_ck_rows with nt = bn_eff), for the plan of an out_lhs call."""
+    return ck_rows(bt, n, k, dtype, plan, plan["bn_eff"], True)
 
 
 def colsum(x, rows: int, cols: int, ldx: int, dtype: DType, out, accumulate: bool = False) -> None:

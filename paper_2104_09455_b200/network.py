@@ -5,11 +5,10 @@ GEMM) with ReLU between them — the chain of ``run_protected_pipeline``
 (checksum.py:198-237) — where every layer carries its own scheme:
 
   unprotected   plain tcgen05 GEMM
-  global-abft   output summation in the epilogue; the layer's activation checksum is
-                accumulated inside the same kernel from the A tiles it stages (the
-                kernel-fused activation checksum of PAPER.md:193, with no extra pass
-                over the activations); all dot products + verdicts run in one batched
-                launch at the end
+  global-abft   output summation (rhs) in the epilogue; lhs colck(A) . rowck(B) regrouped
+                as sum_rows A . rowck(B tile) — one extra MMA N-slice against the weight
+                tile's row sums, summed in the same epilogue, so no activation checksum
+                pass is needed; the verdicts of all layers run in one launch at the end
   thread-one-sided  checksum N-slice in the same MMA, per-row compare in the
                 epilogue; fired thread tiles counted on device
 
@@ -78,32 +77,25 @@ class ProtectedChain:
         self.acts = [t.zeros((m, L.n), dtype=sd, device="cuda") for L in self.layers]
         nl = len(self.layers)
         # every per-forward accumulator lives in ONE block so a single memset node clears it:
-        # [rhs fp64 x nl][counters int32 x 2, pad][colck fp32 per layer]
-        off_cnt = 8 * nl
-        off_ck = off_cnt + 16
-        total = off_ck + 4 * sum(L.k for L in self.layers)
-        self.scratch = t.zeros(total, dtype=t.uint8, device="cuda")
-        self.rhs = self.scratch[:off_cnt].view(t.float64).view(nl, 1)
+        # [(lhs, rhs) fp64 per layer][counters int32 x 2]
+        off_cnt = 16 * nl
+        self.scratch = t.zeros(off_cnt + 16, dtype=t.uint8, device="cuda")
+        self.sums = self.scratch[:off_cnt].view(t.float64).view(nl, 2)
         self.counters = self.scratch[off_cnt:off_cnt + 8].view(t.int32)   # [fired thread tiles, flagged layers]
-        self.colck, o = [], off_ck
-        for L in self.layers:
-            self.colck.append(self.scratch[o:o + 4 * L.k].view(t.float32))
-            o += 4 * L.k
         self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
         self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
-        self._tasks = None
-        if self.global_ids:
-            self._tasks = kernels.global_tasks([(self.colck[i], self.layers[i].pw.rowck, self.rhs[i],
-                                                 self.layers[i].k) for i in self.global_ids])
-            self._ks = t.tensor([self.layers[i].k for i in self.global_ids], dtype=t.int32, device="cuda")
-            self._gsums = t.zeros((len(self.global_ids), 2), dtype=t.float64, device="cuda")
-        # offline checksum rows where the plan says B tiles are re-read by several M-blocks
-        for L in self.layers:
-            if L.scheme is Scheme.THREAD_ONE_SIDED:
-                kw = self._gemm_kwargs(0, L)
+        self._ks_all = t.tensor([L.k for L in self.layers], dtype=t.int32, device="cuda")
+        self._ks = t.tensor([self.layers[i].k for i in self.global_ids] or [0], dtype=t.int32, device="cuda")
+        # offline checksum rows: the global scheme's lhs slice (always), and the one-sided
+        # check's rows where the plan says B tiles are re-read by several M-blocks
+        for i, L in enumerate(self.layers):
+            if L.scheme in (Scheme.THREAD_ONE_SIDED, Scheme.GLOBAL_ABFT):
+                kw = self._gemm_kwargs(i, L)
                 plan = kernels.gemm(self.x, self.x.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype,
                                     self.numeric, L.scheme, plan_only=True, **kw)
-                if plan["ck_offline_recommended"]:
+                if L.scheme is Scheme.GLOBAL_ABFT:
+                    L.ck_rows = kernels.global_ck_rows(L.pw.bt, L.n, L.k, self.dtype, plan)
+                elif plan["ck_offline_recommended"]:
                     L.ck_rows = kernels.ck_rows(L.pw.bt, L.n, L.k, self.dtype, plan, self.tiling.thread_n,
                                                 self.ck_split)
 
@@ -113,8 +105,8 @@ class ProtectedChain:
         kw = dict(out=self.acts[i], ldc=self.acts[i].stride(0),
                   out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu)
         if L.scheme is Scheme.GLOBAL_ABFT:
-            kw["out_sum"] = self.rhs[i]
-            kw["a_colck"] = self.colck[i]
+            kw["out_lhs"] = self.sums[i, 0:1]
+            kw["out_sum"] = self.sums[i, 1:2]
         elif L.scheme is not Scheme.UNPROTECTED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-m // t.thread_m) * t.thread_m,
                       n_ext=-(-L.n // t.thread_n) * t.thread_n, tol_k=-(-L.k // t.k_step) * t.k_step,
@@ -132,22 +124,22 @@ class ProtectedChain:
                          L.scheme, ck_rows=L.ck_rows, **self._gemm_kwargs(i, L))
             a = self.acts[i]
         if self.global_ids:
-            ng = len(self.global_ids)
-            kernels.global_verify(self._tasks, ng, self.numeric, self._gsums, out=self.verdict_buf,
-                                  detected_count=self.counters[1:2])
+            # deferred verification of every layer's (lhs, rhs) in one launch (layers without the
+            # global scheme hold (0, 0) and cannot flag)
+            kernels.verify_sums(self.sums, self._ks_all, len(self.layers), self.numeric, out=self.verdict_buf,
+                                detected_count=self.counters[1:2])
         return a
 
     # ---- multi-GPU helpers (batch sharding): per-layer partial sums, all-reduced by the caller
     def global_partials(self):
         """[n_global, 2] fp64 (lhs, rhs) of this shard, valid after forward() on the stream."""
-        kernels.global_lhs(self._tasks, len(self.global_ids), self._gsums)
-        return self._gsums
+        return self.sums[self.global_ids]
 
     def verify_reduced(self, sums):
         """Verdicts from all-reduced (lhs, rhs) sums; returns the device counter of flagged layers."""
         t = D.torch()
         cnt = t.zeros(1, dtype=t.int32, device="cuda")
-        kernels.verify_sums(sums, self._ks, len(self.global_ids), self.numeric, out=self.verdict_buf,
+        kernels.verify_sums(sums.contiguous(), self._ks, len(self.global_ids), self.numeric, out=self.verdict_buf,
                             detected_count=cnt)
         return cnt
 

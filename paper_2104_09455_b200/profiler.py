@@ -8,8 +8,8 @@ rather than from a T4-calibrated model:
 
   T_o     the layer's GEMM alone (CUDA-graph replayed, CUDA events)
   T_one   GEMM with the checksum N-slice and the per-row compare (flags mode)
-  T_glob  GEMM with the output summation and the activation checksum accumulated
-          from the staged A tiles (both inside the one kernel)
+  T_glob  GEMM with the output summation (rhs) and the checksum N-slice whose row sum
+          is lhs = sum_rows A . rowck(B tile) (both inside the one kernel)
           + this layer's share of the one batched verification launch
 """
 
@@ -67,8 +67,8 @@ def profile_layers(weights: Sequence, batch: int, dtype: DType = BINARY16,
                                                                  dtype, ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw),
                                             iters)
     g = chains[Scheme.GLOBAL_ABFT]
-    t_verify = graph_time_us(lambda: kernels.global_verify(g._tasks, len(g.global_ids), g.numeric, g._gsums,
-                                                           out=g.verdict_buf, detected_count=g.counters[1:2]), iters)
+    t_verify = graph_time_us(lambda: kernels.verify_sums(g.sums, g._ks_all, n, g.numeric, out=g.verdict_buf,
+                                                         detected_count=g.counters[1:2]), iters)
     out = {}
     for i in range(n):
         out[(i, Scheme.UNPROTECTED)] = entries[(i, Scheme.UNPROTECTED)] * 1e-6

@@ -145,16 +145,22 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
     if thread_level:
         ntr, ntc = padded.m // tiling.thread_m, padded.n // tiling.thread_n
         verdicts = t.empty(ntr * ntc * _TV_DTYPE.itemsize, dtype=t.uint8, device="cuda")
-    out_sum = t.zeros(1, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
-    # global: the activation checksum is accumulated by the kernel from the A tiles it stages
-    a_colck = t.zeros(k, dtype=t.float32, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
+    # global: [lhs, rhs] both accumulated by the GEMM kernel — rhs = output summation, lhs =
+    # sum over rows of A . rowck(B tile) from one extra MMA N-slice (colck(A) . rowck(B) regrouped)
+    sums = t.zeros(2, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
+    out_sum = sums[1:2] if sums is not None else None
+    out_lhs = sums[0:1] if sums is not None else None
     if ck_source not in ("auto", "onchip", "offline"):
         raise ValueError(f"ck_source must be 'auto', 'onchip' or 'offline', got {ck_source!r}")
     split = ck_split and not dtype.is_exact
     call = dict(out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
                 m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
-                out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, a_colck=a_colck)
+                out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, out_lhs=out_lhs)
     ckr = None
+    if scheme is Scheme.GLOBAL_ABFT:
+        gplan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
+                             plan_only=True, **call)
+        ckr = kernels.global_ck_rows(bt_dev, n, k, dtype, gplan)
     if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED) and ck_source != "onchip":
         plan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
                             plan_only=True, **call)
@@ -163,11 +169,6 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
     kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
                  ck_rows=ckr, **call)
     if scheme is Scheme.GLOBAL_ABFT:
-        rowck = t.empty(bt_dev.shape[1], dtype=t.float32, device="cuda")
-        kernels.colsum(bt_dev, n, bt_dev.shape[1], bt_dev.stride(0), dtype, rowck)
-        tasks = kernels.global_tasks([(a_colck, rowck, out_sum, k)])
-        sums = t.empty(2, dtype=t.float64, device="cuda")
-        kernels.global_lhs(tasks, 1, sums)
         ks = t.tensor([k], dtype=t.int32, device="cuda")
         vbuf = t.empty(32, dtype=t.uint8, device="cuda")
         kernels.verify_sums(sums, ks, 1, numeric, out=vbuf)

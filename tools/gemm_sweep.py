@@ -26,7 +26,7 @@ def run(m, n, k):
     pw = D.prepare_weight(b, P.BINARY16)
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
     osum = torch.zeros(1, dtype=torch.float64, device="cuda")
-    acol = torch.zeros(k, dtype=torch.float32, device="cuda")
+    lhs = torch.zeros(1, dtype=torch.float64, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     base = dict(out=out, ldc=n, out_kind="f16", relu=True)
     one = dict(base, fired_count=cnt, m_ext=-(-m // 16) * 16, n_ext=-(-n // 8) * 8)
@@ -34,13 +34,16 @@ def run(m, n, k):
                         **one)
     uplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.UNPROTECTED, plan_only=True, **base)
     ckr = kernels.ck_rows(pw.bt, n, k, P.BINARY16, plan, 8, False)
+    gkw = dict(base, out_sum=osum, out_lhs=lhs)
+    gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True, **gkw)
+    gck = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
     it = 50 if m * n * k < 2 ** 33 else 10
     bt = b.t().contiguous()
     res = {"cublas": graph_time_us(lambda: torch.matmul(a, b), it)}
     res["unprot"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                        P.Scheme.UNPROTECTED, **base), it)
     res["global"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
-                                                       P.Scheme.GLOBAL_ABFT, out_sum=osum, a_colck=acol, **base), it)
+                                                       P.Scheme.GLOBAL_ABFT, ck_rows=gck, **gkw), it)
     res["one_chip"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                          P.Scheme.THREAD_ONE_SIDED, **one), it)
     res["one_off"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
