@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
 
-      if (p.gck && h == 0) {
+      if (p.gck && h == 0 && !(p.debug & 524288)) {
         // global lhs: this row's A . rowck(B tile) = checksum column hi + lo
         float ck_hi, ck_lo;
         __syncwarp();
@@ -1408,6 +1408,12 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
     mo = mb;   // unused
   }
   cudaStream_t st = as_stream(stream);
+  if (getenv("ABFT_TRACE"))
+    fprintf(stderr, "[abft] M=%d N=%d K=%d scheme=%d bn=%d bn_eff=%d nb=%d tiles=%d stages=%d acc=%d cols=%d tmem=%d "
+            "nck=%d ck_mode=%d gck=%d tma_store=%d split=%d a_mode=%d smem=%zu grid=%d cls=%d ntc=%d\n",
+            p.M, p.N, p.K, p.scheme, p.bn, p.bn_eff, p.num_n_blocks, p.num_tiles, p.stages, p.acc_stages,
+            p.cols_per_acc, p.tmem_cols, p.nck_pad, p.ck_mode, p.gck, p.tma_store, p.epi_split, p.a_mode, pl.smem,
+            pl.grid, pl.cls, pl.ntc);
   if (p.debug & 64) pl.cls = CLASS_PLAIN;
   if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
   if (a->dtype == ABFT_BF16)

@@ -46,6 +46,9 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
+    # the struct holds raw device pointers: keep every tensor it points to alive with it
+    args._keep = [x for x in (a, bt, out, faults, out_sum, next_colck, verdicts, fired_count, fired, ck_rows,
+                              a_colck, out_lhs) if x is not None]
     return args
 
 
@@ -77,6 +80,7 @@ def conv_args(x, geom: dict, bt, oc: int, dtype: DType, numeric: int, scheme: Sc
     args.c_real = int(geom.get("c_real", 0))
     if workspace is not None:
         args.workspace, args.ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    args._keep = g._keep + [x] + ([workspace] if workspace is not None else [])
     return args
 
 

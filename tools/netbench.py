@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cudnn", action="store_true", help="also time torch/cuDNN conv2d (channels_last fp16)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "netbench.jsonl"))
+    ap.add_argument("--layers", default="", help="comma-separated layer indices (bring-up)")
     args = ap.parse_args()
 
     import torch
@@ -47,9 +48,13 @@ def main():
         for cfg in args.configs.split(","):
             b, h, w = CONFIGS[cfg]
             specs = networks.capture(net, b, h, w)
+            if args.layers:
+                keep = {int(x) for x in args.layers.split(",")}
+                specs = [sp for sp in specs if sp.index in keep]
             t0 = time.time()
             rows = []
             for spec in specs:
+                print(f"# {net} {cfg} layer {spec.index}: {spec}", file=sys.stderr, flush=True)
                 r = LayerRunner(spec)
                 it = args.iters if r.flops() < 2e11 else max(3, args.iters // 4)
                 t_un = profiler.graph_time_us(lambda: r.conv(S.UNPROTECTED), it)
