@@ -95,6 +95,12 @@ typedef struct {
    * N-slice per tile driven by the offline checksum rows (abft_ck_rows with nt = the plan's
    * bn_eff, split hi/lo, nck_pad = 16) and a row sum in the epilogue.  Needs ck_rows. */
   double* out_lhs;
+  /* optional fused deferred verification (checksum.py:207-211, :237): when the launch's last
+   * CTA finishes, the verdicts of vn layers are formed from vsums [vn][2] (lhs, rhs) with the
+   * tau rule for K = vk[i] and this call's numeric mode, written to vout [vn] and counted into
+   * *vdetected.  vdone is a zero-initialised counter the kernel resets for the next launch.
+   * A chain passes this on its last layer and needs no separate verification launch. */
+  const double* vsums; const int32_t* vk; int32_t vn; int32_t* vdone; abft_verdict_t* vout; int32_t* vdetected;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);

@@ -90,6 +90,8 @@ class GemmArgs(ctypes.Structure):
         ("ck_rows", ctypes.c_void_p), ("ldck", ctypes.c_int64), ("ck_rows_n", ctypes.c_int32),
         ("a_colck", ctypes.c_void_p),
         ("out_lhs", ctypes.c_void_p),
+        ("vsums", ctypes.c_void_p), ("vk", ctypes.c_void_p), ("vn", ctypes.c_int32), ("vdone", ctypes.c_void_p),
+        ("vout", ctypes.c_void_p), ("vdetected", ctypes.c_void_p),
     ]
 
 

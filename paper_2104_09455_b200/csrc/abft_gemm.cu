@@ -70,6 +70,12 @@ struct GemmParams {
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
   double* out_lhs;       // global: += sum_rows A . rowck(B tile) (one checksum N-slice per tile)
+  const double* vsums;   // fused deferred verification (last CTA): [vn][2] (lhs, rhs), K per layer
+  const int* vk;
+  int vn;
+  int* vdone;
+  abft_verdict_t* vout;
+  int* vdetected;
   int gck;               // 1: the global checksum slice is active
   int acolck_mode;       // 1: column sums on the tensor cores (ones x A-tile MMA into TMEM), 2: CUDA cores
   int dck_col;           // TMEM column of the two 64-column column-sum buffers (mode 1)
@@ -1001,10 +1007,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
+  if (p.vn > 0) __threadfence();      // this CTA's checksum atomics before its done-count
   __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+  if (p.vn > 0) {
+    // fused deferred verification: the last CTA of the launch forms every layer's verdict
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) ? 1 : 0;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int i = threadIdx.x; i < p.vn; i += blockDim.x) {
+        const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
+        const double tol = tolerance(p.r, p.vk[i], lhs, rhs);
+        abft_verdict_t v;
+        v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = p.vk[i];
+        v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
+        if (p.vout) p.vout[i] = v;
+        if (v.detected && p.vdetected) atomicAdd(p.vdetected, 1);
+      }
+      if (threadIdx.x == 0) *p.vdone = 0;
+    }
+  }
   if (stamp && threadIdx.x == 32) g_dbg_ts[blockIdx.x][4] = gtimer();
 }
 
@@ -1230,6 +1256,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.next_colck = a->next_colck;
   p.colck_in_smem = (a->next_colck != nullptr && a->N <= COLCK_SMEM_MAX) ? 1 : 0;
   p.verdicts = a->verdicts;
+  p.vsums = a->vsums; p.vk = a->vk; p.vn = (a->vsums && a->vk && a->vdone) ? a->vn : 0;
+  p.vdone = a->vdone; p.vout = a->vout; p.vdetected = a->vdetected;
   p.n_trows = m_ext / mt; p.n_tcols = n_ext / nt;
   p.fired_count = a->fired_count; p.fired = a->fired; p.fired_cap = a->fired_cap;
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;

@@ -53,11 +53,13 @@ class ProtectedChain:
     tiling: TilingConfig = TilingConfig()
     relu_last: bool = True
     ck_split: bool = False
+    faults: Optional[dict] = None        # {layer: [(row, col, delta)]}: deltas added to the fp32 accumulator
     layers: List[_Layer] = field(default_factory=list, init=False)
 
     def __post_init__(self):
         D.require_device()
         t = D.torch()
+        self._fault_dev = {int(i): D.faults_tensor(list(f)) for i, f in (self.faults or {}).items() if f}
         if len(self.schemes) != len(self.weights):
             raise ValueError("one scheme per layer")
         self.numeric = D.numeric_code(self.dtype)
@@ -77,11 +79,12 @@ class ProtectedChain:
         self.acts = [t.zeros((m, L.n), dtype=sd, device="cuda") for L in self.layers]
         nl = len(self.layers)
         # every per-forward accumulator lives in ONE block so a single memset node clears it:
-        # [(lhs, rhs) fp64 per layer][counters int32 x 2]
+        # [(lhs, rhs) fp64 per layer][counters int32 x 2][verification done-count int32, pad]
         off_cnt = 16 * nl
         self.scratch = t.zeros(off_cnt + 16, dtype=t.uint8, device="cuda")
         self.sums = self.scratch[:off_cnt].view(t.float64).view(nl, 2)
         self.counters = self.scratch[off_cnt:off_cnt + 8].view(t.int32)   # [fired thread tiles, flagged layers]
+        self.vdone = self.scratch[off_cnt + 8:off_cnt + 12].view(t.int32)
         self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
         self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
         self._ks_all = t.tensor([L.k for L in self.layers], dtype=t.int32, device="cuda")
@@ -104,6 +107,8 @@ class ProtectedChain:
         m = self.batch
         kw = dict(out=self.acts[i], ldc=self.acts[i].stride(0),
                   out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu)
+        if i in self._fault_dev:
+            kw["faults"], kw["nfaults"] = self._fault_dev[i]
         if L.scheme is Scheme.GLOBAL_ABFT:
             kw["out_lhs"] = self.sums[i, 0:1]
             kw["out_sum"] = self.sums[i, 1:2]
@@ -119,15 +124,16 @@ class ProtectedChain:
             self.x.copy_(x, non_blocking=True)
         kernels.zero(self.scratch)
         a = self.x
+        last = len(self.layers) - 1
         for i, L in enumerate(self.layers):
+            kw = self._gemm_kwargs(i, L)
+            if i == last and self.global_ids:
+                # deferred verification of every layer's (lhs, rhs), fused into the last layer's
+                # launch (its last CTA); layers without the global scheme hold (0, 0), never flag
+                kw["verify"] = (self.sums, self._ks_all, self.vdone, self.verdict_buf, self.counters[1:2])
             kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype, self.numeric,
-                         L.scheme, ck_rows=L.ck_rows, **self._gemm_kwargs(i, L))
+                         L.scheme, ck_rows=L.ck_rows, **kw)
             a = self.acts[i]
-        if self.global_ids:
-            # deferred verification of every layer's (lhs, rhs) in one launch (layers without the
-            # global scheme hold (0, 0) and cannot flag)
-            kernels.verify_sums(self.sums, self._ks_all, len(self.layers), self.numeric, out=self.verdict_buf,
-                                detected_count=self.counters[1:2])
         return a
 
     # ---- multi-GPU helpers (batch sharding): per-layer partial sums, all-reduced by the caller
