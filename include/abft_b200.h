@@ -101,6 +101,10 @@ typedef struct {
    * *vdetected.  vdone is a zero-initialised counter the kernel resets for the next launch.
    * A chain passes this on its last layer and needs no separate verification launch. */
   const double* vsums; const int32_t* vk; int32_t vn; int32_t* vdone; abft_verdict_t* vout; int32_t* vdetected;
+  /* 1: programmatic dependent launch — the kernel's prologue (barrier init, TMEM allocation,
+   * descriptor prefetch) overlaps the previous kernel on the stream; its first operand load
+   * waits for that kernel's completion (griddepcontrol.wait).  For chained layers. */
+  int32_t pdl;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);

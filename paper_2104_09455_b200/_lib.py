@@ -92,6 +92,7 @@ class GemmArgs(ctypes.Structure):
         ("out_lhs", ctypes.c_void_p),
         ("vsums", ctypes.c_void_p), ("vk", ctypes.c_void_p), ("vn", ctypes.c_int32), ("vdone", ctypes.c_void_p),
         ("vout", ctypes.c_void_p), ("vdetected", ctypes.c_void_p),
+        ("pdl", ctypes.c_int32),
     ]
 
 

@@ -73,6 +73,7 @@ struct GemmParams {
   const double* vsums;   // fused deferred verification (last CTA): [vn][2] (lhs, rhs), K per layer
   const int* vk;
   int vn;
+  int pdl;
   int* vdone;
   abft_verdict_t* vout;
   int* vdetected;
@@ -361,6 +362,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     ptx::fence_mbar_init();
   }
+  // programmatic dependent launch: let the next kernel on the stream start its prologue now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
@@ -390,6 +393,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      // the operands may be the previous kernel's outputs: wait for its completion (no-op
+      // unless launched as a programmatic dependent)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = p.stage_a_bytes + p.stage_b_bytes + (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
@@ -972,31 +978,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (stamp && et == 0) g_dbg_ts[blockIdx.x][3] = gtimer();
     // -------- per-CTA flush of the global-ABFT output summation and fused colck
-    if (p.out_sum != nullptr) {
-      double x = rhs_acc;
+    if (p.out_sum != nullptr || p.gck) {
+      // one reduction round for the CTA's global-ABFT partials (rhs, lhs)
+      double x = rhs_acc, y = lhs_acc;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) red_d[et >> 5] = x;
+      for (int o = 16; o >= 1; o >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+      }
+      if (lane == 0) { red_d[et >> 5] = x; red_d[8 + (et >> 5)] = y; }
       ptx::named_bar_sync(3, 256);
       if (et == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < 8; ++w) tot += red_d[w];
-        atomicAdd(p.out_sum, tot);
+        double tx = 0.0, ty = 0.0;
+        for (int w = 0; w < 8; ++w) { tx += red_d[w]; ty += red_d[8 + w]; }
+        if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
+        if (p.gck) atomicAdd(p.out_lhs, ty);
       }
     }
-    if (p.gck) {
-      double x = lhs_acc;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) red_d[8 + (et >> 5)] = x;
-      ptx::named_bar_sync(3, 256);
-      if (et == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < 8; ++w) tot += red_d[8 + w];
-        atomicAdd(p.out_lhs, tot);
-      }
-    }
-    if (p.tma_store && lane == 0) ptx::bulk_wait_all();
+    // the staging buffers must stay valid until the bulk stores have READ them; the writes
+    // themselves complete before the grid does
+    if (p.tma_store && lane == 0) ptx::bulk_wait_read<0>();
     if (p.next_colck != nullptr && p.colck_in_smem) {
       ptx::named_bar_sync(3, 256);
       for (int i = col_lo + et; i < col_hi; i += 256) {
@@ -1014,10 +1015,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
   if (p.vn > 0) {
     // fused deferred verification: the last CTA of the launch forms every layer's verdict
-    __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) ? 1 : 0;
+    int* s_last = reinterpret_cast<int*>(red_d + 16);     // in the barrier block (no static smem)
+    if (threadIdx.x == 0) *s_last = (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) ? 1 : 0;
     __syncthreads();
-    if (s_last) {
+    if (*s_last) {
       __threadfence();
       for (int i = threadIdx.x; i < p.vn; i += blockDim.x) {
         const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
@@ -1102,6 +1103,20 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
+  if (p.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT>, ma, mb, mc, mo, p),
+                      "abft_gemm_kernel launch (PDL)");
+  }
   abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
@@ -1258,6 +1273,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.verdicts = a->verdicts;
   p.vsums = a->vsums; p.vk = a->vk; p.vn = (a->vsums && a->vk && a->vdone) ? a->vn : 0;
   p.vdone = a->vdone; p.vout = a->vout; p.vdetected = a->vdetected;
+  p.pdl = a->pdl;
   p.n_trows = m_ext / mt; p.n_tcols = n_ext / nt;
   p.fired_count = a->fired_count; p.fired = a->fired; p.fired_cap = a->fired_cap;
   const uint32_t fmt = a->dtype == ABFT_BF16 ? 1u : 0u;

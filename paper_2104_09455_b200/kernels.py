@@ -23,7 +23,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-               num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None):
+               num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -46,6 +46,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
+    args.pdl = int(pdl)
     vt = ()
     if verify is not None:
         # fused deferred verification in the launch's last CTA: (sums [n][2], ks [n], done, out, count)

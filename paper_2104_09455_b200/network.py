@@ -54,6 +54,7 @@ class ProtectedChain:
     relu_last: bool = True
     ck_split: bool = False
     faults: Optional[dict] = None        # {layer: [(row, col, delta)]}: deltas added to the fp32 accumulator
+    pdl: bool = True                     # programmatic dependent launch between consecutive layers
     layers: List[_Layer] = field(default_factory=list, init=False)
 
     def __post_init__(self):
@@ -127,6 +128,7 @@ class ProtectedChain:
         last = len(self.layers) - 1
         for i, L in enumerate(self.layers):
             kw = self._gemm_kwargs(i, L)
+            kw["pdl"] = i > 0 and self.pdl       # layer i's prologue overlaps layer i-1
             if i == last and self.global_ids:
                 # deferred verification of every layer's (lhs, rhs), fused into the last layer's
                 # launch (its last CTA); layers without the global scheme hold (0, 0), never flag

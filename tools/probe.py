@@ -24,6 +24,10 @@ for spec in sys.argv[1:]:
         kw["out_sum"] = torch.zeros(1, dtype=torch.float64, device="cuda")
         if acol:
             kw["a_colck"] = torch.zeros(k, dtype=torch.float32, device="cuda")
+        elif len(f) > 6 and f[6] == "gck":
+            kw["out_lhs"] = torch.zeros(1, dtype=torch.float64, device="cuda")
+            gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, plan_only=True, **kw)
+            kw["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
     elif sch is not P.Scheme.UNPROTECTED:
         kw.update(fired_count=torch.zeros(1, dtype=torch.int32, device="cuda"), m_ext=-(-m // 16) * 16,
                   n_ext=-(-n // 8) * 8)
