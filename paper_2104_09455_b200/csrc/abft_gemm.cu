@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][2] = gtimer();
       const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * p.cols_per_acc);
 
-      if (has_ck && !(p.debug & 2) && c_first < p.bn_eff) {
+      if (has_ck && NT == 0 && !(p.debug & 2) && c_first < p.bn_eff) {
         // checksum column per (row, group) of the groups this warp handles -> cks[slot][row]
         float hi[32], lo[32];
         __syncwarp();
@@ -767,6 +767,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
         if constexpr (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
+        // static group width: this chunk's checksum columns straight from TMEM (hi, then lo)
+        constexpr int GPCK = NT > 0 ? 32 / NT : 1;
+        float ckh[GPCK], ckl[GPCK];
+        if constexpr (has_ck && NT > 0) {
+          ptx::tmem_ldn<GPCK>(tacc + bn + c0 / NT, ckh);
+          if (p.split) ptx::tmem_ldn<GPCK>(tacc + bn + p.groups + c0 / NT, ckl);
+        }
         ptx::tmem_ld_wait();
         if (stamp && et == 0 && t_local == 0 && c0 == 0) g_dbg_ts[blockIdx.x][5] = gtimer();
         const int gc0 = n0 + c0;
@@ -776,7 +783,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else if constexpr (thread_level && NT > 0) {
           // static group structure: 32 / NT complete groups per chunk (NT divides 32 and bn_eff)
           constexpr int GPC = 32 / NT;
-          const int slot0 = split ? h * 16 + (c0 >> 6) * GPC : c0 / NT;
 #pragma unroll
           for (int gi = 0; gi < GPC; ++gi) {
             if (gi * NT < cmax) {
@@ -785,7 +791,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if constexpr (has_ck) {
 #pragma unroll
                 for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
-                x = cks[(slot0 + gi) * BM + row];
+                x = p.split ? ckh[gi] + ckl[gi] : ckh[gi];
               } else {
                 if (p.scheme == ABFT_REPL_FULL) {
                   float bk = -FLT_MAX;

@@ -19,7 +19,12 @@ colck = torch.zeros(D.round8(n), dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
 kw = {}
 if sch is P.Scheme.GLOBAL_ABFT:
-    kw = dict(out_sum=osum, next_colck=colck)
+    # the product's global scheme: output summation + the lhs checksum slice
+    lhs = torch.zeros(1, dtype=torch.float64, device="cuda")
+    kw = dict(out_sum=osum, out_lhs=lhs)
+    plan = kernels.gemm(a, k8, pw.bt, pw.ldbt, m, n, k8, P.BINARY16, _lib.NUM_BINARY16, sch, out=out,
+                        ldc=out.stride(0), out_kind="f16", relu=True, plan_only=True, **kw)
+    kw["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k8, P.BINARY16, plan)
 elif sch is not P.Scheme.UNPROTECTED:
     kw = dict(fired_count=cnt, m_ext=-(-m // 16) * 16, n_ext=-(-n // 8) * 8)
     if len(sys.argv) > 6 and sys.argv[6] == "offline":
