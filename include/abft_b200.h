@@ -105,6 +105,12 @@ typedef struct {
    * descriptor prefetch) overlaps the previous kernel on the stream; its first operand load
    * waits for that kernel's completion (griddepcontrol.wait).  For chained layers. */
   int32_t pdl;
+  /* layout of ck_rows: 0 = separate checksum rows (abft_ck_rows, loaded by their own TMA and
+   * multiplied by their own MMA N-slice); 1 = augmented weights (abft_aug_weights): per CTA
+   * N-tile the tile's weight rows followed by its checksum rows, so one TMA box and ONE MMA
+   * instruction (N = tile + checksum columns) per k-step produce outputs and checksums.
+   * With layout 1, ck_rows replaces Bt as the B operand (Bt is still used for shapes). */
+  int32_t ck_layout;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
@@ -121,6 +127,12 @@ int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[8]*/);
  * (the weight-tile checksum of tiled.py:240, prepared once per weight like checksum.py:175). */
 int abft_ck_rows(const void* Bt, int32_t N, int32_t K, int64_t ldbt, int32_t dtype, int32_t bn_eff, int32_t nt,
                  int32_t split, int32_t nck_pad, int32_t n_blocks, void* out, int64_t ldo, void* stream);
+
+/* Augmented weights for a plan (ck_layout 1): out [(n_blocks*(tile_n + nck_pad)) x ldo] (tile_n =
+ * plan out[0]); block nb holds Bt rows nb*bn_eff .. +bn_eff (zero past N and past bn_eff), then
+ * the nck_pad checksum rows of abft_ck_rows for that block. */
+int abft_aug_weights(const void* Bt, int32_t N, int32_t K, int64_t ldbt, int32_t dtype, int32_t tile_n, int32_t bn_eff,
+                     int32_t nt, int32_t split, int32_t nck_pad, int32_t n_blocks, void* out, int64_t ldo, void* stream);
 
 /*
  * Column sums of a row-major [rows x cols] matrix into out[cols] (fp32).

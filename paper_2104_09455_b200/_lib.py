@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "abft_gemm",
     "abft_gemm_plan",
     "abft_ck_rows",
+    "abft_aug_weights",
     "abft_colsum",
     "abft_pack",
     "abft_convert_i64",
@@ -92,7 +93,7 @@ class GemmArgs(ctypes.Structure):
         ("out_lhs", ctypes.c_void_p),
         ("vsums", ctypes.c_void_p), ("vk", ctypes.c_void_p), ("vn", ctypes.c_int32), ("vdone", ctypes.c_void_p),
         ("vout", ctypes.c_void_p), ("vdetected", ctypes.c_void_p),
-        ("pdl", ctypes.c_int32),
+        ("pdl", ctypes.c_int32), ("ck_layout", ctypes.c_int32),
     ]
 
 
@@ -118,6 +119,7 @@ def _declare(lib):
     lib.abft_gemm.argtypes = [ctypes.POINTER(GemmArgs), vp]
     lib.abft_gemm_plan.argtypes = [ctypes.POINTER(GemmArgs), vp]
     lib.abft_ck_rows.argtypes = [vp, i32, i32, i64, i32, i32, i32, i32, i32, i32, vp, i64, vp]
+    lib.abft_aug_weights.argtypes = [vp, i32, i32, i64, i32, i32, i32, i32, i32, i32, i32, vp, i64, vp]
     lib.abft_colsum.argtypes = [vp, i32, i32, i64, i32, vp, i32, vp]
     lib.abft_pack.argtypes = [vp, i32, i32, i64, vp, i32, i64, i32, vp]
     lib.abft_convert_i64.argtypes = [vp, i64, i32, vp, vp]

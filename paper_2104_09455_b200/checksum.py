@@ -226,7 +226,7 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
         kw = dict(out=nxt, ldc=nxt.stride(0), out_kind="bf16" if mode.tag is DTypeTag.BFLOAT16 else "f16",
                   relu=True, faults=f_dev, nfaults=nf, out_sum=sums[idx, 1:2], out_lhs=sums[idx, 0:1])
         plan = kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
-                            plan_only=True, **kw)
+                            plan_only=True, ck_layout=1, **kw)
         ckr = kernels.global_ck_rows(pw.bt, n, dims[idx], mode, plan)
         kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
                      ck_rows=ckr, **kw)

@@ -169,8 +169,14 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
         # lhs from the kernel's checksum slice: sum over rows of A . rowck(B tile)
         kw["out_lhs"] = sums[0:1]
         gplan = kernels.gemm(x_dev, 8, pc.bt, pc.bt.stride(0), m, pc.oc, pl["k"], dtype, numeric, scheme,
-                             plan_only=True, **kw)
+                             plan_only=True, ck_layout=1, **kw)
         kw["ck_rows"] = kernels.global_ck_rows(pc.bt, pc.oc, pl["k"], dtype, gplan)
+    if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED):
+        # weights with each tile's checksum rows appended (one MMA per k-step)
+        oplan = kernels.gemm(x_dev, 8, pc.bt, pc.bt.stride(0), m, pc.oc, pl["k"], dtype, numeric, scheme,
+                             plan_only=True, ck_layout=1, **kw)
+        kw["ck_rows"] = kernels.aug_weights(pc.bt, pc.oc, pl["k"], dtype, oplan, tiling.thread_n,
+                                            not dtype.is_exact)
     kernels.conv2d(kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, workspace=ws, **kw))
     if glob:
         vbuf = t.empty(32, dtype=t.uint8, device="cuda")

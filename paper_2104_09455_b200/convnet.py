@@ -84,7 +84,8 @@ class LayerRunner:
                 # lhs from the kernel's checksum N-slice against the weight tile's row sums
                 kw["out_lhs"] = self.scratch[0:1]
                 gplan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
-                                     self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, **kw)
+                                     self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True,
+                                     ck_layout=1, **kw)
                 kw["ck_rows"] = kernels.global_ck_rows(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype,
                                                        gplan)
         elif scheme is Scheme.THREAD_ONE_SIDED:
@@ -94,13 +95,14 @@ class LayerRunner:
         args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric, scheme,
                                  workspace=self.ws, **kw)
         if scheme is Scheme.THREAD_ONE_SIDED and self.offline_ck:
+            # weights with each tile's checksum rows appended (one MMA per k-step)
             plan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
-                                self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, **kw)
-            if plan["ck_offline_recommended"]:
-                self.ck_rows = kernels.ck_rows(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype, plan,
+                                self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, ck_layout=1,
+                                **kw)
+            self.ck_rows = kernels.aug_weights(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype, plan,
                                                t.thread_n, False)
-                args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric,
-                                         scheme, ck_rows=self.ck_rows, workspace=self.ws, **kw)
+            args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric,
+                                     scheme, ck_rows=self.ck_rows, workspace=self.ws, **kw)
         return args
 
     def flops(self) -> int:

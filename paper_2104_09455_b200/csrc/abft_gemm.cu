@@ -62,7 +62,10 @@ struct GemmParams {
   int num_m_blocks, num_n_blocks, num_tiles, nkb;
   int stages, acc_stages, cols_per_acc, shadow_off, tmem_cols;
   int scheme, out_dtype, relu, split;
-  int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline)
+  int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline),
+                         // 3 appended to the weight tiles (augmented B: one box, one MMA per k-step)
+  int b_rows_blk;        // rows per N-block in the B tensor map (bn, or bn + nck_pad when augmented)
+  uint32_t idesc_aug;    // N = bn + nck_pad (augmented B)
   int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
   double r;
   float rk;              // r * tol_k in fp32, for the guard-banded fast compare
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
   const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
   const bool ck_loaded = (has_ck || p.gck) && p.ck_mode == 2 && !(p.debug & 8);
+  const bool ck_aug = p.ck_mode == 3;
   const int bn = p.bn;
   const bool stamp = (p.debug & 2048) && blockIdx.x < 160;
   if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][0] = gtimer();
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::tma_load_im2col_4d(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
             }
           }
-          ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, n0);
+          ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
           if (ck_loaded) ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.nck_pad);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t adesc = a_desc(a_addr, k);
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
-            ptx::mma_f16_ss(d, adesc, bdesc, p.idesc_main, accum);
+            ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
             if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
             if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
           }
@@ -1229,6 +1233,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
         const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
         const long long waves = (tiles + sms - 1) / sms;
         const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
+        if (a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256) continue;
         const long long cost = waves * (128 + 2LL * cand + nck);
         if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
       }
@@ -1268,6 +1273,11 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc + (p.acolck_mode == 1 ? 32 : 0)));
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
   p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : (gck ? 2 : 0);
+  if ((has_ck || gck) && a->ck_layout == 1) {
+    if (bn + p.nck_pad > 256) return fail(ABFT_E_UNSUPPORTED, "augmented weights need tile_n + checksum rows <= 256");
+    p.ck_mode = 3;
+  }
+  p.b_rows_blk = p.ck_mode == 3 ? bn + p.nck_pad : bn;
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
   p.rk = (float)(p.r * (double)p.tol_k);
@@ -1286,6 +1296,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = (has_ck || gck) ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
   p.idesc_ones = ptx::idesc_f16(fmt, 64, 8) | (1u << 15);    // M=64, N=8, A MN-major
+  p.idesc_aug = ptx::idesc_f16(fmt, BM, (uint32_t)(bn + p.nck_pad));
   {
     const char* dbg = getenv("ABFT_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
@@ -1303,8 +1314,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
 
   // ---- shared memory carve-up (all tile buffers 1024-aligned)
   p.stage_a_bytes = BM * BK * 2;
-  p.stage_b_bytes = bn * BK * 2;
-  p.stage_ck_bytes = (uint32_t)round_up(p.nck_pad * BK * 2, 1024);
+  p.stage_b_bytes = (uint32_t)round_up(p.b_rows_blk * BK * 2, 1024);
+  p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2, 1024);
   p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
   const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
   const uint32_t rec_bytes = p.rec_stride ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
@@ -1380,10 +1391,66 @@ __global__ void ck_rows_kernel(const T* __restrict__ bt, int n, int k, long long
   }
 }
 
+// augmented weights: block nb = [Bt rows nb*bn_eff .. (tile_n rows, zero past bn_eff / N) | checksum rows]
+template <typename T>
+__global__ void aug_weights_kernel(const T* __restrict__ bt, int n, int k, long long ldbt, int tile_n, int bn_eff,
+                                   int nt, int groups, int split, int nck_pad, int n_blocks, T* __restrict__ out,
+                                   long long ldo) {
+  const int blk = tile_n + nck_pad;
+  const long long total = (long long)n_blocks * blk * ldo;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / ldo), kk = (int)(i % ldo);
+    const int nb = row / blk, j = row % blk;
+    float val = 0.f;
+    if (kk < k) {
+      if (j < tile_n) {
+        const int r = nb * bn_eff + j;
+        if (j < bn_eff && r < n) val = (float)bt[(long long)r * ldbt + kk];
+      } else {
+        const int jj = j - tile_n;
+        const int g = (jj < groups) ? jj : (split && jj < 2 * groups ? jj - groups : -1);
+        if (g >= 0) {
+          float acc = 0.f;
+          for (int r = 0; r < nt; ++r) {
+            const int nrow = nb * bn_eff + g * nt + r;
+            if (nrow < n) acc += (float)bt[(long long)nrow * ldbt + kk];
+          }
+          const float hi = (float)ElemTraits<T>::from_f(acc);
+          val = (jj < groups) ? hi : acc - hi;
+        }
+      }
+    }
+    out[i] = ElemTraits<T>::from_f(val);
+  }
+}
+
 }  // namespace
 }  // namespace abft
 
 using namespace abft;
+
+extern "C" __attribute__((visibility("default"))) int abft_aug_weights(const void* Bt, int32_t N, int32_t K,
+                                                                      int64_t ldbt, int32_t dtype, int32_t tile_n,
+                                                                      int32_t bn_eff, int32_t nt, int32_t split,
+                                                                      int32_t nck_pad, int32_t n_blocks, void* out,
+                                                                      int64_t ldo, void* stream) {
+  if (N < 1 || K < 1 || nt < 1 || bn_eff < nt || bn_eff % nt || bn_eff > tile_n || nck_pad < 16 || nck_pad % 16 ||
+      ldo < K || ldbt < K || tile_n + nck_pad > 256)
+    return fail(ABFT_E_SHAPE, "aug_weights: bad extents");
+  const int groups = bn_eff / nt;
+  if (groups * (split ? 2 : 1) > nck_pad) return fail(ABFT_E_SHAPE, "aug_weights: nck_pad too small");
+  if (n_blocks < ceil_div(N, bn_eff)) return fail(ABFT_E_SHAPE, "aug_weights: n_blocks does not cover N");
+  const long long total = (long long)n_blocks * (tile_n + nck_pad) * ldo;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
+  cudaStream_t st = as_stream(stream);
+  if (dtype == ABFT_BF16)
+    aug_weights_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)Bt, N, K, ldbt, tile_n, bn_eff, nt,
+                                                              groups, split, nck_pad, n_blocks, (__nv_bfloat16*)out, ldo);
+  else
+    aug_weights_kernel<__half><<<blocks, 256, 0, st>>>((const __half*)Bt, N, K, ldbt, tile_n, bn_eff, nt, groups, split,
+                                                       nck_pad, n_blocks, (__half*)out, ldo);
+  return cuda_check(cudaGetLastError(), "aug_weights launch");
+}
 
 extern "C" __attribute__((visibility("default"))) int abft_debug_timestamps(unsigned long long* host_out /*[160*8]*/) {
   return cuda_check(cudaMemcpyFromSymbol(host_out, g_dbg_ts, sizeof(g_dbg_ts)), "debug timestamps");
@@ -1437,7 +1504,16 @@ int validate_common(const abft_gemm_args_t* a) {
 int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, void* stream) {
   GemmParams& p = pl.p;
   CUtensorMap mb, mc;
-  int rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
+  int rc;
+  if (p.ck_mode == 3) {
+    // augmented weights: the B operand (tile rows + checksum rows per N-block) is ck_rows
+    if (a->ck_rows == nullptr || a->ck_rows_n != p.num_n_blocks * p.b_rows_blk || a->ldck < a->K || (a->ldck % 8) ||
+        (reinterpret_cast<uintptr_t>(a->ck_rows) & 15))
+      return fail(ABFT_E_SHAPE, "augmented weights do not match this call's plan (see abft_gemm_plan / abft_aug_weights)");
+    rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.b_rows_blk);
+  } else {
+    rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
+  }
   if (rc != ABFT_OK) return rc;
   if (p.ck_mode == 2) {
     if (a->ck_rows == nullptr || a->ck_rows_n != p.num_n_blocks * p.nck_pad || a->ldck < a->K || (a->ldck % 8) ||

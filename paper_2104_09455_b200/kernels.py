@@ -23,7 +23,8 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                relu: bool = False, thread_m: int = 16, thread_n: int = 8, m_ext: int = 0, n_ext: int = 0,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
-               num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False):
+               num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
+               ck_layout: int = None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -44,6 +45,10 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     args.tile_n, args.num_sms = tile_n, num_sms
     if ck_rows is not None:
         args.ck_rows, args.ldck, args.ck_rows_n = ck_rows.data_ptr(), ck_rows.stride(0), ck_rows.shape[0]
+    if ck_layout is not None:
+        args.ck_layout = int(ck_layout)
+    elif ck_rows is not None:
+        args.ck_layout = int(getattr(ck_rows, "_abft_aug", 0))
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
     args.pdl = int(pdl)
@@ -133,9 +138,24 @@ def ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, split: 
     return out
 
 
-def global_ck_rows(bt, n: int, k: int, dtype: DType, plan: dict):
+def aug_weights(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, split: bool):
+    """Augmented weights of a plan (ck_layout 1): each CTA N-tile's weight rows followed by its
+    checksum rows, so the tile's outputs and checksums come from one MMA instruction."""
+    t = torch()
+    blk = plan["tile_n"] + plan["nck_pad"]
+    out = t.empty((plan["n_blocks"] * blk, bt.shape[1]), dtype=bt.dtype, device="cuda")
+    _lib.call("abft_aug_weights", ptr(bt), n, k, bt.stride(0), storage_code(dtype), plan["tile_n"], plan["bn_eff"],
+              thread_n, int(split), plan["nck_pad"], plan["n_blocks"], ptr(out), out.stride(0), stream_handle())
+    out._abft_aug = 1
+    return out
+
+
+def global_ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, augmented: bool = True):
     """Checksum rows of the global scheme's lhs slice: per CTA N-tile, the hi/lo split of the
-    tile's weight row sums (abft_ck_rows with nt = bn_eff), for the plan of an out_lhs call."""
+    tile's weight row sums (nt = bn_eff), for the plan of an out_lhs call — appended to the
+    weight tiles (default) or as separate rows (abft_ck_rows)."""
+    if augmented:
+        return aug_weights(bt, n, k, dtype, plan, plan["bn_eff"], True)
     return ck_rows(bt, n, k, dtype, plan, plan["bn_eff"], True)
 
 

@@ -94,14 +94,15 @@ class ProtectedChain:
         # check's rows where the plan says B tiles are re-read by several M-blocks
         for i, L in enumerate(self.layers):
             if L.scheme in (Scheme.THREAD_ONE_SIDED, Scheme.GLOBAL_ABFT):
+                # weights with each tile's checksum rows appended: outputs and checksums from one MMA
                 kw = self._gemm_kwargs(i, L)
                 plan = kernels.gemm(self.x, self.x.stride(0), L.pw.bt, L.pw.ldbt, self.batch, L.n, L.k, self.dtype,
-                                    self.numeric, L.scheme, plan_only=True, **kw)
+                                    self.numeric, L.scheme, plan_only=True, ck_layout=1, **kw)
                 if L.scheme is Scheme.GLOBAL_ABFT:
                     L.ck_rows = kernels.global_ck_rows(L.pw.bt, L.n, L.k, self.dtype, plan)
-                elif plan["ck_offline_recommended"]:
-                    L.ck_rows = kernels.ck_rows(L.pw.bt, L.n, L.k, self.dtype, plan, self.tiling.thread_n,
-                                                self.ck_split)
+                else:
+                    L.ck_rows = kernels.aug_weights(L.pw.bt, L.n, L.k, self.dtype, plan, self.tiling.thread_n,
+                                                    self.ck_split)
 
     def _gemm_kwargs(self, i: int, L: _Layer) -> dict:
         t = self.tiling

@@ -150,21 +150,29 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
     sums = t.zeros(2, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
     out_sum = sums[1:2] if sums is not None else None
     out_lhs = sums[0:1] if sums is not None else None
-    if ck_source not in ("auto", "onchip", "offline"):
-        raise ValueError(f"ck_source must be 'auto', 'onchip' or 'offline', got {ck_source!r}")
+    if ck_source not in ("auto", "aug", "onchip", "offline"):
+        raise ValueError(f"ck_source must be 'auto', 'aug', 'onchip' or 'offline', got {ck_source!r}")
+    if ck_source == "auto":
+        ck_source = "aug"
     split = ck_split and not dtype.is_exact
     call = dict(out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
                 m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
                 out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, out_lhs=out_lhs)
     ckr = None
+    # checksum rows of the weights: appended to each weight tile ("aug": one MMA per k-step),
+    # as separate rows ("offline": their own MMA slice) or generated on chip ("onchip")
     if scheme is Scheme.GLOBAL_ABFT:
+        aug = ck_source != "offline"
         gplan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
-                             plan_only=True, **call)
-        ckr = kernels.global_ck_rows(bt_dev, n, k, dtype, gplan)
+                             plan_only=True, ck_layout=int(aug), **call)
+        ckr = kernels.global_ck_rows(bt_dev, n, k, dtype, gplan, augmented=aug)
     if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED) and ck_source != "onchip":
+        aug = ck_source == "aug"
         plan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
-                            plan_only=True, **call)
-        if ck_source == "offline" or plan["ck_offline_recommended"]:
+                            plan_only=True, ck_layout=int(aug), **call)
+        if aug:
+            ckr = kernels.aug_weights(bt_dev, n, k, dtype, plan, tiling.thread_n, split)
+        else:
             ckr = kernels.ck_rows(bt_dev, n, k, dtype, plan, tiling.thread_n, split)
     kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
                  ck_rows=ckr, **call)

@@ -172,7 +172,7 @@ def test_reference_tolerance_is_vacuous_for_k_at_least_1024(P):
             assert rep.detected is False
 
 
-@pytest.mark.parametrize("source", ["onchip", "offline"])
+@pytest.mark.parametrize("source", ["onchip", "offline", "aug"])
 @pytest.mark.parametrize("tiling", [dict(thread_m=16, thread_n=8), dict(thread_m=6, thread_n=6, warp_m=24, warp_n=24,
                                                                         tb_m=48, tb_n=48, k_step=3),
                                     dict(thread_m=32, thread_n=16, warp_m=64, warp_n=64)])
@@ -194,7 +194,7 @@ def test_checksum_sources_agree(P, source, tiling):
     xf = rng.uniform(-1, 1, size=(600, 320)).astype(np.float16)
     wf = rng.uniform(-1, 1, size=(320, 256)).astype(np.float16)
     r1 = P.execute(xf, wf, t, P.Scheme.THREAD_ONE_SIDED, ck_source="onchip")
-    r2 = P.execute(xf, wf, t, P.Scheme.THREAD_ONE_SIDED, ck_source="offline")
+    r2 = P.execute(xf, wf, t, P.Scheme.THREAD_ONE_SIDED, ck_source="offline" if source == "onchip" else source)
     assert [(v.detected, v.max_abs_diff, v.tolerance_used) for v in r1.verdicts] == \
            [(v.detected, v.max_abs_diff, v.tolerance_used) for v in r2.verdicts]
 

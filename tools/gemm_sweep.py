@@ -34,8 +34,12 @@ def run(m, n, k):
                         **one)
     uplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.UNPROTECTED, plan_only=True, **base)
     ckr = kernels.ck_rows(pw.bt, n, k, P.BINARY16, plan, 8, False)
+    aplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.THREAD_ONE_SIDED, plan_only=True,
+                         ck_layout=1, **one)
+    augw = kernels.aug_weights(pw.bt, n, k, P.BINARY16, aplan, 8, False)
     gkw = dict(base, out_sum=osum, out_lhs=lhs)
-    gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True, **gkw)
+    gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True,
+                         ck_layout=1, **gkw)
     gck = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
     it = 50 if m * n * k < 2 ** 33 else 10
     bt = b.t().contiguous()
@@ -48,6 +52,8 @@ def run(m, n, k):
                                                          P.Scheme.THREAD_ONE_SIDED, **one), it)
     res["one_off"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                         P.Scheme.THREAD_ONE_SIDED, ck_rows=ckr, **one), it)
+    res["one_aug"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
+                                                        P.Scheme.THREAD_ONE_SIDED, ck_rows=augw, **one), it)
     del bt
     tf = 2 * m * n * k / (res["unprot"] * 1e-6) / 1e12
     gbs = 2 * (m * k + k * n + m * n) / (res["unprot"] * 1e-6) / 1e9

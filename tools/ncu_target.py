@@ -23,11 +23,15 @@ if sch is P.Scheme.GLOBAL_ABFT:
     lhs = torch.zeros(1, dtype=torch.float64, device="cuda")
     kw = dict(out_sum=osum, out_lhs=lhs)
     plan = kernels.gemm(a, k8, pw.bt, pw.ldbt, m, n, k8, P.BINARY16, _lib.NUM_BINARY16, sch, out=out,
-                        ldc=out.stride(0), out_kind="f16", relu=True, plan_only=True, **kw)
+                        ldc=out.stride(0), out_kind="f16", relu=True, plan_only=True, ck_layout=1, **kw)
     kw["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k8, P.BINARY16, plan)
 elif sch is not P.Scheme.UNPROTECTED:
     kw = dict(fired_count=cnt, m_ext=-(-m // 16) * 16, n_ext=-(-n // 8) * 8)
-    if len(sys.argv) > 6 and sys.argv[6] == "offline":
+    if len(sys.argv) <= 6 or sys.argv[6] == "aug":
+        plan = kernels.gemm(a, k8, pw.bt, pw.ldbt, m, n, k8, P.BINARY16, _lib.NUM_BINARY16, sch, out=out,
+                            ldc=out.stride(0), out_kind="f16", relu=True, plan_only=True, ck_layout=1, **kw)
+        kw["ck_rows"] = kernels.aug_weights(pw.bt, n, k8, P.BINARY16, plan, 8, False)
+    elif sys.argv[6] == "offline":
         plan = kernels.gemm(a, k8, pw.bt, pw.ldbt, m, n, k8, P.BINARY16, _lib.NUM_BINARY16, sch, out=out,
                             ldc=out.stride(0), out_kind="f16", relu=True, plan_only=True, **kw)
         kw["ck_rows"] = kernels.ck_rows(pw.bt, n, k8, P.BINARY16, plan, 8, False)
