@@ -1224,8 +1224,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     int best = 0;
     for (int pass = 0; pass < 2 && best == 0; ++pass) {
       long long best_cost = 0;
-      for (int cand : {256, 224, 192, 128, 64, 32}) {
+      for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
         if (cand < nt || (thread_level && cand / nt > 32)) continue;
+        if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
         const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
         if (cols + extra_cols > 512) continue;
         if (pass == 0 && 2 * cols + extra_cols > 512) continue;                      // pass 0: double-buffered only
@@ -1241,8 +1242,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     bn = best;
     if (bn == 0) return fail(ABFT_E_UNSUPPORTED, "no CTA tile fits this thread tile");
   }
-  if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 224 && bn != 256)
-    return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/192/224/256");
+  if (bn != 32 && bn != 64 && bn != 128 && bn != 192 && bn != 224 && bn != 240 && bn != 256)
+    return fail(ABFT_E_VALUE, "tile_n must be 32/64/128/192/224/240/256");
   if (bn < nt) return fail(ABFT_E_UNSUPPORTED, "thread_n larger than the CTA tile");
 
   GemmParams& p = out.p;
