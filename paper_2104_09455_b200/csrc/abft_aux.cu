@@ -200,38 +200,57 @@ __global__ void conv_pack_weight_kernel(const uint16_t* __restrict__ w, int oc, 
 
 // Explicit im2col of an NHWC input into A [M x ld] (row m = (n*P + p)*Q + q, column
 // (ri*S + si)*cr + c over the cr real channels, zero for padding / columns >= R*S*cr):
-// the lowering of shapes.py:169-177, used for convs with few input channels.
+// the lowering of shapes.py:169-177, used for convs with few input channels (network stems).
+// A CTA builds IM2COL_PIX output rows in shared memory: each (pixel, filter row) task reads
+// the S input pixels of that window row as 16-byte channel vectors (C is a multiple of 8) and
+// scatters their cr real channels; the finished rows leave as coalesced 16-byte stores.
+constexpr int IM2COL_PIX = 64;
+
 __global__ void __launch_bounds__(256) im2col_kernel(const uint16_t* __restrict__ x, int H, int W, int C, int cr,
                                                      int R, int S, int sh, int sw, int ph, int pw, int P, int Q,
                                                      long long M, int K, int ld, uint16_t* __restrict__ out) {
-  const int vpr = ld / 8;                       // 16-byte vectors per row
-  const long long total = M * vpr;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long m = i / vpr;
-    const int v = (int)(i - m * vpr);
-    const int pq = P * Q;
-    const int n = (int)(m / pq);
-    const int rem = (int)(m - (long long)n * pq);
-    const int p = rem / Q, q = rem - p * Q;
-    uint16_t e[8];
+  extern __shared__ uint16_t tile[];          // [IM2COL_PIX][ld]
+  const int cv = C / 8;                        // 16-byte channel vectors per pixel
+  const int pq = P * Q;
+  for (long long m0 = (long long)blockIdx.x * IM2COL_PIX; m0 < M; m0 += (long long)gridDim.x * IM2COL_PIX) {
+    const int npix = (int)min((long long)IM2COL_PIX, M - m0);
+    // zero the tile (padding taps, channels >= cr, columns >= K)
+    for (int i = threadIdx.x; i < IM2COL_PIX * ld / 8; i += blockDim.x)
+      reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    // tasks: (pixel, filter row, channel vector)
+    const int ntask = npix * R * cv;
+    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+      const int v = t % cv;
+      const int pr = t / cv;
+      const int ri = pr % R, pl = pr / R;
+      const long long m = m0 + pl;
+      const int n = (int)(m / pq);
+      const int rem = (int)(m - (long long)n * pq);
+      const int p = rem / Q, q = rem - p * Q;
+      const int hh = p * sh - ph + ri;
+      if (hh < 0 || hh >= H) continue;
+      const uint16_t* rowp = x + ((long long)n * H + hh) * W * C;
+      uint16_t* dst = tile + pl * ld + ri * S * cr;
+      for (int si = 0; si < S; ++si) {
+        const int ww = q * sw - pw + si;
+        if (ww < 0 || ww >= W) continue;
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(rowp + (long long)ww * C) + v);
+        const uint16_t* e = reinterpret_cast<const uint16_t*>(&u);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = v * 8 + j;
-      uint16_t val = 0;
-      if (k < K) {
-        const int tap = k / cr, c = k - tap * cr;
-        const int ri = tap / S, si = tap - ri * S;
-        const int hh = p * sh - ph + ri, ww = q * sw - pw + si;
-        if (hh >= 0 && hh < H && ww >= 0 && ww < W) val = __ldg(x + (((long long)n * H + hh) * W + ww) * C + c);
+        for (int j = 0; j < 8; ++j) {
+          const int c = v * 8 + j;
+          if (c < cr) dst[si * cr + c] = e[j];
+        }
       }
-      e[j] = val;
     }
-    uint4 u;
-    u.x = e[0] | ((uint32_t)e[1] << 16);
-    u.y = e[2] | ((uint32_t)e[3] << 16);
-    u.z = e[4] | ((uint32_t)e[5] << 16);
-    u.w = e[6] | ((uint32_t)e[7] << 16);
-    *reinterpret_cast<uint4*>(out + m * ld + v * 8) = u;
+    __syncthreads();
+    const int vpr = ld / 8;
+    for (int i = threadIdx.x; i < npix * vpr; i += blockDim.x) {
+      const int pl = i / vpr, vv = i - pl * vpr;
+      reinterpret_cast<uint4*>(out + (m0 + pl) * ld)[vv] = reinterpret_cast<const uint4*>(tile + pl * ld)[vv];
+    }
+    __syncthreads();
   }
 }
 
@@ -300,6 +319,23 @@ __global__ void __launch_bounds__(256) conv_colck_kernel(const T* __restrict__ x
     if (part[i] != 0.f) atomicAdd(&out[i], part[i]);
 }
 
+
+int launch_im2col(const void* x, int n, int h, int w, int c, int cr, int r, int s, int sh, int sw, int ph, int pw,
+                  int P, int Q, int K, int ld, void* out, cudaStream_t st) {
+  const long long M = (long long)n * P * Q;
+  const size_t smem = (size_t)IM2COL_PIX * ld * 2;
+  if (smem > 200 * 1024) return fail(ABFT_E_UNSUPPORTED, "im2col: row too long for the shared-memory tile");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const long long tiles = (M + IM2COL_PIX - 1) / IM2COL_PIX;
+  int blocks = (int)std::min<long long>(tiles, 8LL * num_sms());
+  im2col_kernel<<<blocks, 256, smem, st>>>((const uint16_t*)x, h, w, c, cr, r, s, sh, sw, ph, pw, P, Q, M, K, ld,
+                                          (uint16_t*)out);
+  return cuda_check(cudaGetLastError(), "im2col launch");
+}
 }  // namespace abft
 
 using namespace abft;
@@ -316,17 +352,7 @@ extern "C" __attribute__((visibility("default"))) int abft_conv_pack_weight(cons
   return cuda_check(cudaGetLastError(), "conv_pack_weight launch");
 }
 
-namespace abft {
-int launch_im2col(const void* x, int n, int h, int w, int c, int cr, int r, int s, int sh, int sw, int ph, int pw,
-                  int P, int Q, int K, int ld, void* out, cudaStream_t st) {
-  const long long M = (long long)n * P * Q;
-  const long long total = M * (ld / 8);
-  int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
-  im2col_kernel<<<blocks, 256, 0, st>>>((const uint16_t*)x, h, w, c, cr, r, s, sh, sw, ph, pw, P, Q, M, K, ld,
-                                        (uint16_t*)out);
-  return cuda_check(cudaGetLastError(), "im2col launch");
-}
-}  // namespace abft
+
 
 extern "C" __attribute__((visibility("default"))) int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w,
                                                                      int32_t c, int32_t r, int32_t s, int32_t stride_h,
