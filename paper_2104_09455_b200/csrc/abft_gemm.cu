@@ -107,6 +107,12 @@ struct GemmParams {
   // (no swizzle, 8 (tap, chunk) pairs per k-block)
   int a_mode;
   int cv_P, cv_Q, cv_S, cv_sh, cv_sw, cv_ph, cv_pw, cv_chunks, cv_pairs, cv_c;
+  // a_mode 4 (halo reuse, stride-1 convs): a k-block is (filter row r, 64-channel chunk); one TMA
+  // box loads the input-row window of the tile's Qt = bm_eff output pixels plus S-1 halo pixels,
+  // and the S filter taps of that row read it at row offsets 0..S-1 (no per-tap reload)
+  uint32_t tx_a;         // bytes of one A box (the window), for the full-barrier count
+  uint32_t b_tile_bytes; // one [b_rows x 64] B tile (a halo stage holds S of them)
+  int cv_kstride;        // packed-weight channel stride (ck)
   int debug;   // ABFT_DEBUG bits (bring-up experiments only): 1 skip verdicts, 2 skip checksum TMEM load, 4 skip checksum MMA
 };
 
@@ -402,7 +408,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = p.stage_a_bytes + p.stage_b_bytes + (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
+      const uint32_t tx = (p.a_mode == 4 ? p.tx_a : p.stage_a_bytes) + p.stage_b_bytes +
+                          (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         const int nb = tile % p.num_n_blocks;
         const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
@@ -422,7 +429,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&empty[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], tx);
           uint8_t* a_dst = sm_a + s * p.stage_a_bytes;
-          if (p.a_mode == 0) {
+          if (p.a_mode == 4) {
+            // window of input row (p + r - pad), columns q0 - pad .. q0 - pad + Qt + S - 2
+            const int r = kb / p.cv_chunks;
+            const int cc = kb - r * p.cv_chunks;
+            ptx::tma_load_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
+            const int brow = ck_aug ? nb * p.b_rows_blk : n0;
+#pragma unroll 1
+            for (int si = 0; si < p.cv_S; ++si)
+              ptx::tma_load_2d(sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, &full[s],
+                               (r * p.cv_S + si) * p.cv_kstride + cc * BK, brow);
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+            continue;
+          } else if (p.a_mode == 0) {
             ptx::tma_load_2d(a_dst, &tmA, &full[s], kb * BK, m0);
           } else if (p.a_mode == 1) {
             const int tap = kb / p.cv_chunks;
@@ -480,6 +499,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
           const uint32_t b_addr = ptx::smem_u32(sm_b + s * p.stage_b_bytes);
           const uint32_t c_addr = ptx::smem_u32(sm_ck + s * p.stage_ck_bytes);
+          if (p.a_mode == 4) {
+            // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile
+#pragma unroll 1
+            for (int si = 0; si < p.cv_S; ++si) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + (uint32_t)si * 128u + (uint32_t)k * 32u) |
+                                       (p.debug & 1048576 ? ((uint64_t)(si & 7) << 49) : 0ull);
+                const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + (uint32_t)si * p.b_tile_bytes + k * 32);
+                ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, (kb | si | k) != 0 ? 1u : 0u);
+              }
+            }
+            ptx::mma_commit(&empty[s]);
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t adesc = a_desc(a_addr, k);
@@ -1173,6 +1208,12 @@ uint32_t pow2_at_least(uint32_t x) {
   return r;
 }
 
+struct ConvGeom {
+  int a_mode, ck, P, Q, K, cr;
+  long long ws;
+  int R, S, chunks, Qt;     // halo mode (4): filter extents, 64-channel chunks, output pixels per tile
+};
+
 struct Plan {
   GemmParams p;
   int cls, ntc;
@@ -1189,7 +1230,8 @@ int tile_cols(int bn, int nt, bool has_ck, bool has_shadow, int split) {
 }
 
 // Choose the CTA tile and carve shared memory / TMEM for one call.
-int make_plan(const abft_gemm_args_t* a, Plan& out) {
+int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr) {
+  const bool halo = cg != nullptr && cg->a_mode == 4;
   if (a == nullptr) return fail(ABFT_E_VALUE, "null args");
   if (a->M < 1 || a->N < 1 || a->K < 1) return fail(ABFT_E_SHAPE, "GEMM extents must be >= 1");
   if (a->dtype != ABFT_F16 && a->dtype != ABFT_BF16) return fail(ABFT_E_VALUE, "dtype must be ABFT_F16 or ABFT_BF16");
@@ -1212,7 +1254,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
   const int extra_cols = want_acolck ? 32 : 0;
   const int sms = a->num_sms > 0 ? a->num_sms : num_sms();
-  const int bm_eff = (BM / mt) * mt;
+  const int bm_eff = halo ? cg->Qt : (BM / mt) * mt;
+  if (halo && bm_eff % mt) return fail(ABFT_E_UNSUPPORTED, "halo tile is not a multiple of the thread tile");
   const int m_blocks = ceil_div(m_ext, bm_eff);
 
   int bn = a->tile_n;
@@ -1263,7 +1306,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   p.num_m_blocks = m_blocks;
   p.num_n_blocks = ceil_div(n_ext, p.bn_eff);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  p.nkb = ceil_div(a->K, BK);
+  p.nkb = halo ? cg->R * cg->chunks : ceil_div(a->K, BK);
   p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
   p.shadow_off = bn + p.nck_pad;
   if (p.cols_per_acc > 512) return fail(ABFT_E_UNSUPPORTED, "TMEM budget exceeded");
@@ -1279,6 +1322,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
     p.ck_mode = 3;
   }
   p.b_rows_blk = p.ck_mode == 3 ? bn + p.nck_pad : bn;
+  if (halo && (p.ck_mode == 1 || p.ck_mode == 2 || want_acolck))
+    return fail(ABFT_E_UNSUPPORTED, "halo conv mode needs augmented checksum weights");
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
   p.rk = (float)(p.r * (double)p.tol_k);
@@ -1316,6 +1361,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out) {
   // ---- shared memory carve-up (all tile buffers 1024-aligned)
   p.stage_a_bytes = BM * BK * 2;
   p.stage_b_bytes = (uint32_t)round_up(p.b_rows_blk * BK * 2, 1024);
+  p.b_tile_bytes = p.stage_b_bytes;
+  if (halo) {
+    // one input-row window [Qt + S - 1 pixels x 64 channels] and the S taps' B tiles per stage
+    p.tx_a = (uint32_t)(cg->Qt + cg->S - 1) * BK * 2;
+    p.stage_a_bytes = (uint32_t)round_up((int)p.tx_a, 1024);
+    p.stage_b_bytes = p.b_tile_bytes * (uint32_t)cg->S;
+  }
   p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2, 1024);
   p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
   const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
@@ -1562,10 +1614,6 @@ PFN_cuTensorMapEncodeIm2col_v12000 get_im2col_fn() {
   return fn;
 }
 
-struct ConvGeom {
-  int a_mode, ck, P, Q, K, cr;
-  long long ws;
-};
 
 int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   if (c->n < 1 || c->h < 1 || c->w < 1 || c->c < 1 || c->r < 1 || c->s < 1)
@@ -1583,15 +1631,37 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   if (g.cr > c->c) return fail(ABFT_E_SHAPE, "c_real exceeds the physical channel count");
   const char* force = getenv("ABFT_CONV_MODE");     // bring-up / measurement override
   int mode = pointwise ? 0 : (c->c % 64 == 0 ? 1 : (c->c >= 48 ? 1 : 3));
-  if (force && !pointwise) mode = atoi(force);
+  // halo reuse (mode 4): stride 1, a tile of Qt | Q output pixels in one output row, so every
+  // filter row's S taps come from one input-row window; needs checksum rows appended to the
+  // weights (or none) and no in-kernel activation checksum
+  g.R = c->r; g.S = c->s; g.Qt = 0;
+  {
+    const bool thread_level = c->gemm.scheme >= ABFT_ONE_SIDED;
+    const bool ck_ok = c->gemm.scheme == ABFT_UNPROTECTED ||
+                       (c->gemm.scheme == ABFT_GLOBAL ? (c->gemm.out_lhs == nullptr || c->gemm.ck_layout == 1)
+                                                      : (c->gemm.ck_layout == 1 && c->gemm.ck_rows != nullptr));
+    const int mt = thread_level ? std::max(1, c->gemm.thread_m) : 1;
+    if (mode == 1 && c->stride_h == 1 && c->stride_w == 1 && c->s <= 16 && ck_ok && c->gemm.a_colck == nullptr &&
+        c->gemm.scheme != ABFT_REPL_FULL && c->gemm.scheme != ABFT_REPL_SINGLE) {
+      for (int t = 128; t >= 64; t -= 16)
+        if (g.Q % t == 0 && t % mt == 0) { g.Qt = t; break; }
+      if (g.Qt) mode = 4;
+    }
+  }
+  if (force && !pointwise) {
+    const int fm = atoi(force);
+    if (fm != 4 || g.Qt) mode = fm;
+    if (fm == 4 && !g.Qt) mode = c->c % 64 == 0 || c->c >= 48 ? 1 : 3;
+  }
   g.a_mode = mode;
   g.ws = 0;
   if (mode == 0 || mode == 2) {
     g.ck = c->c;
     g.K = c->r * c->s * c->c;
-  } else if (mode == 1) {
+  } else if (mode == 1 || mode == 4) {
     g.ck = (c->c + 63) / 64 * 64;            // channels past c arrive as zeros from the TMA
     g.K = c->r * c->s * g.ck;
+    g.chunks = g.ck / 64;
   } else {
     g.ck = g.cr;                              // dense (r, s, c_real) columns
     g.K = (c->r * c->s * g.cr + 7) / 8 * 8;
@@ -1678,9 +1748,31 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
   rc = validate_common(&ga);
   if (rc != ABFT_OK) return rc;
   Plan pl;
-  rc = make_plan(&ga, pl);
+  rc = make_plan(&ga, pl, &g);
   if (rc != ABFT_OK) return rc;
   GemmParams& p = pl.p;
+  if (g.a_mode == 4) {
+    p.a_mode = 4;
+    p.cv_P = g.P; p.cv_Q = g.Q; p.cv_S = c->s;
+    p.cv_sh = 1; p.cv_sw = 1; p.cv_ph = c->pad_h; p.cv_pw = c->pad_w;
+    p.cv_c = c->c;
+    p.cv_chunks = g.chunks;
+    p.cv_kstride = g.ck;
+    // A: 4-D tiled map over the NHWC input, box = one input-row window of Qt + S - 1 pixels
+    auto enc = get_encode_fn();
+    if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    CUtensorMap ma;
+    const cuuint64_t C = (cuuint64_t)c->c;
+    cuuint64_t dims[4] = {C, (cuuint64_t)c->w, (cuuint64_t)c->h, (cuuint64_t)c->n};
+    cuuint64_t strides[3] = {C * 2, C * 2 * (cuuint64_t)c->w, C * 2 * (cuuint64_t)c->w * (cuuint64_t)c->h};
+    cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)(g.Qt + c->s - 1), 1u, 1u};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&ma, c->gemm.dtype == ABFT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     4, const_cast<void*>(c->gemm.A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ABFT_E_CUDA, "halo window map encode failed: " + std::to_string((int)r));
+    return launch_with_a(&ga, pl, ma, stream);
+  }
   if (g.a_mode == 3) {
     // explicit im2col into the caller's workspace, then the plain GEMM on it
     if (c->workspace == nullptr || c->ws_bytes < g.ws || (reinterpret_cast<uintptr_t>(c->workspace) & 15))

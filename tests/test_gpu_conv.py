@@ -26,6 +26,11 @@ CASES = [
     (1, 35, 33, 3, 16, 11, 11, 4, 2),    # AlexNet stem geometry
     (2, 9, 9, 24, 136, 5, 5, 1, 2),      # several 8-channel chunks per tap, N > one CTA tile
     (1, 8, 8, 128, 64, 3, 3, 1, 1),      # two 64-channel chunks per tap
+    # halo reuse (mode 4): stride 1 and Q divisible into 64..128-pixel row tiles
+    (1, 6, 64, 64, 48, 3, 3, 1, 1),      # Qt = 64
+    (2, 5, 112, 96, 80, 3, 3, 1, 1),     # Qt = 112 (16 junk MMA rows), C = 96 -> 2 zero-padded chunks
+    (1, 4, 128, 64, 32, 5, 5, 1, 2),     # Qt = 128, 5x5 taps
+    (1, 3, 96, 64, 144, 3, 3, 1, 1),     # Qt = 96, two N tiles
 ]
 
 
@@ -133,7 +138,7 @@ def test_conv_global_fused_and_standalone_checksums_agree(P, case):
         assert va.detected == bool(faults)
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
 def test_conv_every_a_load_mode_bit_exact(P, mode, monkeypatch):
     """Each A-load mode (64-channel TMA im2col, 8-channel TMA im2col, explicit im2col) on the
     same non-pointwise cases gives the oracle's exact-int outputs and verdicts."""
