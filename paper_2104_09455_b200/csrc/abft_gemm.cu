@@ -65,6 +65,7 @@ struct GemmParams {
   int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline),
                          // 3 appended to the weight tiles (augmented B: one box, one MMA per k-step)
   int b_rows_blk;        // rows per N-block in the B tensor map (bn, or bn + nck_pad when augmented)
+  int b_resident;        // 1: single N-block whose whole B (all k-blocks) stays in smem (weight-stationary)
   uint32_t idesc_aug;    // N = bn + nck_pad (augmented B)
   int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
   double r;
@@ -341,7 +342,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* dfull = tempty + 2;     // column-sum TMEM buffers (acolck_mode 1), DCK_BUFS deep
   uint64_t* dempty = dfull + DCK_BUFS;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + DCK_BUFS);
+  uint64_t* bres = dempty + DCK_BUFS;    // resident-B loaded (b_resident)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bres + 2);
   double* red_d = reinterpret_cast<double*>(tmem_holder + 4);
 
   const int warp = threadIdx.x >> 5;
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
       ptx::mbar_init(&empty[s], p.acolck_mode == 2 ? 5 : 1);   // + one arrival per CUDA-core A-checksum warp
     }
+    ptx::mbar_init(bres, 1);
     for (int a = 0; a < DCK_BUFS; ++a) {
       ptx::mbar_init(&dfull[a], 1);
       ptx::mbar_init(&dempty[a], 4);    // one arrival per checksum warp
@@ -408,8 +411,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = (p.a_mode == 4 ? p.tx_a : p.stage_a_bytes) + p.stage_b_bytes +
+      const uint32_t tx = (p.a_mode == 4 ? p.tx_a : p.stage_a_bytes) + (p.b_resident ? 0u : p.stage_b_bytes) +
                           (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
+      if (p.b_resident && blockIdx.x < p.num_tiles) {
+        // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
+        // tap of the k-block's filter row), loaded once per CTA
+        ptx::mbar_arrive_expect_tx(bres, (uint32_t)p.nkb * p.stage_b_bytes);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          if (p.a_mode == 4) {
+            const int r = kb / p.cv_chunks, cc = kb - (kb / p.cv_chunks) * p.cv_chunks;
+            for (int si = 0; si < p.cv_S; ++si)
+              ptx::tma_load_2d(sm_b + kb * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, bres,
+                               (r * p.cv_S + si) * p.cv_kstride + cc * BK, 0);
+          } else {
+            ptx::tma_load_2d(sm_b + kb * p.stage_b_bytes, &tmB, bres, kb * BK, 0);
+          }
+        }
+      }
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         const int nb = tile % p.num_n_blocks;
         const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
@@ -435,10 +453,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int cc = kb - r * p.cv_chunks;
             ptx::tma_load_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
             const int brow = ck_aug ? nb * p.b_rows_blk : n0;
+            if (!p.b_resident) {
 #pragma unroll 1
-            for (int si = 0; si < p.cv_S; ++si)
-              ptx::tma_load_2d(sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, &full[s],
-                               (r * p.cv_S + si) * p.cv_kstride + cc * BK, brow);
+              for (int si = 0; si < p.cv_S; ++si)
+                ptx::tma_load_2d(sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, &full[s],
+                                 (r * p.cv_S + si) * p.cv_kstride + cc * BK, brow);
+            }
             if (++s == p.stages) { s = 0; ph ^= 1; }
             continue;
           } else if (p.a_mode == 0) {
@@ -462,7 +482,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::tma_load_im2col_4d(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
             }
           }
-          ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
+          if (!p.b_resident)
+            ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
           if (ck_loaded) ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.nck_pad);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
@@ -485,6 +506,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int db = 0;
       uint32_t dph = 0;
       int t_local = 0;
+      if (p.b_resident && blockIdx.x < p.num_tiles) ptx::mbar_wait(bres, 0);
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
         const bool count_tile = (tile % p.num_n_blocks) == 0;
         const int acc = t_local % p.acc_stages;
@@ -497,7 +519,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
-          const uint32_t b_addr = ptx::smem_u32(sm_b + s * p.stage_b_bytes);
+          const uint32_t b_addr = ptx::smem_u32(sm_b + (p.b_resident ? kb : s) * p.stage_b_bytes);
           const uint32_t c_addr = ptx::smem_u32(sm_ck + s * p.stage_ck_bytes);
           if (p.a_mode == 4) {
             // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile
@@ -1393,15 +1415,20 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const uint32_t bar_bytes = 1024;
   const uint32_t extras =
       cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + out_bytes + acolck_bytes + ones_bytes + bar_bytes;
-  const uint32_t stage_bytes = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes;
   int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
   if (const char* cap = getenv("ABFT_SMEM_CAP")) budget = std::min(budget, atoi(cap) * 1024 - (int)extras);
-  int stages = budget / (int)stage_bytes;
+  // weight-stationary B (halo convs, whose stages carry S weight tiles each): one N-block, several M
+  // tiles per CTA, B for all k-blocks fits beside >= 4 A stages
+  const long long b_all = (long long)p.nkb * p.stage_b_bytes;
+  p.b_resident = (halo && p.num_n_blocks == 1 && p.num_tiles > 1 && p.ck_mode != 1 && p.ck_mode != 2 && !has_shadow &&
+                  b_all + 4LL * p.stage_a_bytes <= budget && !(dbg_env & 262144)) ? 1 : 0;
+  const uint32_t stage_bytes = p.stage_a_bytes + (p.b_resident ? 0u : p.stage_b_bytes) + p.stage_ck_bytes;
+  int stages = (budget - (p.b_resident ? (int)b_all : 0)) / (int)stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(ABFT_E_UNSUPPORTED, "shared memory budget too small for a 2-stage pipeline");
   p.stages = stages;
   p.off_b = stages * p.stage_a_bytes;
-  p.off_ck = p.off_b + stages * p.stage_b_bytes;
+  p.off_ck = p.off_b + (p.b_resident ? (uint32_t)b_all : stages * p.stage_b_bytes);
   p.off_cks = p.off_ck + stages * p.stage_ck_bytes;
   p.off_rec = p.off_cks + cks_bytes;
   p.off_stage = p.off_rec + rec_bytes;
