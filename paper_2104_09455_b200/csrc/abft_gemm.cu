@@ -319,7 +319,7 @@ template <typename T, int CLASS, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
-                     const __grid_constant__ GemmParams p) {
+                     const __grid_constant__ CUtensorMap tmC16, const __grid_constant__ GemmParams p) {
   using TR = ElemTraits<T>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -966,9 +966,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (!(p.debug & (131072 | 262144))) {
               ptx::fence_proxy_async_smem();
               __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0,
-                                  m0 + q * 32);
+              // rows of this lane quadrant inside the tile: 32, 16 (a tile of bm_eff = 16 mod 32 rows) or 0
+              const int qrows = min(32, max(0, p.bm_eff - q * 32));
+              if (lane == 0 && qrows > 0) {
+                const void* src = my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048);
+                if (qrows == 32) ptx::tma_store_2d(&tmC, src, gc0, m0 + q * 32);
+                else ptx::tma_store_2d(&tmC16, src, gc0, m0 + q * 32);
                 ptx::bulk_commit();
               }
             }
@@ -1162,7 +1165,7 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
 
 template <typename T, int CLASS, int NT>
 int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo,
-                const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+                const CUtensorMap& mo16, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -1181,30 +1184,31 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT>, ma, mb, mc, mo, p),
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT>, ma, mb, mc, mo, mo16, p),
                       "abft_gemm_kernel launch (PDL)");
   }
-  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
+  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo16, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                 const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, mo, p, smem, grid, st);
+                 const CUtensorMap& mo, const CUtensorMap& mo16, const GemmParams& p, size_t smem, int grid,
+                 cudaStream_t st) {
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
   if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, mo, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, mo, p, smem, grid, st);
-    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, mo, mo16, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, mo, mo16, p, smem, grid, st);
+    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
   }
-  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, mo, p, smem, grid, st);
-  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, mo, p, smem, grid, st);
-  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, mo, p, smem, grid, st);
+  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, mo, mo16, p, smem, grid, st);
+  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, mo, mo16, p, smem, grid, st);
+  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
 }
 
 // output map for the bulk tensor stores: dims {N, M}, box {32 columns, 32 rows}; fp32 rows are
 // 128 B (SW128), 16-bit rows 64 B (SW64)
-int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a) {
+int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a, int box_rows = 32) {
   auto enc = get_encode_fn();
   if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
@@ -1213,7 +1217,7 @@ int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a) {
                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   cuuint64_t dims[2] = {(cuuint64_t)a->N, (cuuint64_t)a->M};
   cuuint64_t strides[1] = {(cuuint64_t)(a->ldc * esz)};
-  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, a->C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -1400,7 +1404,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // bulk tensor stores of the output: whole 128-row tiles, 128-byte row units (32 fp32 / 64
     // 16-bit columns) that tile bn_eff exactly, 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
-    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 32 == 0 &&
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff % 16 == 0 && p.bn_eff % 32 == 0 &&
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
                    !(dbg_env & 8192)) ? 1 : 0;
   }
@@ -1606,12 +1610,19 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   } else {
     mc = mb;   // unused
   }
-  CUtensorMap mo;
+  CUtensorMap mo, mo16;
   if (p.tma_store) {
     rc = make_out_map(&mo, a);
     if (rc != ABFT_OK) return rc;
+    if (p.bm_eff % 32) {
+      rc = make_out_map(&mo16, a, 16);
+      if (rc != ABFT_OK) return rc;
+    } else {
+      mo16 = mo;
+    }
   } else {
     mo = mb;   // unused
+    mo16 = mb;
   }
   cudaStream_t st = as_stream(stream);
   if (getenv("ABFT_TRACE"))
@@ -1623,8 +1634,8 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   if (p.debug & 64) pl.cls = CLASS_PLAIN;
   if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
   if (a->dtype == ABFT_BF16)
-    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
-  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
+    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, mo16, p, pl.smem, pl.grid, st);
+  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, mo16, p, pl.smem, pl.grid, st);
 }
 
 // ---------------------------------------------------------------- implicit-GEMM conv
