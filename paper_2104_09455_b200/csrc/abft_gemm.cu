@@ -1787,6 +1787,12 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
   if (rc != ABFT_OK) return rc;
   Plan pl;
   rc = make_plan(&ga, pl, &g);
+  if (rc != ABFT_OK && g.a_mode == 4) {
+    // the halo stages (S weight tiles each) do not fit this tile: per-tap im2col instead
+    // (same packed-weight layout: channels padded to 64)
+    g.a_mode = 1;
+    rc = make_plan(&ga, pl, &g);
+  }
   if (rc != ABFT_OK) return rc;
   GemmParams& p = pl.p;
   if (g.a_mode == 4) {
