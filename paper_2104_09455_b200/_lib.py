@@ -14,7 +14,7 @@ import threading
 from .errors import AbftGuardError, ExactOverflowError, ShapeMismatchError
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libabft_b200.so")
+LIB_PATH = os.environ.get("ABFT_B200_LIB") or os.path.join(LIB_DIR, "libabft_b200.so")
 
 # enums of abft_b200.h
 OK, E_SHAPE, E_VALUE, E_OVERFLOW, E_CUDA, E_UNSUPPORTED = range(6)

@@ -315,11 +315,11 @@ __device__ __forceinline__ void apply_faults(const abft_fault_t* faults, int nfa
   }
 }
 
-template <typename T, int CLASS, int NT>
+template <typename T, int CLASS, int NT, bool HALO>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
-                     const __grid_constant__ CUtensorMap tmC16, const __grid_constant__ GemmParams p) {
+                     const __grid_constant__ GemmParams p) {
   using TR = ElemTraits<T>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -354,6 +354,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
   const bool ck_loaded = (has_ck || p.gck) && p.ck_mode == 2 && !(p.debug & 8);
   const bool ck_aug = p.ck_mode == 3;
+  // halo-reuse conv (a_mode 4) and its weight-stationary B exist only in the HALO instances,
+  // keeping the GEMM instances' hot loops free of them
+  const bool halo = HALO && p.a_mode == 4;
+  const bool b_res = HALO && p.b_resident;
   const int bn = p.bn;
   const bool stamp = (p.debug & 2048) && blockIdx.x < 160;
   if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][0] = gtimer();
@@ -411,14 +415,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = (p.a_mode == 4 ? p.tx_a : p.stage_a_bytes) + (p.b_resident ? 0u : p.stage_b_bytes) +
+      const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : p.stage_b_bytes) +
                           (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
-      if (p.b_resident && blockIdx.x < p.num_tiles) {
+      if (b_res && blockIdx.x < p.num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
         ptx::mbar_arrive_expect_tx(bres, (uint32_t)p.nkb * p.stage_b_bytes);
         for (int kb = 0; kb < p.nkb; ++kb) {
-          if (p.a_mode == 4) {
+          if (halo) {
             const int r = kb / p.cv_chunks, cc = kb - (kb / p.cv_chunks) * p.cv_chunks;
             for (int si = 0; si < p.cv_S; ++si)
               ptx::tma_load_2d(sm_b + kb * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, bres,
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&empty[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], tx);
           uint8_t* a_dst = sm_a + s * p.stage_a_bytes;
-          if (p.a_mode == 4) {
+          if (halo) {
             // window of input row (p + r - pad), columns q0 - pad .. q0 - pad + Qt + S - 2
             const int r = kb / p.cv_chunks;
             const int cc = kb - r * p.cv_chunks;
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else   // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
               ptx::tma_load_im2col_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
             const int brow = ck_aug ? nb * p.b_rows_blk : n0;
-            if (!p.b_resident) {
+            if (!b_res) {
 #pragma unroll 1
               for (int si = 0; si < p.cv_S; ++si)
                 ptx::tma_load_2d(sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, &full[s],
@@ -485,8 +489,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::tma_load_im2col_4d(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
             }
           }
-          if (!p.b_resident)
-            ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
+          ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
           if (ck_loaded) ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.nck_pad);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
@@ -509,7 +512,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int db = 0;
       uint32_t dph = 0;
       int t_local = 0;
-      if (p.b_resident && blockIdx.x < p.num_tiles) ptx::mbar_wait(bres, 0);
+      if (b_res && blockIdx.x < p.num_tiles) ptx::mbar_wait(bres, 0);
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
         const bool count_tile = (tile % p.num_n_blocks) == 0;
         const int acc = t_local % p.acc_stages;
@@ -522,9 +525,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
-          const uint32_t b_addr = ptx::smem_u32(sm_b + (p.b_resident ? kb : s) * p.stage_b_bytes);
+          const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * p.stage_b_bytes);
           const uint32_t c_addr = ptx::smem_u32(sm_ck + s * p.stage_ck_bytes);
-          if (p.a_mode == 4) {
+          if (halo) {
             // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile
 #pragma unroll 1
             for (int si = 0; si < p.cv_S; ++si) {
@@ -809,10 +812,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
 
-      // global lhs: this row's A . rowck(B tile) = checksum column hi + lo, loaded with the
-      // first chunk (one TMEM round trip)
-      const bool lhs_here = p.gck && h == 0 && !(p.debug & 524288);
-      float ck_hi = 0.f, ck_lo = 0.f;
+      if (p.gck && h == 0 && !(p.debug & 524288)) {
+        // global lhs: this row's A . rowck(B tile) = checksum column hi + lo
+        float ck_hi, ck_lo;
+        __syncwarp();
+        ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
+        ptx::tmem_ld_wait();
+        if (row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
+      }
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
       const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
       uint32_t fmask = 0;
@@ -827,7 +834,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float v[32], sh[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
-        if (lhs_here && c0 == c_first) ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
         if constexpr (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
         // static group width: this chunk's checksum columns straight from TMEM (hi, then lo)
         constexpr int GPCK = NT > 0 ? 32 / NT : 1;
@@ -837,7 +843,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (p.split) ptx::tmem_ldn<GPCK>(tacc + bn + p.groups + c0 / NT, ckl);
         }
         ptx::tmem_ld_wait();
-        if (lhs_here && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
         if (stamp && et == 0 && t_local == 0 && c0 == 0) g_dbg_ts[blockIdx.x][5] = gtimer();
         const int gc0 = n0 + c0;
         const int cmax = p.bn_eff - c0;
@@ -968,12 +973,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (!(p.debug & (131072 | 262144))) {
               ptx::fence_proxy_async_smem();
               __syncwarp();
-              // rows of this lane quadrant inside the tile: 32, 16 (a tile of bm_eff = 16 mod 32 rows) or 0
-              const int qrows = min(32, max(0, p.bm_eff - q * 32));
-              if (lane == 0 && qrows > 0) {
-                const void* src = my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048);
-                if (qrows == 32) ptx::tma_store_2d(&tmC, src, gc0, m0 + q * 32);
-                else ptx::tma_store_2d(&tmC16, src, gc0, m0 + q * 32);
+              if (lane == 0) {
+                ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0,
+                                  m0 + q * 32);
                 ptx::bulk_commit();
               }
             }
@@ -1067,24 +1069,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.gck) atomicAdd(p.out_lhs, ty);
       }
     }
-    if (p.vn > 0 && et == 0) {
-      // fused deferred verification: the launch's last CTA to finish (done-count) forms every
-      // layer's verdict from the accumulated (lhs, rhs) pairs (checksum.py:151-153, :237)
-      __threadfence();                                   // this CTA's (rhs, lhs) atomics first
-      if (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) {
-        __threadfence();
-        for (int i = 0; i < p.vn; ++i) {
-          const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
-          const double tol = tolerance(p.r, p.vk[i], lhs, rhs);
-          abft_verdict_t v;
-          v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = p.vk[i];
-          v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
-          if (p.vout) p.vout[i] = v;
-          if (v.detected && p.vdetected) atomicAdd(p.vdetected, 1);
-        }
-        *p.vdone = 0;                                    // ready for the next launch / replay
-      }
-    }
     // the staging buffers must stay valid until the bulk stores have READ them; the writes
     // themselves complete before the grid does
     if (p.tma_store && lane == 0) ptx::bulk_wait_read<0>();
@@ -1102,6 +1086,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   __syncwarp();
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+  if (p.vn > 0 && threadIdx.x == EPI_WARP0 * 32) {
+    // fused deferred verification: the launch's last CTA to finish (done-count) forms every
+    // layer's verdict from the accumulated (lhs, rhs) pairs (checksum.py:151-153, :237); this is
+    // the thread that added the CTA's (rhs, lhs)
+    __threadfence();
+    if (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      for (int i = 0; i < p.vn; ++i) {
+        const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
+        const double tol = tolerance(p.r, p.vk[i], lhs, rhs);
+        abft_verdict_t v;
+        v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = p.vk[i];
+        v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
+        if (p.vout) p.vout[i] = v;
+        if (v.detected && p.vdetected) atomicAdd(p.vdetected, 1);
+      }
+      *p.vdone = 0;                                  // ready for the next launch / replay
+    }
+  }
   if (stamp && threadIdx.x == 32) g_dbg_ts[blockIdx.x][4] = gtimer();
 }
 
@@ -1163,13 +1166,13 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
   return ABFT_OK;
 }
 
-template <typename T, int CLASS, int NT>
+template <typename T, int CLASS, int NT, bool HALO>
 int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo,
-                const CUtensorMap& mo16, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+                const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
@@ -1184,26 +1187,35 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT>, ma, mb, mc, mo, mo16, p),
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, HALO>, ma, mb, mc, mo, p),
                       "abft_gemm_kernel launch (PDL)");
   }
-  abft_gemm_kernel<T, CLASS, NT><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo16, p);
+  abft_gemm_kernel<T, CLASS, NT, HALO><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
+}
+
+template <typename T, bool HALO>
+int launch_cls(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+               const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+  if (cls == CLASS_CHECKSUM) {
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+    return launch_inst<T, CLASS_CHECKSUM, 0, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+  }
+  if constexpr (!HALO) {
+    if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, false>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, false>(ma, mb, mc, mo, p, smem, grid, st);
+    return launch_inst<T, CLASS_REPLICA, 0, false>(ma, mb, mc, mo, p, smem, grid, st);
+  }
+  return fail(ABFT_E_UNSUPPORTED, "replication schemes have no halo conv path");
 }
 
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                 const CUtensorMap& mo, const CUtensorMap& mo16, const GemmParams& p, size_t smem, int grid,
-                 cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-  if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-    return launch_inst<T, CLASS_CHECKSUM, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-  }
-  if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-  if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16>(ma, mb, mc, mo, mo16, p, smem, grid, st);
-  return launch_inst<T, CLASS_REPLICA, 0>(ma, mb, mc, mo, mo16, p, smem, grid, st);
+                 const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (p.a_mode == 4) return launch_cls<T, true>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
+  return launch_cls<T, false>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
 }
 
 // output map for the bulk tensor stores: dims {N, M}, box {32 columns, 32 rows}; fp32 rows are
@@ -1405,7 +1417,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // bulk tensor stores of the output: whole 128-row tiles, 128-byte row units (32 fp32 / 64
     // 16-bit columns) that tile bn_eff exactly, 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
-    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff % 16 == 0 && p.bn_eff % 32 == 0 &&
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 32 == 0 &&
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
                    !(dbg_env & 8192)) ? 1 : 0;
   }
@@ -1611,19 +1623,12 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   } else {
     mc = mb;   // unused
   }
-  CUtensorMap mo, mo16;
+  CUtensorMap mo;
   if (p.tma_store) {
     rc = make_out_map(&mo, a);
     if (rc != ABFT_OK) return rc;
-    if (p.bm_eff % 32) {
-      rc = make_out_map(&mo16, a, 16);
-      if (rc != ABFT_OK) return rc;
-    } else {
-      mo16 = mo;
-    }
   } else {
     mo = mb;   // unused
-    mo16 = mb;
   }
   cudaStream_t st = as_stream(stream);
   if (getenv("ABFT_TRACE"))
@@ -1635,8 +1640,8 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   if (p.debug & 64) pl.cls = CLASS_PLAIN;
   if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
   if (a->dtype == ABFT_BF16)
-    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, mo16, p, pl.smem, pl.grid, st);
-  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, mo16, p, pl.smem, pl.grid, st);
+    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
+  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
 }
 
 // ---------------------------------------------------------------- implicit-GEMM conv
