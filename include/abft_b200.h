@@ -118,8 +118,9 @@ int abft_gemm(const abft_gemm_args_t* args, void* stream);
 /* The kernel configuration abft_gemm would use for `args` (no launch):
  * out[0] tile_n, [1] bn_eff, [2] checksum groups per tile, [3] nck_pad, [4] pipeline stages,
  * [5] 1 if offline checksum rows are recommended (B tiles re-read by > 2 M-blocks),
- * [6] number of N blocks, [7] persistent grid size. */
-int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[8]*/);
+ * [6] number of N blocks, [7] persistent grid size, [8] rows per N-block of augmented weights
+ * (tile_n + real checksum rows), [9] reserved. */
+int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[10]*/);
 
 /* Offline checksum rows for a plan: out [(n_blocks*nck_pad) x ldo] (n_blocks = plan out[6], rows of
  * blocks past N are zero), row nb*nck_pad + j holds
@@ -128,9 +129,10 @@ int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[8]*/);
 int abft_ck_rows(const void* Bt, int32_t N, int32_t K, int64_t ldbt, int32_t dtype, int32_t bn_eff, int32_t nt,
                  int32_t split, int32_t nck_pad, int32_t n_blocks, void* out, int64_t ldo, void* stream);
 
-/* Augmented weights for a plan (ck_layout 1): out [(n_blocks*(tile_n + nck_pad)) x ldo] (tile_n =
- * plan out[0]); block nb holds Bt rows nb*bn_eff .. +bn_eff (zero past N and past bn_eff), then
- * the nck_pad checksum rows of abft_ck_rows for that block. */
+/* Augmented weights for a plan (ck_layout 1): out [(n_blocks * rows) x ldo], rows = plan out[8]
+ * = tile_n + G*(split ? 2 : 1) with G = bn_eff / nt; block nb holds Bt rows nb*bn_eff .. +bn_eff
+ * (zero past N and past bn_eff), then that block's G hi (and G lo) checksum rows.  The MMA
+ * reads nck_pad checksum rows; the padding rows are never stored and their products are ignored. */
 int abft_aug_weights(const void* Bt, int32_t N, int32_t K, int64_t ldbt, int32_t dtype, int32_t tile_n, int32_t bn_eff,
                      int32_t nt, int32_t split, int32_t nck_pad, int32_t n_blocks, void* out, int64_t ldo, void* stream);
 

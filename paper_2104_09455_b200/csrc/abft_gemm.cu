@@ -64,7 +64,9 @@ struct GemmParams {
   int scheme, out_dtype, relu, split;
   int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline),
                          // 3 appended to the weight tiles (augmented B: one box, one MMA per k-step)
-  int b_rows_blk;        // rows per N-block in the B tensor map (bn, or bn + nck_pad when augmented)
+  int b_rows_blk;        // rows per N-block in the B tensor (bn, or bn + nck real checksum rows when augmented:
+                         // the MMA reads bn + nck_pad rows, the padding rows' products land in ignored columns)
+  uint32_t tx_b;         // bytes one B box delivers (b_rows_blk x 128)
   int b_resident;        // 1: single N-block whose whole B (all k-blocks) stays in smem (weight-stationary)
   uint32_t idesc_aug;    // N = bn + nck_pad (augmented B)
   int shuffle_verdicts;  // 1: Mt divides 32 -> verdicts by warp shuffles/ballots, 0: smem records
@@ -415,12 +417,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : p.stage_b_bytes) +
+      const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b) +
                           (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
       if (b_res && blockIdx.x < p.num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
-        ptx::mbar_arrive_expect_tx(bres, (uint32_t)p.nkb * p.stage_b_bytes);
+        ptx::mbar_arrive_expect_tx(bres, (uint32_t)p.nkb * (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b);
         for (int kb = 0; kb < p.nkb; ++kb) {
           if (halo) {
             const int r = kb / p.cv_chunks, cc = kb - (kb / p.cv_chunks) * p.cv_chunks;
@@ -1360,7 +1362,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     if (bn + p.nck_pad > 256) return fail(ABFT_E_UNSUPPORTED, "augmented weights need tile_n + checksum rows <= 256");
     p.ck_mode = 3;
   }
-  p.b_rows_blk = p.ck_mode == 3 ? bn + p.nck_pad : bn;
+  p.b_rows_blk = p.ck_mode == 3 ? bn + p.nck : bn;
+  p.tx_b = (uint32_t)p.b_rows_blk * BK * 2;
   if (halo && (p.ck_mode == 1 || p.ck_mode == 2 || want_acolck))
     return fail(ABFT_E_UNSUPPORTED, "halo conv mode needs augmented checksum weights");
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
@@ -1399,7 +1402,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
 
   // ---- shared memory carve-up (all tile buffers 1024-aligned)
   p.stage_a_bytes = BM * BK * 2;
-  p.stage_b_bytes = (uint32_t)round_up(p.b_rows_blk * BK * 2, 1024);
+  p.stage_b_bytes = (uint32_t)round_up((p.ck_mode == 3 ? bn + p.nck_pad : bn) * BK * 2, 1024);
   p.b_tile_bytes = p.stage_b_bytes;
   if (halo) {
     // one input-row window [Qt + S - 1 pixels x 64 channels] and the S taps' B tiles per stage
@@ -1493,7 +1496,7 @@ template <typename T>
 __global__ void aug_weights_kernel(const T* __restrict__ bt, int n, int k, long long ldbt, int tile_n, int bn_eff,
                                    int nt, int groups, int split, int nck_pad, int n_blocks, T* __restrict__ out,
                                    long long ldo) {
-  const int blk = tile_n + nck_pad;
+  const int blk = tile_n + groups * (split ? 2 : 1);     // only the real checksum rows are stored
   const long long total = (long long)n_blocks * blk * ldo;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const int row = (int)(i / ldo), kk = (int)(i % ldo);
@@ -1537,7 +1540,7 @@ extern "C" __attribute__((visibility("default"))) int abft_aug_weights(const voi
   const int groups = bn_eff / nt;
   if (groups * (split ? 2 : 1) > nck_pad) return fail(ABFT_E_SHAPE, "aug_weights: nck_pad too small");
   if (n_blocks < ceil_div(N, bn_eff)) return fail(ABFT_E_SHAPE, "aug_weights: n_blocks does not cover N");
-  const long long total = (long long)n_blocks * (tile_n + nck_pad) * ldo;
+  const long long total = (long long)n_blocks * (tile_n + groups * (split ? 2 : 1)) * ldo;
   int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * num_sms());
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
@@ -1559,6 +1562,8 @@ extern "C" __attribute__((visibility("default"))) int abft_gemm_plan(const abft_
   if (rc != ABFT_OK) return rc;
   out[0] = pl.p.bn; out[1] = pl.p.bn_eff; out[2] = pl.p.groups; out[3] = pl.p.nck_pad; out[4] = pl.p.stages;
   out[5] = pl.ck_offline_recommended; out[6] = pl.p.num_n_blocks; out[7] = pl.grid;
+  out[8] = pl.p.bn + pl.p.nck;                  // rows per N-block of augmented weights
+  out[9] = pl.p.stages;
   return ABFT_OK;
 }
 

@@ -73,10 +73,10 @@ def gemm(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType, numer
     Keyword arguments are the fields of abft_gemm_args_t (see _gemm_args)."""
     args = _gemm_args(a, lda, bt, ldbt, m, n, k, dtype, numeric, scheme, **kw)
     if plan_only:
-        out = (ctypes.c_int32 * 8)()
+        out = (ctypes.c_int32 * 10)()
         _lib.check(_lib.load().abft_gemm_plan(ctypes.byref(args), out))
         return dict(tile_n=out[0], bn_eff=out[1], groups=out[2], nck_pad=out[3], stages=out[4],
-                    ck_offline_recommended=bool(out[5]), n_blocks=out[6], grid=out[7])
+                    ck_offline_recommended=bool(out[5]), n_blocks=out[6], grid=out[7], aug_rows=out[8])
     _lib.check(_lib.load().abft_gemm(ctypes.byref(args), stream_handle()))
     return None
 
@@ -142,7 +142,8 @@ def aug_weights(bt, n: int, k: int, dtype: DType, plan: dict, thread_n: int, spl
     """Augmented weights of a plan (ck_layout 1): each CTA N-tile's weight rows followed by its
     checksum rows, so the tile's outputs and checksums come from one MMA instruction."""
     t = torch()
-    blk = plan["tile_n"] + plan["nck_pad"]
+    groups = plan["bn_eff"] // thread_n
+    blk = plan["tile_n"] + groups * (2 if split else 1)
     out = t.empty((plan["n_blocks"] * blk, bt.shape[1]), dtype=bt.dtype, device="cuda")
     _lib.call("abft_aug_weights", ptr(bt), n, k, bt.stride(0), storage_code(dtype), plan["tile_n"], plan["bn_eff"],
               thread_n, int(split), plan["nck_pad"], plan["n_blocks"], ptr(out), out.stride(0), stream_handle())
