@@ -111,6 +111,13 @@ typedef struct {
    * instruction (N = tile + checksum columns) per k-step produce outputs and checksums.
    * With layout 1, ck_rows replaces Bt as the B operand (Bt is still used for shapes). */
   int32_t ck_layout;
+  /* optional [ceil(K/64)*64] fp32 (zero past K, 16-byte aligned), global scheme with out_lhs:
+   * the row checksum of B (sum over N of Bt[n][k], in Bt's K layout; checksum.py:99-105).  The lhs is then accumulated as
+   * sum over rows of A . lhs_rowck by the checksum warps, from the shared-memory A tiles the
+   * MMA consumes (each A tile once, in its first N block): no checksum rows in the MMA, so the
+   * CTA tile stays as wide as the unprotected one.  ck_rows is not used; excludes a_colck.
+   * Works in every A-load mode, the halo conv included. */
+  const float* lhs_rowck;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
@@ -119,7 +126,8 @@ int abft_gemm(const abft_gemm_args_t* args, void* stream);
  * out[0] tile_n, [1] bn_eff, [2] checksum groups per tile, [3] nck_pad, [4] pipeline stages,
  * [5] 1 if offline checksum rows are recommended (B tiles re-read by > 2 M-blocks),
  * [6] number of N blocks, [7] persistent grid size, [8] rows per N-block of augmented weights
- * (tile_n + real checksum rows), [9] reserved. */
+ * (tile_n + real checksum rows), [9] reserved.  Augmented weights with tile_n = 256 keep their
+ * layout; the kernel then reads the checksum rows by a second box into their own MMA N-slice. */
 int abft_gemm_plan(const abft_gemm_args_t* args, int32_t* out /*[10]*/);
 
 /* Offline checksum rows for a plan: out [(n_blocks*nck_pad) x ldo] (n_blocks = plan out[6], rows of
@@ -218,6 +226,10 @@ int abft_conv2d(const abft_conv_args_t* args, void* stream);
  *   out[4] K of the GEMM (r*s*ck, or round8(r*s*c_real) in mode 3), out[5] M = n*P*Q,
  *   out[6] workspace bytes (mode 3) */
 int abft_conv_plan(const abft_conv_args_t* args, int32_t* out /*[8]*/);
+/* The kernel plan abft_conv2d would use for `args` (no launch), laid out as abft_gemm_plan's
+ * out[0..8]; out[9] = the A-load mode actually used.  Augmented weights / checksum rows for a
+ * conv call are prepared from THIS plan (the conv's A-load mode enters the tile choice). */
+int abft_conv_gemm_plan(const abft_conv_args_t* args, int32_t* out /*[10]*/);
 /* torch-layout weight [OC][cin][r][s] -> K-major [OC][ldo] with element (r, s, c) at
  * (r*s_ + s)*ck + c, channels >= cin and columns >= r*s*ck zero (ldo >= r*s*ck) */
 int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin, int32_t r, int32_t s, int32_t ck, void* out,
@@ -234,6 +246,8 @@ int abft_zero(void* p, int64_t bytes, void* stream);
 /* Library introspection */
 const char* abft_last_error(void);
 int abft_version(void);                 /* 10000*major + 100*minor + patch */
+int abft_struct_size(int32_t which);    /* sizeof: 0 gemm args, 1 conv args, 2 global task, 3 verdict,
+                                          4 thread verdict, 5 fault (ABI check for FFI mirrors) */
 int abft_device_sms(void);              /* SM count of the current device (0 if none) */
 
 #ifdef __cplusplus

@@ -24,6 +24,7 @@ NUM_EXACT, NUM_BINARY16, NUM_BINARY32, NUM_BF16 = 0, 1, 2, 3
 UNPROTECTED, GLOBAL, ONE_SIDED, TWO_SIDED, REPL_FULL, REPL_SINGLE = range(6)
 
 EXPORTED_SYMBOLS = (
+    "abft_struct_size",
     "abft_gemm",
     "abft_gemm_plan",
     "abft_ck_rows",
@@ -35,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "abft_zero",
     "abft_conv2d",
     "abft_conv_plan",
+    "abft_conv_gemm_plan",
     "abft_conv_pack_weight",
     "abft_conv_colck",
     "abft_global_lhs",
@@ -94,6 +96,7 @@ class GemmArgs(ctypes.Structure):
         ("vsums", ctypes.c_void_p), ("vk", ctypes.c_void_p), ("vn", ctypes.c_int32), ("vdone", ctypes.c_void_p),
         ("vout", ctypes.c_void_p), ("vdetected", ctypes.c_void_p),
         ("pdl", ctypes.c_int32), ("ck_layout", ctypes.c_int32),
+        ("lhs_rowck", ctypes.c_void_p),
     ]
 
 
@@ -130,6 +133,7 @@ def _declare(lib):
     lib.abft_verify_sums.argtypes = [vp, vp, i32, i32, vp, vp, vp]
     lib.abft_conv2d.argtypes = [ctypes.POINTER(ConvArgs), vp]
     lib.abft_conv_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]
+    lib.abft_conv_gemm_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]
     lib.abft_conv_pack_weight.argtypes = [vp, i32, i32, i32, i32, i32, vp, i64, vp]
     lib.abft_conv_colck.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, i32, vp]
     lib.abft_last_error.restype = ctypes.c_char_p

@@ -75,7 +75,7 @@ def prepare_conv_weight(weight, dtype: DType, ck: int, k_pitch: int) -> Prepared
     else:
         w = t.from_numpy(np.ascontiguousarray(np.asarray(weight).astype(np.float32))).to("cuda").to(sd)
     bt = kernels.conv_pack_weight(w, ck, k_pitch)
-    rowck = t.empty(bt.shape[1], dtype=t.float32, device="cuda")
+    rowck = t.zeros(-(-bt.shape[1] // 64) * 64, dtype=t.float32, device="cuda")     # k-block padded
     kernels.colsum(bt, oc, bt.shape[1], bt.stride(0), dtype, rowck)
     return PreparedConv(bt=bt, rowck=rowck, oc=oc, cin=cin, ck=ck, r=r, s=s, dtype=dtype)
 
@@ -119,13 +119,15 @@ def standalone_colck(x_dev, geom: dict, pl: dict, dtype: DType, out) -> None:
 
 def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig(),
            scheme: Scheme = Scheme.UNPROTECTED, faults: Sequence[FaultSpec] = (), dtype: DType | None = None,
-           colck_source: str = "fused"):
+           colck_source: str = "fused", tile_n: int = 0):
     """Protected NHWC convolution; returns the reference's ExecutionReport for the lowered GEMM.
 
     ``report.output`` is [n, P, Q, OC] fp32 (int64 in exact-int mode); ``report.shape`` is
     the reference lowering GemmShape(n*P*Q, OC, C*R*S).  Global scheme: lhs comes from the
-    conv kernel's checksum N-slice, sum over rows of A . rowck(B tile) ("fused"), or from
-    colck(A) . rowck(B) with the windowed checksum of a standalone pass ("standalone")."""
+    conv kernel's checksum N-slice, sum over rows of A . rowck(B tile) ("slice"), from the
+    checksum warps' dot of the staged A tiles with rowck(B) ("dot"; the default "fused" is
+    "slice"), or from colck(A) . rowck(B) with the windowed checksum of a standalone pass
+    ("standalone")."""
     from .checksum import Verdict
     from .tiled import _TV_DTYPE, ExecutionReport, _counts, _thread_verdicts
 
@@ -157,24 +159,29 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     if thread_level:
         ntr, ntc = padded.m // tiling.thread_m, padded.n // tiling.thread_n
         verdicts = t.empty(ntr * ntc * _TV_DTYPE.itemsize, dtype=t.uint8, device="cuda")
-    if colck_source not in ("fused", "standalone"):
-        raise ValueError(f"colck_source must be 'fused' or 'standalone', got {colck_source!r}")
+    if colck_source not in ("fused", "slice", "dot", "standalone"):
+        raise ValueError(f"colck_source must be 'fused', 'slice', 'dot' or 'standalone', got {colck_source!r}")
     glob = scheme is Scheme.GLOBAL_ABFT
     sums = t.zeros(2, dtype=t.float64, device="cuda") if glob else None       # [lhs, rhs]
     kw = dict(out=out, ldc=pc.oc, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
               m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
-              out_sum=sums[1:2] if glob else None, verdicts=verdicts, ck_split=not dtype.is_exact)
+              out_sum=sums[1:2] if glob else None, verdicts=verdicts, ck_split=not dtype.is_exact, tile_n=tile_n)
     colck = None
     if glob and colck_source == "fused":
+        colck_source = "slice"
+    if glob and colck_source == "dot":
+        # lhs = sum over rows of A . rowck(B) by the checksum warps from the staged A tiles
+        kw["out_lhs"], kw["lhs_rowck"] = sums[0:1], pc.rowck
+    if glob and colck_source == "slice":
         # lhs from the kernel's checksum slice: sum over rows of A . rowck(B tile)
         kw["out_lhs"] = sums[0:1]
-        gplan = kernels.gemm(x_dev, 8, pc.bt, pc.bt.stride(0), m, pc.oc, pl["k"], dtype, numeric, scheme,
-                             plan_only=True, ck_layout=1, **kw)
+        gplan = kernels.conv_gemm_plan(kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme,
+                                                         workspace=ws, ck_layout=1, **kw))
         kw["ck_rows"] = kernels.global_ck_rows(pc.bt, pc.oc, pl["k"], dtype, gplan)
     if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED):
         # weights with each tile's checksum rows appended (one MMA per k-step)
-        oplan = kernels.gemm(x_dev, 8, pc.bt, pc.bt.stride(0), m, pc.oc, pl["k"], dtype, numeric, scheme,
-                             plan_only=True, ck_layout=1, **kw)
+        oplan = kernels.conv_gemm_plan(kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme,
+                                                         workspace=ws, ck_layout=1, **kw))
         kw["ck_rows"] = kernels.aug_weights(pc.bt, pc.oc, pl["k"], dtype, oplan, tiling.thread_n,
                                             not dtype.is_exact)
     kernels.conv2d(kernels.conv_args(x_dev, geom, pc.bt, pc.oc, dtype, numeric, scheme, workspace=ws, **kw))

@@ -11,8 +11,10 @@ unprotected / global / one-sided ABFT:
                     lhs colck(A) . rowck(B) regrouped as sum_rows A . rowck(B tile): one
                     extra MMA N-slice against the weight tile's row sums, summed in the
                     epilogue (the input comes out of pooling / residual / BN glue, so a
-                    producer-fused activation checksum is not available; SURVEY H3);
-                    alternatively the windowed activation checksum by a standalone pass
+                    producer-fused activation checksum is not available); or the
+                    lhs as the checksum warps' dot of the staged A tiles with rowck(B)
+                    (the tile stays as wide as the unprotected one); or the windowed
+                    activation checksum by a standalone pass
                     + its share of the network's single batched verification
   thread-one-sided  checksum N-slice in the same MMA, per-row compares in the epilogue
 
@@ -70,22 +72,26 @@ class LayerRunner:
         self.offline_ck = offline_ck
         for s in (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED):
             self._args[s] = self._make_args(s)
-        # global scheme with the activation checksum from a separate pass instead of in-kernel
+        # global scheme with the activation checksum from a separate pass instead of in-kernel,
+        # and with the lhs as the checksum warps' dot of the staged A tiles with rowck(B)
         self._args["global-standalone"] = self._make_args(Scheme.GLOBAL_ABFT, fused_colck=False)
+        self._args["global-dot"] = self._make_args(Scheme.GLOBAL_ABFT, dot=True)
         self.global_variant = "fused"
 
-    def _make_args(self, scheme: Scheme, fused_colck: bool = True):
+    def _make_args(self, scheme: Scheme, fused_colck: bool = True, dot: bool = False):
         t = self.tiling
         kw = dict(out=self.out, ldc=self.n8, out_kind="bf16" if self.out.dtype == D.torch().bfloat16 else "f16",
                   relu=True)
         if scheme is Scheme.GLOBAL_ABFT:
             kw["out_sum"] = self.rhs
-            if fused_colck:
+            if dot:
+                kw["out_lhs"], kw["lhs_rowck"] = self.scratch[0:1], self.pc.rowck
+            elif fused_colck:
                 # lhs from the kernel's checksum N-slice against the weight tile's row sums
                 kw["out_lhs"] = self.scratch[0:1]
-                gplan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
-                                     self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True,
-                                     ck_layout=1, **kw)
+                gplan = kernels.conv_gemm_plan(kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc,
+                                                                 self.dtype, self.numeric, scheme, workspace=self.ws,
+                                                                 ck_layout=1, **kw))
                 kw["ck_rows"] = kernels.global_ck_rows(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype,
                                                        gplan)
         elif scheme is Scheme.THREAD_ONE_SIDED:
@@ -96,9 +102,9 @@ class LayerRunner:
                                  workspace=self.ws, **kw)
         if scheme is Scheme.THREAD_ONE_SIDED and self.offline_ck:
             # weights with each tile's checksum rows appended (one MMA per k-step)
-            plan = kernels.gemm(self.x, 8, self.pc.bt, self.pc.bt.stride(0), self.m, self.spec.oc,
-                                self.pc.bt.shape[1], self.dtype, self.numeric, scheme, plan_only=True, ck_layout=1,
-                                **kw)
+            plan = kernels.conv_gemm_plan(kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype,
+                                                            self.numeric, scheme, workspace=self.ws, ck_layout=1,
+                                                            **kw))
             self.ck_rows = kernels.aug_weights(self.pc.bt, self.spec.oc, self.pc.bt.shape[1], self.dtype, plan,
                                                t.thread_n, False)
             args = kernels.conv_args(self.x, self.geom, self.pc.bt, self.spec.oc, self.dtype, self.numeric,
@@ -109,7 +115,11 @@ class LayerRunner:
         return 2 * self.m * self.spec.oc * self.k_ref
 
     def conv(self, scheme) -> None:
-        kernels.conv2d(self._args[scheme])
+        kernels.conv2d(self._args["global-dot"] if scheme is Scheme.GLOBAL_ABFT and self.global_variant == "dot"
+                       else self._args[scheme])
+
+    def conv_variant(self, key) -> None:
+        kernels.conv2d(self._args[key])
 
     def global_standalone(self) -> None:
         """Global ABFT with the standalone checksum pass (the other measured variant)."""
@@ -122,7 +132,7 @@ class LayerRunner:
         standalone_colck(self.x, self.geom, self.plan, self.dtype, self.colck)
 
     def verify(self) -> None:
-        if self.global_variant == "fused":
+        if self.global_variant in ("fused", "dot"):
             kernels.verify_sums(self.lhs_rhs, self.ks, 1, self.numeric, out=self.verdict,
                                 detected_count=self.counters)
         else:
@@ -133,7 +143,7 @@ class LayerRunner:
         """One protected execution of the layer (verification included for global)."""
         if scheme is Scheme.GLOBAL_ABFT:
             kernels.zero(self.scratch)
-            if self.global_variant == "fused":
+            if self.global_variant in ("fused", "dot"):
                 self.conv(scheme)
             else:
                 self.global_standalone()

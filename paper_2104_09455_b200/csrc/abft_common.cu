@@ -49,6 +49,17 @@ int max_smem_optin() {
 
 extern "C" __attribute__((visibility("default"))) const char* abft_last_error(void) { return abft::g_last_error.c_str(); }
 extern "C" __attribute__((visibility("default"))) int abft_version(void) { return 100; }  // 0.1.0
+extern "C" __attribute__((visibility("default"))) int abft_struct_size(int which) {
+  switch (which) {
+    case 0: return (int)sizeof(abft_gemm_args_t);
+    case 1: return (int)sizeof(abft_conv_args_t);
+    case 2: return (int)sizeof(abft_global_task_t);
+    case 3: return (int)sizeof(abft_verdict_t);
+    case 4: return (int)sizeof(abft_thread_verdict_t);
+    case 5: return (int)sizeof(abft_fault_t);
+    default: return -1;
+  }
+}
 extern "C" __attribute__((visibility("default"))) int abft_device_sms(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;

@@ -63,7 +63,10 @@ struct GemmParams {
   int stages, acc_stages, cols_per_acc, shadow_off, tmem_cols;
   int scheme, out_dtype, relu, split;
   int ck_mode;           // 0 none, 1 generated on chip by the checksum warps, 2 TMA-loaded (prepared offline),
-                         // 3 appended to the weight tiles (augmented B: one box, one MMA per k-step)
+                         // 3 appended to the weight tiles (augmented B: one box, one MMA per k-step),
+                         // 4 augmented B with bn = 256 (bn + nck_pad > the MMA's N limit): the block's
+                         //   checksum rows by their own box + MMA N-slice, as in mode 2
+  int ck_rstride, ck_roff;   // row of N-block nb's checksum box = nb * ck_rstride + ck_roff
   int b_rows_blk;        // rows per N-block in the B tensor (bn, or bn + nck real checksum rows when augmented:
                          // the MMA reads bn + nck_pad rows, the padding rows' products land in ignored columns)
   uint32_t tx_b;         // bytes one B box delivers (b_rows_blk x 128)
@@ -76,6 +79,8 @@ struct GemmParams {
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
   double* out_lhs;       // global: += sum_rows A . rowck(B tile) (one checksum N-slice per tile)
+  const float* lhs_w;    // global: rowck(B) [ceil(K/64)*64]; lhs = sum_rows A . rowck(B) by the checksum warps
+  uint32_t off_w, stage_w_bytes;   // per stage: the k-block's rowck(B) slice(s) (S x 256 B in halo mode)
   const double* vsums;   // fused deferred verification (last CTA): [vn][2] (lhs, rhs), K per layer
   const int* vk;
   int vn;
@@ -90,6 +95,7 @@ struct GemmParams {
   uint32_t idesc_ones;
   int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
   int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
+  int out_single;        // 1: one 2 KB 16-bit staging buffer per epilogue warp (else two)
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
   void* C;
@@ -354,8 +360,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool has_shadow = CLASS == CLASS_REPLICA;
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
   const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
-  const bool ck_loaded = (has_ck || p.gck) && p.ck_mode == 2 && !(p.debug & 8);
-  const bool ck_aug = p.ck_mode == 3;
+  const bool ck_loaded = (has_ck || p.gck) && (p.ck_mode == 2 || p.ck_mode == 4) && !(p.debug & 8);
+  // augmented weights: B rows of N-block nb start at nb * b_rows_blk (idesc_aug = idesc_main in mode 4)
+  const bool ck_aug = p.ck_mode == 3 || p.ck_mode == 4;
   // halo-reuse conv (a_mode 4) and its weight-stationary B exist only in the HALO instances,
   // keeping the GEMM instances' hot loops free of them
   const bool halo = HALO && p.a_mode == 4;
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < p.stages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
-      ptx::mbar_init(&empty[s], p.acolck_mode == 2 ? 5 : 1);   // + one arrival per CUDA-core A-checksum warp
+      ptx::mbar_init(&empty[s], (p.acolck_mode == 2 || p.lhs_w != nullptr) ? 5 : 1);   // + one per CUDA-core A-checksum warp
     }
     ptx::mbar_init(bres, 1);
     for (int a = 0; a < DCK_BUFS; ++a) {
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b) +
-                          (ck_loaded ? (uint32_t)p.nck_pad * 128u : 0u);
+                          (ck_loaded ? (halo ? (uint32_t)p.cv_S : 1u) * (uint32_t)p.nck_pad * 128u : 0u);
       if (b_res && blockIdx.x < p.num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
@@ -438,6 +445,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nb = tile % p.num_n_blocks;
         const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
         const int n0 = nb * p.bn_eff;
+        // global lhs dot: the tile row's first N block also brings each k-block's rowck(B) slice
+        const bool w_tile = p.lhs_w != nullptr && nb == 0;
+        const uint32_t txt = tx + (w_tile ? p.stage_w_bytes : 0u);
         // conv: window origin of the tile's first output pixel (the TMA walks the next 127)
         int img = 0, wo = 0, ho = 0;
         if (p.a_mode != 0) {
@@ -451,8 +461,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], tx);
+          ptx::mbar_arrive_expect_tx(&full[s], txt);
           uint8_t* a_dst = sm_a + s * p.stage_a_bytes;
+          uint8_t* w_dst = smem + p.off_w + s * p.stage_w_bytes;
           if (halo) {
             // window of input row (p + r - pad), columns q0 - pad .. q0 - pad + Qt + S - 2
             const int r = kb / p.cv_chunks;
@@ -462,11 +473,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else   // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
               ptx::tma_load_im2col_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
             const int brow = ck_aug ? nb * p.b_rows_blk : n0;
-            if (!b_res) {
+            if (w_tile) {
 #pragma unroll 1
               for (int si = 0; si < p.cv_S; ++si)
-                ptx::tma_load_2d(sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, &full[s],
-                                 (r * p.cv_S + si) * p.cv_kstride + cc * BK, brow);
+                ptx::bulk_load(w_dst + si * 256, p.lhs_w + (r * p.cv_S + si) * p.cv_kstride + cc * BK, 256u, &full[s]);
+            }
+            if (!b_res) {
+#pragma unroll 1
+              for (int si = 0; si < p.cv_S; ++si) {
+                uint8_t* bdst = sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes;
+                const int kx = (r * p.cv_S + si) * p.cv_kstride + cc * BK;
+                ptx::tma_load_2d(bdst, &tmB, &full[s], kx, brow);
+                if (ck_loaded)
+                  ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes + si * p.nck_pad * 128, &tmCK, &full[s], kx,
+                                   nb * p.ck_rstride + p.ck_roff);
+              }
             }
             if (++s == p.stages) { s = 0; ph ^= 1; }
             continue;
@@ -492,7 +513,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
-          if (ck_loaded) ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.nck_pad);
+          if (w_tile) ptx::bulk_load(w_dst, p.lhs_w + kb * BK, 256u, &full[s]);
+          if (ck_loaded)
+            ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.ck_rstride + p.ck_roff);
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       }
@@ -538,8 +561,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t row_off = (p.debug & 2097152) ? 0u : (uint32_t)si * 128u;   // bring-up timing bit
                 const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + row_off + (uint32_t)k * 32u) |
                                        (p.debug & 1048576 ? ((uint64_t)(si & 7) << 49) : 0ull);
-                const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + (uint32_t)si * p.b_tile_bytes + k * 32);
-                ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, (kb | si | k) != 0 ? 1u : 0u);
+                const uint32_t bt_addr = b_addr + (uint32_t)si * p.b_tile_bytes;
+                const uint64_t bdesc = ptx::desc_kmajor_sw128(bt_addr + k * 32);
+                const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
+                ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
+                if (ck_loaded)
+                  ptx::mma_f16_ss(d + bn, adesc,
+                                  ptx::desc_kmajor_sw128(c_addr + (uint32_t)(si * p.nck_pad * 128) + k * 32),
+                                  p.idesc_ck, accum);
               }
             }
             ptx::mma_commit(&empty[s]);
@@ -691,6 +720,90 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128)
           if (acolck_s[i] != 0.f) atomicAdd(&p.a_colck[i], acolck_s[i]);
       }
+    } else if (p.lhs_w != nullptr) {
+      // --------------------------- global: lhs = sum over rows of A . rowck(B), CUDA cores
+      // colck(A) . rowck(B) (checksum.py:108-117) accumulated tile by tile: each A tile is read
+      // once from shared memory (in its tile row's first N block); thread (chunk c = 8 columns,
+      // row group g) sums its rows of the chunk and dots the 8 sums with rowck(B).  OOB rows,
+      // padding pixels and padded channels arrive as zeros from the TMA.
+      const int ct = threadIdx.x - CK_WARP0 * 32;
+      const int c = ct & 7, g = ct >> 3;
+      const bool a_none = p.a_mode == 2;
+      double part = 0.0;
+      int s = 0;
+      uint32_t ph = 0;
+      // rowck(B) slice staged with the k-block by the producer (zero past K); fp64 products:
+      // exact for the exact-integer mode's operands
+      auto dot8 = [&](const float (&acc)[8], const float* w) -> double {
+        const float4 w0 = *reinterpret_cast<const float4*>(w);
+        const float4 w1 = *reinterpret_cast<const float4*>(w + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        double d = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d += (double)acc[e] * (double)wv[e];
+        return d;
+      };
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const bool count = (tile % p.num_n_blocks) == 0;
+#pragma unroll 1
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          ptx::mbar_wait(&full[s], ph);
+          if (count) {
+            const uint8_t* at = sm_a + s * p.stage_a_bytes;
+            const float* wst = reinterpret_cast<const float*>(smem + p.off_w + s * p.stage_w_bytes);
+            if (halo) {
+              // im2col column (tap si, channel) = window rows si .. si + Qt - 1 of that channel
+              double tsum = 0.0;
+#pragma unroll 1
+              for (int si = 0; si < p.cv_S; ++si) {
+                float acc[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll 2
+                for (int j = si + g; j < si + p.bm_eff; j += 16) {
+                  const uint4 raw = *reinterpret_cast<const uint4*>(at + j * 128 + ((c ^ (j & 7)) << 4));
+                  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 f = TR::unpack2(w[e]);
+                    acc[2 * e] += f.x;
+                    acc[2 * e + 1] += f.y;
+                  }
+                }
+                tsum += dot8(acc, wst + si * 64 + c * 8);
+              }
+              part += tsum;
+            } else {
+              float acc[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int r = g + 16 * i;
+                const uint8_t* src = a_none ? at + c * 2048 + r * 16 : at + r * 128 + ((c ^ (r & 7)) << 4);
+                const uint4 raw = *reinterpret_cast<const uint4*>(src);
+                const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = TR::unpack2(w[e]);
+                  acc[2 * e] += f.x;
+                  acc[2 * e + 1] += f.y;
+                }
+              }
+              part += dot8(acc, wst + c * 8);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&empty[s]);
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0 && part != 0.0) {
+        atomicAdd(p.out_lhs, part);
+        __threadfence();
+      }
     } else if (p.a_colck != nullptr) {
       // ------------------------------------- global: activation column checksum
       // Each A tile is summed over its 128 rows once (in the tile's first N block): thread
@@ -768,7 +881,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     double rhs_acc = 0.0, lhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
     int sbuf = 0;
-    uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * 4096;
+    uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * (p.out_single ? 2048 : 4096);
     int t_local = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
@@ -918,8 +1031,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         if (p.out_sum != nullptr) {
+          // four independent partial chains instead of one 32-deep dependent FADD chain
+          float t4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
+          for (int j = 0; j < 32; ++j) t4[j & 3] += (j < cmax) ? v[j] : 0.f;
+          tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
         }
         if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
@@ -947,7 +1063,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
-              if (lane == 0) ptx::bulk_wait_read<1>();
+              if (lane == 0) {
+                if (p.out_single) ptx::bulk_wait_read<0>();
+                else ptx::bulk_wait_read<1>();
+              }
               __syncwarp();
               uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
               if (relu_in_pack) {
@@ -981,7 +1100,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::bulk_commit();
               }
             }
-            sbuf ^= 1;
+            sbuf ^= p.out_single ? 0 : 1;
           } else if (row_store && p.out_dtype != ABFT_OUT_NONE) {
             const bool full_chunk = (cmax >= 32) && (gc0 + 32 <= p.N);
             if (p.out_dtype == ABFT_OUT_F32) {
@@ -1288,7 +1407,12 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     if (m_ext < a->M || n_ext < a->N || m_ext % mt || n_ext % nt)
       return fail(ABFT_E_SHAPE, "m_ext/n_ext must cover M/N and be multiples of the thread tile");
   }
-  const bool gck = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && !as_plain;
+  // global lhs: 'gdot' = CUDA-core dot of the staged A tiles with rowck(B) (lhs_rowck), else
+  // 'gck' = a checksum N-slice in the MMA (checksum rows, separate or appended to the weights)
+  const bool gdot = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && a->lhs_rowck != nullptr && !as_plain;
+  const bool gck = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && !gdot && !as_plain;
+  if (gdot && a->a_colck != nullptr) return fail(ABFT_E_VALUE, "lhs_rowck and a_colck are alternatives");
+  if (gdot && (reinterpret_cast<uintptr_t>(a->lhs_rowck) & 15)) return fail(ABFT_E_VALUE, "lhs_rowck must be 16-byte aligned");
   const int split = (has_ck && a->ck_split) ? 1 : 0;
   // global scheme with the activation checksum: 2 x 64 TMEM columns for the column-sum MMA
   const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
@@ -1299,29 +1423,39 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   if (halo && bm_eff % mt) return fail(ABFT_E_UNSUPPORTED, "halo tile is not a multiple of the thread tile");
   const int m_blocks = ceil_div(m_ext, bm_eff);
 
+  const int nkb_plan = halo ? cg->R * cg->chunks : ceil_div(a->K, BK);
   int bn = a->tile_n;
   if (bn == 0) {
-    // Wave-quantised cost model over the legal tiles (TMEM double buffering required unless no
-    // tile allows it): waves x per-tile cost, a tile costing its operand bytes per k-block
-    // (128 A rows + bn B rows + checksum rows) and its epilogue (~bn); ties go to the wider tile.
-    // Thread-level schemes keep <= 32 checksum groups per tile.
+    // Wave-quantised cost model over the legal tiles: waves x per-tile cost, a tile costing its
+    // operand rows per k-block (128 A rows + bn B rows + checksum rows, B weighted twice: it also
+    // sets the MMA's N) times its k-blocks, plus ~2 k-blocks of exposed epilogue (8 for the
+    // heavier thread-level epilogues) per tile after a CTA's first when the accumulator cannot
+    // be double-buffered in TMEM.
+    // Augmented weights with bn = 256 put the checksum rows in their own MMA N-slice.
+    // Thread-level schemes keep <= 32 checksum groups per tile; ties go to the wider tile.
     int best = 0;
-    for (int pass = 0; pass < 2 && best == 0; ++pass) {
-      long long best_cost = 0;
-      for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
-        if (cand < nt || (thread_level && cand / nt > 32)) continue;
-        if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
-        const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
-        if (cols + extra_cols > 512) continue;
-        if (pass == 0 && 2 * cols + extra_cols > 512) continue;                      // pass 0: double-buffered only
-        const int eff = (cand / nt) * nt;
-        const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
-        const long long waves = (tiles + sms - 1) / sms;
-        const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
-        if (a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256) continue;
-        const long long cost = waves * (128 + 2LL * cand + nck);
-        if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
-      }
+    long long best_cost = 0;
+    for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
+      if (cand < nt || (thread_level && cand / nt > 32)) continue;
+      if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
+      const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
+      if (cols + extra_cols > 512) continue;
+      const bool dbuf = 2 * cols + extra_cols <= 512;
+      const int eff = (cand / nt) * nt;
+      const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
+      const long long waves = (tiles + sms - 1) / sms;
+      const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
+      const bool asplit = a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256;
+      if (asplit && cand != 256) continue;
+      // the split's second (N = nck) MMA per k-step costs about 64 rows' worth
+      // im2col A boxes cost about twice a tiled box; tiles whose width is not a whole number of
+      // 32-column chunks lose the bulk-tensor output stores (~4 k-blocks of epilogue)
+      const int a_rows = (cg != nullptr && (cg->a_mode == 1 || cg->a_mode == 2)) ? 256 : 128;
+      const long long rows = a_rows + 2LL * cand + nck + (asplit ? 64 : 0);
+      const int no_tma_store = (a->out_dtype != ABFT_OUT_NONE && !halo && cand % 32 != 0) ? 4 : 0;
+      const long long cost = waves * (nkb_plan + no_tma_store) * rows +
+                             (dbuf ? 0 : (waves - 1) * (thread_level ? 8 : 2) * rows);
+      if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
     }
     bn = best;
     if (bn == 0) return fail(ABFT_E_UNSUPPORTED, "no CTA tile fits this thread tile");
@@ -1343,11 +1477,12 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.nck = has_ck ? p.groups * (split ? 2 : 1) : (gck ? 2 : 0);
   p.nck_pad = (has_ck || gck) ? round_up(p.nck, 16) : 0;
   p.gck = gck ? 1 : 0;
-  p.out_lhs = gck ? a->out_lhs : nullptr;
+  p.out_lhs = (gck || gdot) ? a->out_lhs : nullptr;
+  p.lhs_w = gdot ? a->lhs_rowck : nullptr;
   p.num_m_blocks = m_blocks;
   p.num_n_blocks = ceil_div(n_ext, p.bn_eff);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  p.nkb = halo ? cg->R * cg->chunks : ceil_div(a->K, BK);
+  p.nkb = nkb_plan;
   p.cols_per_acc = tile_cols(bn, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
   p.shadow_off = bn + p.nck_pad;
   if (p.cols_per_acc > 512) return fail(ABFT_E_UNSUPPORTED, "TMEM budget exceeded");
@@ -1359,11 +1494,16 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.scheme = a->scheme; p.out_dtype = a->out_dtype; p.relu = a->relu;
   p.ck_mode = has_ck ? ((a->ck_rows != nullptr) ? 2 : 1) : (gck ? 2 : 0);
   if ((has_ck || gck) && a->ck_layout == 1) {
-    if (bn + p.nck_pad > 256) return fail(ABFT_E_UNSUPPORTED, "augmented weights need tile_n + checksum rows <= 256");
     p.ck_mode = 3;
+    if (bn + p.nck_pad > 256) {
+      if (bn != 256) return fail(ABFT_E_UNSUPPORTED, "augmented weights need tile_n + checksum rows <= 256 or tile_n 256");
+      p.ck_mode = 4;
+    }
   }
-  p.b_rows_blk = p.ck_mode == 3 ? bn + p.nck : bn;
-  p.tx_b = (uint32_t)p.b_rows_blk * BK * 2;
+  p.b_rows_blk = (p.ck_mode == 3 || p.ck_mode == 4) ? bn + p.nck : bn;
+  p.tx_b = (uint32_t)(p.ck_mode == 4 ? bn : p.b_rows_blk) * BK * 2;
+  p.ck_rstride = p.ck_mode == 4 ? p.b_rows_blk : p.nck_pad;
+  p.ck_roff = p.ck_mode == 4 ? bn : 0;
   if (halo && (p.ck_mode == 1 || p.ck_mode == 2 || want_acolck))
     return fail(ABFT_E_UNSUPPORTED, "halo conv mode needs augmented checksum weights");
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
@@ -1384,7 +1524,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.idesc_main = ptx::idesc_f16(fmt, BM, bn);
   p.idesc_ck = (has_ck || gck) ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
   p.idesc_ones = ptx::idesc_f16(fmt, 64, 8) | (1u << 15);    // M=64, N=8, A MN-major
-  p.idesc_aug = ptx::idesc_f16(fmt, BM, (uint32_t)(bn + p.nck_pad));
+  p.idesc_aug = p.ck_mode == 4 ? p.idesc_main : ptx::idesc_f16(fmt, BM, (uint32_t)(bn + p.nck_pad));
   {
     const char* dbg = getenv("ABFT_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
@@ -1410,7 +1550,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     p.stage_a_bytes = (uint32_t)round_up((int)p.tx_a, 1024);
     p.stage_b_bytes = p.b_tile_bytes * (uint32_t)cg->S;
   }
-  p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2, 1024);
+  p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2 * (halo ? cg->S : 1), 1024);
   p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
   const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
   const uint32_t rec_bytes = p.rec_stride ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
@@ -1424,7 +1564,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
                    !(dbg_env & 8192)) ? 1 : 0;
   }
-  const uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
+  uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
   // chunks split across both warps of a quadrant unless a check needs whole rows in one warp
   p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) && !(dbg_env & 65536) ? 1 : 0;
   if (a->a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
@@ -1433,23 +1573,41 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : 0u;
   const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
-  const uint32_t extras =
-      cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + out_bytes + acolck_bytes + ones_bytes + bar_bytes;
-  int budget = max_smem_optin() - 1024 /*alignment slack*/ - (int)extras;
-  if (const char* cap = getenv("ABFT_SMEM_CAP")) budget = std::min(budget, atoi(cap) * 1024 - (int)extras);
+  const uint32_t extras0 = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + acolck_bytes + ones_bytes + bar_bytes;
+  const int smem_cap = getenv("ABFT_SMEM_CAP") ? std::min(max_smem_optin() - 1024, atoi(getenv("ABFT_SMEM_CAP")) * 1024)
+                                              : max_smem_optin() - 1024 /*alignment slack*/;
+  p.out_single = 0;
+  {
+    // 16-bit outputs: one 2 KB staging buffer per epilogue warp instead of two when that buys
+    // a 4th pipeline stage (the stage_w / checksum-box layouts sit just past the 3-stage line)
+    const uint32_t stage_bytes0 = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes +
+                                  (p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u);
+    const int room = smem_cap - (int)extras0 - (p.lhs_w != nullptr ? 1024 : 0);
+    if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo && room / (int)stage_bytes0 < 4 &&
+        (room - (int)(8u * 2048u)) / (int)stage_bytes0 >= 4 && (room - (int)out_bytes) / (int)stage_bytes0 < 4) {
+      p.out_single = 1;
+      out_bytes = 8u * 2048u;
+    }
+  }
+  const uint32_t extras = extras0 + out_bytes;
+  int budget = smem_cap - (int)extras;
   // weight-stationary B (halo convs, whose stages carry S weight tiles each): one N-block, several M
   // tiles per CTA, B for all k-blocks fits beside >= 4 A stages
   const long long b_all = (long long)p.nkb * p.stage_b_bytes;
-  p.b_resident = (halo && p.num_n_blocks == 1 && p.num_tiles > 1 && p.ck_mode != 1 && p.ck_mode != 2 && !has_shadow &&
+  p.b_resident = (halo && p.num_n_blocks == 1 && p.num_tiles > 1 && p.ck_mode != 1 && p.ck_mode != 2 && p.ck_mode != 4 &&
+                  !has_shadow &&
                   b_all + 4LL * p.stage_a_bytes <= budget && !(dbg_env & 262144)) ? 1 : 0;
-  const uint32_t stage_bytes = p.stage_a_bytes + (p.b_resident ? 0u : p.stage_b_bytes) + p.stage_ck_bytes;
-  int stages = (budget - (p.b_resident ? (int)b_all : 0)) / (int)stage_bytes;
+  p.stage_w_bytes = p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u;
+  const uint32_t stage_bytes =
+      p.stage_a_bytes + (p.b_resident ? 0u : p.stage_b_bytes) + p.stage_ck_bytes + p.stage_w_bytes;
+  int stages = (budget - (p.b_resident ? (int)b_all : 0) - (p.stage_w_bytes ? 1024 : 0)) / (int)stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(ABFT_E_UNSUPPORTED, "shared memory budget too small for a 2-stage pipeline");
   p.stages = stages;
   p.off_b = stages * p.stage_a_bytes;
   p.off_ck = p.off_b + (p.b_resident ? (uint32_t)b_all : stages * p.stage_b_bytes);
-  p.off_cks = p.off_ck + stages * p.stage_ck_bytes;
+  p.off_w = p.off_ck + stages * p.stage_ck_bytes;
+  p.off_cks = (uint32_t)round_up((int)(p.off_w + stages * p.stage_w_bytes), 1024);
   p.off_rec = p.off_cks + cks_bytes;
   p.off_stage = p.off_rec + rec_bytes;
   p.off_colck = p.off_stage + stage_bytes_ep;
@@ -1535,7 +1693,7 @@ extern "C" __attribute__((visibility("default"))) int abft_aug_weights(const voi
                                                                       int32_t nck_pad, int32_t n_blocks, void* out,
                                                                       int64_t ldo, void* stream) {
   if (N < 1 || K < 1 || nt < 1 || bn_eff < nt || bn_eff % nt || bn_eff > tile_n || nck_pad < 16 || nck_pad % 16 ||
-      ldo < K || ldbt < K || tile_n + nck_pad > 256)
+      ldo < K || ldbt < K || (tile_n + nck_pad > 256 && tile_n != 256))
     return fail(ABFT_E_SHAPE, "aug_weights: bad extents");
   const int groups = bn_eff / nt;
   if (groups * (split ? 2 : 1) > nck_pad) return fail(ABFT_E_SHAPE, "aug_weights: nck_pad too small");
@@ -1607,12 +1765,15 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   GemmParams& p = pl.p;
   CUtensorMap mb, mc;
   int rc;
-  if (p.ck_mode == 3) {
+  if (p.ck_mode == 3 || p.ck_mode == 4) {
     // augmented weights: the B operand (tile rows + checksum rows per N-block) is ck_rows
     if (a->ck_rows == nullptr || a->ck_rows_n != p.num_n_blocks * p.b_rows_blk || a->ldck < a->K || (a->ldck % 8) ||
         (reinterpret_cast<uintptr_t>(a->ck_rows) & 15))
       return fail(ABFT_E_SHAPE, "augmented weights do not match this call's plan (see abft_gemm_plan / abft_aug_weights)");
-    rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.b_rows_blk);
+    rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.ck_mode == 4 ? p.bn : p.b_rows_blk);
+    // split: the block's checksum rows (and the next block's first rows, whose products land in
+    // ignored checksum columns) by a second box
+    if (rc == ABFT_OK && p.ck_mode == 4) rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
   } else {
     rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
   }
@@ -1625,7 +1786,7 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
                                       : "ck_rows do not match this call's plan (see abft_gemm_plan)");
     rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
     if (rc != ABFT_OK) return rc;
-  } else {
+  } else if (p.ck_mode != 4) {
     mc = mb;   // unused
   }
   CUtensorMap mo;
@@ -1687,7 +1848,8 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   {
     const bool thread_level = c->gemm.scheme >= ABFT_ONE_SIDED;
     const bool ck_ok = c->gemm.scheme == ABFT_UNPROTECTED ||
-                       (c->gemm.scheme == ABFT_GLOBAL ? (c->gemm.out_lhs == nullptr || c->gemm.ck_layout == 1)
+                       (c->gemm.scheme == ABFT_GLOBAL ? (c->gemm.out_lhs == nullptr || c->gemm.ck_layout == 1 ||
+                                                         c->gemm.lhs_rowck != nullptr)
                                                       : (c->gemm.ck_layout == 1 && c->gemm.ck_rows != nullptr));
     const int mt = thread_level ? std::max(1, c->gemm.thread_m) : 1;
     if (mode == 1 && c->stride_h == 1 && c->stride_w == 1 && c->s <= 16 && ck_ok && c->gemm.a_colck == nullptr &&
@@ -1784,19 +1946,16 @@ extern "C" __attribute__((visibility("default"))) int abft_conv_plan(const abft_
   return ABFT_OK;
 }
 
-extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_conv_args_t* c, void* stream) {
-  if (c == nullptr) return fail(ABFT_E_VALUE, "null args");
-  ConvGeom g;
+// geometry, GEMM view and kernel plan of one conv call (shared by abft_conv2d and its plan query)
+static int conv_make_plan(const abft_conv_args_t* c, ConvGeom& g, abft_gemm_args_t& ga, Plan& pl) {
   int rc = conv_geom(c, g);
   if (rc != ABFT_OK) return rc;
-  abft_gemm_args_t ga;
   rc = conv_gemm_args(c, g, ga);
   if (rc != ABFT_OK) return rc;
   if (c->gemm.K != 0 && c->gemm.K != g.K)
     return fail(ABFT_E_SHAPE, "packed weight K must equal r*s*c (see abft_conv_plan)");
   rc = validate_common(&ga);
   if (rc != ABFT_OK) return rc;
-  Plan pl;
   rc = make_plan(&ga, pl, &g);
   if (rc != ABFT_OK && g.a_mode == 4) {
     // the halo stages (S weight tiles each) do not fit this tile: per-tap im2col instead
@@ -1804,6 +1963,29 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
     g.a_mode = 1;
     rc = make_plan(&ga, pl, &g);
   }
+  return rc;
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_conv_gemm_plan(const abft_conv_args_t* c, int32_t* out) {
+  if (c == nullptr || out == nullptr) return fail(ABFT_E_VALUE, "null args");
+  ConvGeom g;
+  abft_gemm_args_t ga;
+  Plan pl;
+  int rc = conv_make_plan(c, g, ga, pl);
+  if (rc != ABFT_OK) return rc;
+  out[0] = pl.p.bn; out[1] = pl.p.bn_eff; out[2] = pl.p.groups; out[3] = pl.p.nck_pad; out[4] = pl.p.stages;
+  out[5] = pl.ck_offline_recommended; out[6] = pl.p.num_n_blocks; out[7] = pl.grid;
+  out[8] = pl.p.bn + pl.p.nck;
+  out[9] = g.a_mode;
+  return ABFT_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_conv_args_t* c, void* stream) {
+  if (c == nullptr) return fail(ABFT_E_VALUE, "null args");
+  ConvGeom g;
+  abft_gemm_args_t ga;
+  Plan pl;
+  int rc = conv_make_plan(c, g, ga, pl);
   if (rc != ABFT_OK) return rc;
   GemmParams& p = pl.p;
   if (g.a_mode == 4) {

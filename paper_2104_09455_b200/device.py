@@ -194,7 +194,8 @@ def prepare_weight(b, dtype: DType, with_rowck: bool = True) -> PreparedWeight:
     bt = upload_transposed(b, dtype)
     rowck = None
     if with_rowck:
-        rowck = torch().empty(bt.shape[1], dtype=torch().float32, device="cuda")
+        # zero-padded to a whole number of 64-column k-blocks (the global lhs_rowck layout)
+        rowck = torch().zeros(-(-bt.shape[1] // 64) * 64, dtype=torch().float32, device="cuda")
         _lib.call("abft_colsum", ptr(bt), n, bt.shape[1], bt.shape[1], storage_code(dtype), ptr(rowck), 0,
                   stream_handle())
     return PreparedWeight(bt=bt, rowck=rowck, k=k, n=n, dtype=dtype)

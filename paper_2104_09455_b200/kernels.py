@@ -24,7 +24,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
                num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
-               ck_layout: int = None):
+               ck_layout: int = None, lhs_rowck=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -51,6 +51,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         args.ck_layout = int(getattr(ck_rows, "_abft_aug", 0))
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
+    args.lhs_rowck = lhs_rowck.data_ptr() if lhs_rowck is not None else None
     args.pdl = int(pdl)
     vt = ()
     if verify is not None:
@@ -62,7 +63,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         vt = (vsums, vks, vdone, vout, vdet)
     # the struct holds raw device pointers: keep every tensor it points to alive with it
     args._keep = [x for x in (a, bt, out, faults, out_sum, next_colck, verdicts, fired_count, fired, ck_rows,
-                              a_colck, out_lhs) + vt if x is not None]
+                              a_colck, out_lhs, lhs_rowck) + vt if x is not None]
     return args
 
 
@@ -103,6 +104,15 @@ def conv_plan(args) -> dict:
     out = (ctypes.c_int32 * 8)()
     _lib.check(_lib.load().abft_conv_plan(ctypes.byref(args), out))
     return dict(a_mode=out[0], ck=out[1], p=out[2], q=out[3], k=out[4], m=out[5], ws=out[6])
+
+
+def conv_gemm_plan(args) -> dict:
+    """abft_conv_gemm_plan: the conv kernel's tile plan (abft_gemm_plan's fields + a_mode) — the
+    plan augmented weights / checksum rows of a conv call are built for."""
+    out = (ctypes.c_int32 * 10)()
+    _lib.check(_lib.load().abft_conv_gemm_plan(ctypes.byref(args), out))
+    return dict(tile_n=out[0], bn_eff=out[1], groups=out[2], nck_pad=out[3], stages=out[4],
+                ck_offline_recommended=bool(out[5]), n_blocks=out[6], grid=out[7], aug_rows=out[8], a_mode=out[9])
 
 
 def conv2d(args) -> None:
@@ -163,6 +173,14 @@ def global_ck_rows(bt, n: int, k: int, dtype: DType, plan: dict, augmented: bool
 def colsum(x, rows: int, cols: int, ldx: int, dtype: DType, out, accumulate: bool = False) -> None:
     _lib.call("abft_colsum", ptr(x), rows, cols, ldx, storage_code(dtype), ptr(out), int(accumulate),
               stream_handle())
+
+
+def weight_rowck(bt, n: int, k: int, dtype: DType):
+    """rowck(B) fp32: column sums of B^T [n x k] (checksum.py:99-105), zero-padded to whole
+    64-column k-blocks — the global scheme's lhs_rowck."""
+    out = torch().zeros(-(-bt.stride(0) // 64) * 64, dtype=torch().float32, device="cuda")
+    colsum(bt, n, bt.stride(0), bt.stride(0), dtype, out)
+    return out
 
 
 def matrix_sum(x, out) -> None:

@@ -150,22 +150,29 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
     sums = t.zeros(2, dtype=t.float64, device="cuda") if scheme is Scheme.GLOBAL_ABFT else None
     out_sum = sums[1:2] if sums is not None else None
     out_lhs = sums[0:1] if sums is not None else None
-    if ck_source not in ("auto", "aug", "onchip", "offline"):
-        raise ValueError(f"ck_source must be 'auto', 'aug', 'onchip' or 'offline', got {ck_source!r}")
-    if ck_source == "auto":
-        ck_source = "aug"
+    if ck_source not in ("auto", "aug", "onchip", "offline", "dot"):
+        raise ValueError(f"ck_source must be 'auto', 'aug', 'onchip', 'offline' or 'dot', got {ck_source!r}")
+    if ck_source == "dot" and scheme is not Scheme.GLOBAL_ABFT:
+        raise ValueError("ck_source 'dot' is the global scheme's lhs")
     split = ck_split and not dtype.is_exact
     call = dict(out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
                 m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
                 out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, out_lhs=out_lhs)
     ckr = None
     # checksum rows of the weights: appended to each weight tile ("aug": one MMA per k-step),
-    # as separate rows ("offline": their own MMA slice) or generated on chip ("onchip")
+    # as separate rows ("offline": their own MMA slice) or generated on chip ("onchip").
+    # Global lhs: the checksum N-slice ("aug", default / "offline") or the checksum warps' dot of
+    # the staged A tiles with rowck(B) ("dot": no MMA slice, but an extra shared-memory read of A).
+    if ck_source == "auto":
+        ck_source = "aug"
     if scheme is Scheme.GLOBAL_ABFT:
-        aug = ck_source != "offline"
-        gplan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
-                             plan_only=True, ck_layout=int(aug), **call)
-        ckr = kernels.global_ck_rows(bt_dev, n, k, dtype, gplan, augmented=aug)
+        if ck_source == "dot":
+            call["lhs_rowck"] = kernels.weight_rowck(bt_dev, n, k, dtype)
+        else:
+            aug = ck_source != "offline"
+            gplan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,
+                                 plan_only=True, ck_layout=int(aug), **call)
+            ckr = kernels.global_ck_rows(bt_dev, n, k, dtype, gplan, augmented=aug)
     if scheme in (Scheme.THREAD_ONE_SIDED, Scheme.THREAD_TWO_SIDED) and ck_source != "onchip":
         aug = ck_source == "aug"
         plan = kernels.gemm(a_dev, a_dev.stride(0), bt_dev, bt_dev.stride(0), m, n, k, dtype, numeric, scheme,

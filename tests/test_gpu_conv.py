@@ -130,12 +130,16 @@ def test_conv_global_fused_and_standalone_checksums_agree(P, case):
     x, wt, cols, wmat = _data(case, exact=True, seed=3)
     m = cols.shape[0]
     for faults in ([], [P.OutputFault(row=m // 3, col=1, delta=7)]):
-        a = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme.GLOBAL_ABFT, faults=faults)
         b = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme.GLOBAL_ABFT, faults=faults,
                      colck_source="standalone")
-        va, vb = a.verdicts[0], b.verdicts[0]
-        assert (va.detected, va.lhs, va.rhs) == (vb.detected, vb.lhs, vb.rhs)
-        assert va.detected == bool(faults)
+        vb = b.verdicts[0]
+        assert vb.detected == bool(faults)
+        # checksum N-slice, checksum-warp dot with rowck(B), and the default choice between them
+        for src in ("slice", "dot", "fused"):
+            a = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme.GLOBAL_ABFT, faults=faults, colck_source=src)
+            va = a.verdicts[0]
+            assert (va.detected, va.lhs, va.rhs) == (vb.detected, vb.lhs, vb.rhs), src
+            assert np.array_equal(a.output, b.output), src
 
 
 @pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
@@ -152,7 +156,35 @@ def test_conv_every_a_load_mode_bit_exact(P, mode, monkeypatch):
         for scheme in ("unprotected", "global-abft", "thread-one-sided"):
             faults_ref = [("output", m - 1, 0, 9)] if scheme != "unprotected" else []
             faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in faults_ref]
-            rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults)
             out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, faults_ref)
-            assert np.array_equal(rep.output.reshape(m, oc), out), (mode, case, scheme)
-            assert rep.detected == any(v.detected for v in verdicts), (mode, case, scheme)
+            for src in (("slice", "dot") if scheme == "global-abft" else ("fused",)):
+                rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults,
+                               colck_source=src)
+                assert np.array_equal(rep.output.reshape(m, oc), out), (mode, case, scheme, src)
+                assert rep.detected == any(v.detected for v in verdicts), (mode, case, scheme, src)
+                if scheme == "global-abft":
+                    v, rv = rep.verdicts[0], verdicts[0]
+                    assert (v.lhs, v.rhs) == (rv.lhs, rv.rhs), (mode, case, src)
+
+
+@pytest.mark.parametrize("case", [(1, 6, 64, 64, 256, 3, 3, 1, 1),      # halo (Qt = 64), N = one 256 tile
+                                  (2, 7, 9, 64, 300, 3, 3, 1, 1),       # 64-channel im2col, two N tiles
+                                  (2, 12, 12, 32, 260, 1, 1, 1, 0)])    # pointwise
+@pytest.mark.parametrize("scheme", ["global-abft", "thread-one-sided"])
+def test_conv_full_width_tile_checksum_slice(P, case, scheme):
+    """tile_n = 256: the checksum rows of the augmented weights go through their own box and
+    MMA N-slice (ck_mode 4), in every A-load mode.  Exact-int parity with the oracle."""
+    n, h, w, c, oc, r, s, st, pd = case
+    x, wt, cols, wmat = _data(case, exact=True, seed=5)
+    m = cols.shape[0]
+    fr = [("output", m - 1, oc - 1, 6), ("output", 3, 130, -2)]
+    faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
+    rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults, tile_n=256)
+    out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, fr)
+    assert np.array_equal(rep.output.reshape(m, oc), out)
+    if scheme == "global-abft":
+        v, rv = rep.verdicts[0], verdicts[0]
+        assert (v.detected, v.lhs, v.rhs) == (rv.detected, rv.lhs, rv.rhs)
+    else:
+        assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \
+            [(v.thread_row, v.thread_col) for v in verdicts if v.detected]

@@ -232,3 +232,53 @@ def test_shape_errors_map_to_reference_exceptions(P):
     with pytest.raises(ValueError):
         P.execute(np.ones((16, 16), dtype=np.int64), np.ones((16, 16), dtype=np.int64), P.TilingConfig(),
                   P.Scheme.GLOBAL_ABFT, [P.OutputFault(row=16, col=0, delta=1)])
+
+
+@pytest.mark.parametrize("m,n,k", [(700, 300, 200), (1, 512, 13), (300, 1000, 72), (2048, 512, 512)])
+def test_global_lhs_variants_agree(P, m, n, k):
+    """Global lhs from the checksum N-slice (appended or separate checksum rows) and from the
+    checksum warps' dot of the staged A tiles with rowck(B): exact-int verdict values equal the
+    oracle's (colck(A) . rowck(B) and the output summation, checksum.py:108-127)."""
+    rng = np.random.default_rng(m + n + k)
+    a = rng.integers(-8, 9, size=(m, k), dtype=np.int64)
+    b = rng.integers(-8, 9, size=(k, n), dtype=np.int64)
+    fr = [("output", m // 2, n - 1, 13)]
+    out_ref, v_ref = O.execute(a, b, O.Tiling(), "global-abft", fr)
+    faults = [P.OutputFault(row=m // 2, col=n - 1, delta=13)]
+    for src in ("aug", "offline", "dot", "auto"):
+        rep = P.execute(a, b, P.TilingConfig(), P.Scheme.GLOBAL_ABFT, faults, ck_source=src)
+        assert np.array_equal(rep.output, out_ref), src
+        v = rep.verdicts[0]
+        assert (v.detected, v.lhs, v.rhs, v.tolerance_used) == \
+            (v_ref[0].detected, v_ref[0].lhs, v_ref[0].rhs, v_ref[0].tolerance_used), src
+    # binary16: the dot and the slice agree to fp32-accumulation rounding, no false positive
+    af = rng.uniform(-1, 1, size=(m, k)).astype(np.float16)
+    bf = rng.uniform(-1, 1, size=(k, n)).astype(np.float16)
+    r1 = P.execute(af, bf, P.TilingConfig(), P.Scheme.GLOBAL_ABFT, ck_source="aug")
+    r2 = P.execute(af, bf, P.TilingConfig(), P.Scheme.GLOBAL_ABFT, ck_source="dot")
+    assert r1.detected is False and r2.detected is False
+    assert r1.verdicts[0].rhs == pytest.approx(r2.verdicts[0].rhs, rel=1e-6, abs=1e-6)
+    assert r1.verdicts[0].lhs == pytest.approx(r2.verdicts[0].lhs, rel=1e-4, abs=1e-3)
+
+
+@pytest.mark.parametrize("scheme", ["global-abft", "thread-one-sided", "thread-two-sided"])
+@pytest.mark.parametrize("m,n,k", [(700, 600, 300), (300, 256, 1000)])
+def test_augmented_weights_with_full_width_tile(P, scheme, m, n, k):
+    """tile_n = 256 with augmented weights: the checksum rows no longer fit the one MMA
+    (N <= 256), so they come by their own box into their own N-slice (single-buffered
+    accumulator).  Exact-int outputs and verdicts equal the oracle's."""
+    rng = np.random.default_rng(m * 3 + n + k)
+    a = rng.integers(-8, 9, size=(m, k), dtype=np.int64)
+    b = rng.integers(-8, 9, size=(k, n), dtype=np.int64)
+    fr = [("output", m - 2, n - 3, -9), ("output", 17, 255, 4)]
+    out_ref, v_ref = O.execute(a, b, O.Tiling(), scheme, fr)
+    faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
+    rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults, ck_source="aug", tile_n=256)
+    assert np.array_equal(rep.output, out_ref)
+    if scheme == "global-abft":
+        v = rep.verdicts[0]
+        assert (v.detected, v.lhs, v.rhs) == (v_ref[0].detected, v_ref[0].lhs, v_ref[0].rhs)
+    else:
+        assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \
+            [(v.thread_row, v.thread_col) for v in v_ref if v.detected]
+        assert len([v for v in rep.verdicts if v.detected]) == 2

@@ -41,6 +41,11 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert not missing, missing
     assert set(_lib.EXPORTED_SYMBOLS) == set(_declared_symbols())
     assert lib.abft_version() == 100
+    # the ctypes mirrors of the header's structs have the C layout's size
+    import ctypes
+    for which, cls in enumerate((_lib.GemmArgs, _lib.ConvArgs, _lib.GlobalTask, _lib.VerdictC, _lib.ThreadVerdictC,
+                                 _lib.Fault)):
+        assert lib.abft_struct_size(which) == ctypes.sizeof(cls), cls.__name__
     # pure host query: no device in this container
     assert lib.abft_device_sms() in (0, 148) or lib.abft_device_sms() > 0
 

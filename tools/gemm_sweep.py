@@ -48,6 +48,9 @@ def run(m, n, k):
                                                        P.Scheme.UNPROTECTED, **base), it)
     res["global"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                        P.Scheme.GLOBAL_ABFT, ck_rows=gck, **gkw), it)
+    rowck = kernels.weight_rowck(pw.bt, n, k, P.BINARY16)
+    res["global_dot"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
+                                                           P.Scheme.GLOBAL_ABFT, lhs_rowck=rowck, **gkw), it)
     res["one_chip"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
                                                          P.Scheme.THREAD_ONE_SIDED, **one), it)
     res["one_off"] = graph_time_us(lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1,
@@ -59,7 +62,8 @@ def run(m, n, k):
     gbs = 2 * (m * k + k * n + m * n) / (res["unprot"] * 1e-6) / 1e9
     print(f"{m:6d} {n:5d} {k:5d} | " + " ".join(f"{key}={v:8.2f}" for key, v in res.items()) +
           f" | unprot {tf:7.1f} TF/s {gbs:7.1f} GB/s | plan u={uplan['tile_n']}/{uplan['stages']}st grid {uplan['grid']}"
-          f" one={plan['tile_n']}/{plan['stages']}st", flush=True)
+          f" one={plan['tile_n']}/{plan['stages']}st aug={aplan['tile_n']}/{aplan['stages']}st"
+          f" glob={gplan['tile_n']}/{gplan['stages']}st", flush=True)
 
 
 def stamps(m, n, k):

@@ -1,11 +1,9 @@
 #!/bin/bash
-# one iteration on the GPU box: GPU tests, GEMM sweep, a network subset
+# GPU tests + GEMM sweep + one default bench run
 TAG=${1:-r01x}
-NETS=${2:-resnet50,vgg16}
-CFGS=${3:-b256}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 tail -3 gpurun_out/pytest_gpu_$TAG.log
 timeout 600 python tools/gemm_sweep.py > gpurun_out/gemm_sweep_$TAG.log 2>&1
-timeout 1500 python tools/netbench.py --nets $NETS --configs $CFGS --cudnn --out gpurun_out/netbench_$TAG.jsonl > gpurun_out/netbench_$TAG.log 2>&1
-echo done
+timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+tail -c 600 gpurun_out/bench_$TAG.json

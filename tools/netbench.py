@@ -58,14 +58,16 @@ def main():
                 r = LayerRunner(spec)
                 it = args.iters if r.flops() < 2e11 else max(3, args.iters // 4)
                 t_un = profiler.graph_time_us(lambda: r.conv(S.UNPROTECTED), it)
-                t_glf = profiler.graph_time_us(lambda: r.conv(S.GLOBAL_ABFT), it)        # checksum in-kernel
+                t_glf = profiler.graph_time_us(lambda: r.conv(S.GLOBAL_ABFT), it)        # checksum N-slice
+                t_gld = profiler.graph_time_us(lambda: r.conv_variant("global-dot"), it)  # checksum-warp dot
                 t_gls = profiler.graph_time_us(r.global_standalone, it)                  # + standalone pass
                 t_ck = profiler.graph_time_us(r.colck_pass, it)
-                t_gl = min(t_glf, t_gls)
+                t_gl = min(t_glf, t_gld, t_gls)
                 t_one = profiler.graph_time_us(lambda: r.conv(S.THREAD_ONE_SIDED), it)
                 row = dict(i=spec.index, kind=spec.kind, m=r.m, n=spec.oc, k=r.k_ref, r=spec.r, stride=spec.stride_h,
                            cin=spec.cin, t_un=t_un, t_gl=t_gl, t_gl_fused=t_glf, t_gl_standalone=t_gls, t_ck=t_ck,
-                           t_one=t_one, global_variant="fused" if t_glf <= t_gls else "standalone")
+                           t_gl_dot=t_gld, t_one=t_one,
+                           global_variant=min((t_glf, "fused"), (t_gld, "dot"), (t_gls, "standalone"))[1])
                 if args.cudnn:
                     x = torch.randn(spec.n, spec.cin, spec.h, spec.w, device="cuda", dtype=torch.float16) \
                         .to(memory_format=torch.channels_last)

@@ -1,4 +1,4 @@
-"""Time protected-GEMM variants: python tools/probe.py "M N K scheme tile_n [debug] [acolck]" ..."""
+"""Time protected-GEMM variants: python tools/probe.py "M N K scheme tile_n [debug] [acolck|dot|gck]" ..."""
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -24,13 +24,19 @@ for spec in sys.argv[1:]:
         kw["out_sum"] = torch.zeros(1, dtype=torch.float64, device="cuda")
         if acol:
             kw["a_colck"] = torch.zeros(k, dtype=torch.float32, device="cuda")
+        elif len(f) > 6 and f[6] == "dot":
+            kw["out_lhs"] = torch.zeros(1, dtype=torch.float64, device="cuda")
+            kw["lhs_rowck"] = kernels.weight_rowck(pw.bt, n, k, P.BINARY16)
         elif len(f) > 6 and f[6] == "gck":
             kw["out_lhs"] = torch.zeros(1, dtype=torch.float64, device="cuda")
-            gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, plan_only=True, **kw)
+            gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, plan_only=True, ck_layout=1, **kw)
             kw["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
     elif sch is not P.Scheme.UNPROTECTED:
         kw.update(fired_count=torch.zeros(1, dtype=torch.int32, device="cuda"), m_ext=-(-m // 16) * 16,
                   n_ext=-(-n // 8) * 8)
+        if len(f) > 6 and f[6] == "aug":
+            tplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, plan_only=True, ck_layout=1, **kw)
+            kw["ck_rows"] = kernels.aug_weights(pw.bt, n, k, P.BINARY16, tplan, 8, False)
     os.environ["ABFT_DEBUG"] = str(dbg)
     try:
         plan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, plan_only=True, **kw)
