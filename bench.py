@@ -190,7 +190,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2104_09455_b200 as P
     from paper_2104_09455_b200 import kernels, profiler
-    from paper_2104_09455_b200.network import ProtectedChain
+    from paper_2104_09455_b200.network import ChainGroup
     from paper_2104_09455_b200.shapes import DeviceProfile, GemmShape
 
     base = load_baseline()
@@ -221,28 +221,54 @@ def main():
     wt = {name: [torch.from_numpy(w).cuda() for w in ws] for name, ws in mlps.items()}
     policies = {"unprotected": lambda k: [S.UNPROTECTED] * 3, "global": lambda k: [S.GLOBAL_ABFT] * 3,
                 "thread": lambda k: [S.THREAD_ONE_SIDED] * 3, "ig": lambda k: plans[k]}
-    chains = {pol: {k: ProtectedChain(wt[k[0]], k[1], f(k)) for k in inputs} for pol, f in policies.items()}
+    # one ChainGroup per policy: one memset clears all 24 chains' accumulators, one launch at the
+    # end verifies every global layer of the step (deferred verification, batched)
+    keys = list(inputs)
+    groups = {pol: ChainGroup([(wt[k[0]], k[1], f(k)) for k in keys]) for pol, f in policies.items()}
+    chains = {pol: dict(zip(keys, groups[pol].chains)) for pol in groups}
+    # every chain's input and final output are views of one device block, so the end-to-end
+    # step moves them with ONE host->device and ONE device->host copy
+    io = {}
+    for pol, grp in groups.items():
+        n_in = sum(ch.x.numel() for ch in grp.chains)
+        n_out = sum(ch.acts[-1].numel() for ch in grp.chains)
+        dev_in = torch.zeros(n_in, dtype=torch.float16, device="cuda")
+        dev_out = torch.zeros(n_out, dtype=torch.float16, device="cuda")
+        oi = oo = 0
+        for ch in grp.chains:
+            ch.x = dev_in[oi:oi + ch.x.numel()].view(ch.x.shape)
+            ch.acts[-1] = dev_out[oo:oo + ch.acts[-1].numel()].view(ch.acts[-1].shape)
+            oi += ch.x.numel()
+            oo += ch.acts[-1].numel()
+        io[pol] = (dev_in, dev_out)
     for pol in chains:
         for k, ch in chains[pol].items():
             ch.x.copy_(torch.from_numpy(inputs[k]).cuda())
 
     def capture(pol):
-        """All chains of a policy as parallel branches of one CUDA graph."""
-        cs = list(chains[pol].values())
+        """All chains of a policy as parallel branches of one CUDA graph, between the group's
+        accumulator clear and its one verification launch."""
+        grp = groups[pol]
+        cs = grp.chains
         main = torch.cuda.Stream()
         streams = [torch.cuda.Stream() for _ in cs]
         main.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(main):
-            for ch in cs:
-                ch.forward()
+            grp.forward()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=main):
-            for s, ch in zip(streams, cs):
-                s.wait_stream(main)
-                with torch.cuda.stream(s):
+            grp.begin()
+            if os.environ.get("BENCH_SERIAL"):
+                for ch in cs:
                     ch.forward()
-                main.wait_stream(s)
+            else:
+                for s, ch in zip(streams, cs):
+                    s.wait_stream(main)
+                    with torch.cuda.stream(s):
+                        ch.forward()
+                    main.wait_stream(s)
+            grp.end()
         torch.cuda.synchronize()
         return g
 
@@ -251,11 +277,10 @@ def main():
 
     # multi-GPU: the only collective of a protected forward — one all-reduce of every chain's
     # flag counters (fired thread tiles, flagged global layers) over NVLink
-    ig_chains = list(chains["ig"].values())
-    flags_buf = torch.zeros((len(ig_chains), 2), dtype=torch.int32, device="cuda")
+    flags_buf = torch.zeros(len(keys) + 1, dtype=torch.int32, device="cuda")
 
     def reduce_flags():
-        torch.stack([c.counters for c in ig_chains], out=flags_buf)
+        torch.cat([groups["ig"].counters[:, 0], groups["ig"].flagged], out=flags_buf)
         torch.distributed.all_reduce(flags_buf)
 
     def timed(pol, steps, warmup):
@@ -265,7 +290,8 @@ def main():
         torch.cuda.synchronize()
         ts = []
         for _ in range(steps):
-            flush.fill_(1.0)
+            if not os.environ.get("BENCH_NOFLUSH"):
+                flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 torch.distributed.barrier()
@@ -296,25 +322,26 @@ def main():
     value = world * flops / (ms_step * 1e-3) / 1e12
 
     # ---- correctness of the timed configuration: clean run flags nothing
-    fired = {pol: [ch.flags() for ch in chains[pol].values()] for pol in ("ig", "global", "thread")}
-    clean_ok = all(f == (0, 0) for v in fired.values() for f in v)
+    fired = {pol: groups[pol].flags() for pol in ("ig", "global", "thread")}
+    clean_ok = all(f == (0, 0) for f in fired.values())
 
     # ---- end to end through the host API: pinned inputs in, outputs + verdict counters out
-    host_in = {k: torch.from_numpy(v).pin_memory() for k, v in inputs.items()}
-    host_out = {k: torch.empty(chains["ig"][k].acts[-1].shape, dtype=torch.float16).pin_memory() for k in inputs}
-    host_cnt = {k: torch.empty(2, dtype=torch.int32).pin_memory() for k in inputs}
-    h2d = sum(v.numel() * 2 for v in host_in.values())
-    d2h = sum(v.numel() * 2 for v in host_out.values()) + 8 * len(host_cnt)
+    dev_in, dev_out = io["ig"]
+    host_in = torch.cat([torch.from_numpy(inputs[k]).reshape(-1) for k in keys]).pin_memory()
+    host_out = torch.empty(dev_out.shape, dtype=torch.float16).pin_memory()
+    host_cnt = torch.empty(groups["ig"].counters.shape, dtype=torch.int32).pin_memory()
+    host_flagged = torch.empty(1, dtype=torch.int32).pin_memory()
+    h2d = host_in.numel() * 2
+    d2h = host_out.numel() * 2 + host_cnt.numel() * 4 + 4
 
     def e2e_step():
-        for k, ch in chains["ig"].items():
-            ch.x.copy_(host_in[k], non_blocking=True)
+        dev_in.copy_(host_in, non_blocking=True)
         graphs["ig"].replay()
-        for k, ch in chains["ig"].items():
-            host_out[k].copy_(ch.acts[-1], non_blocking=True)
-            host_cnt[k].copy_(ch.counters, non_blocking=True)
+        host_out.copy_(dev_out, non_blocking=True)
+        host_cnt.copy_(groups["ig"].counters, non_blocking=True)
+        host_flagged.copy_(groups["ig"].flagged, non_blocking=True)
         torch.cuda.synchronize()
-        return sum(int(c[0]) + int(c[1]) for c in host_cnt.values())
+        return int(host_cnt[:, 0].sum()) + int(host_flagged[0])
     for _ in range(args.warmup):
         e2e_step()
     e2e_ts = []

@@ -1207,23 +1207,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   __syncwarp();
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
-  if (p.vn > 0 && threadIdx.x == EPI_WARP0 * 32) {
+  if (p.vn > 0 && warp == EPI_WARP0) {
     // fused deferred verification: the launch's last CTA to finish (done-count) forms every
-    // layer's verdict from the accumulated (lhs, rhs) pairs (checksum.py:151-153, :237); this is
-    // the thread that added the CTA's (rhs, lhs)
-    __threadfence();
-    if (atomicAdd(p.vdone, 1) == (int)gridDim.x - 1) {
+    // layer's verdict from the accumulated (lhs, rhs) pairs (checksum.py:151-153, :237).  Lane 0
+    // added the CTA's (rhs, lhs) after the epilogue barrier; its acq_rel count increment
+    // publishes them (and the checksum warps' lhs atomics, ordered by __syncthreads) at gpu
+    // scope without a full fence per CTA.
+    int last = 0;
+    if (lane == 0) {
+      int prev;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.vdone) : "memory");
+      last = prev == (int)gridDim.x - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
       __threadfence();
-      for (int i = 0; i < p.vn; ++i) {
-        const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
-        const double tol = tolerance(p.r, p.vk[i], lhs, rhs);
-        abft_verdict_t v;
-        v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = p.vk[i];
-        v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
-        if (p.vout) p.vout[i] = v;
-        if (v.detected && p.vdetected) atomicAdd(p.vdetected, 1);
+      int ndet = 0;
+      for (int i0 = 0; i0 < p.vn; i0 += 32) {
+        const int i = i0 + lane;
+        bool det = false;
+        if (i < p.vn) {
+          const double lhs = __ldcg(p.vsums + 2 * i), rhs = __ldcg(p.vsums + 2 * i + 1);
+          const double tol = tolerance(p.r, p.vk[i], lhs, rhs);
+          abft_verdict_t v;
+          v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = p.vk[i];
+          v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
+          det = v.detected != 0;
+          if (p.vout) p.vout[i] = v;
+        }
+        ndet += __popc(__ballot_sync(0xffffffffu, det));
       }
-      *p.vdone = 0;                                  // ready for the next launch / replay
+      if (lane == 0) {
+        if (ndet && p.vdetected) atomicAdd(p.vdetected, ndet);
+        *p.vdone = 0;                                  // ready for the next launch / replay
+      }
     }
   }
   if (stamp && threadIdx.x == 32) g_dbg_ts[blockIdx.x][4] = gtimer();

@@ -23,6 +23,10 @@ exposes the per-layer [lhs, rhs] sums so callers can all-reduce them (NCCL) and 
 
 from __future__ import annotations
 
+import os
+
+_NO_PDL = bool(os.environ.get("ABFT_NO_PDL"))     # measurement toggle
+
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -55,6 +59,9 @@ class ProtectedChain:
     ck_split: bool = False
     faults: Optional[dict] = None        # {layer: [(row, col, delta)]}: deltas added to the fp32 accumulator
     pdl: bool = True                     # programmatic dependent launch between consecutive layers
+    # (sums [nl, 2] fp64, counters int32 [2], vdone int32 [1]) views of a ChainGroup's block: the
+    # group clears them and verifies every member's global layers in one launch
+    shared: Optional[tuple] = None
     layers: List[_Layer] = field(default_factory=list, init=False)
 
     def __post_init__(self):
@@ -79,13 +86,17 @@ class ProtectedChain:
         self.x = t.zeros((m, self.layers[0].k), dtype=sd, device="cuda")
         self.acts = [t.zeros((m, L.n), dtype=sd, device="cuda") for L in self.layers]
         nl = len(self.layers)
-        # every per-forward accumulator lives in ONE block so a single memset node clears it:
-        # [(lhs, rhs) fp64 per layer][counters int32 x 2][verification done-count int32, pad]
-        off_cnt = 16 * nl
-        self.scratch = t.zeros(off_cnt + 16, dtype=t.uint8, device="cuda")
-        self.sums = self.scratch[:off_cnt].view(t.float64).view(nl, 2)
-        self.counters = self.scratch[off_cnt:off_cnt + 8].view(t.int32)   # [fired thread tiles, flagged layers]
-        self.vdone = self.scratch[off_cnt + 8:off_cnt + 12].view(t.int32)
+        if self.shared is None:
+            # every per-forward accumulator lives in ONE block so a single memset node clears it:
+            # [(lhs, rhs) fp64 per layer][counters int32 x 2][verification done-count int32, pad]
+            off_cnt = 16 * nl
+            self.scratch = t.zeros(off_cnt + 16, dtype=t.uint8, device="cuda")
+            self.sums = self.scratch[:off_cnt].view(t.float64).view(nl, 2)
+            self.counters = self.scratch[off_cnt:off_cnt + 8].view(t.int32)   # [fired thread tiles, flagged layers]
+            self.vdone = self.scratch[off_cnt + 8:off_cnt + 12].view(t.int32)
+        else:
+            self.scratch = None
+            self.sums, self.counters, self.vdone = self.shared
         self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
         self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
         self._ks_all = t.tensor([L.k for L in self.layers], dtype=t.int32, device="cuda")
@@ -124,13 +135,14 @@ class ProtectedChain:
         """Enqueue one protected forward (no host sync); returns the last activation tensor."""
         if x is not None:
             self.x.copy_(x, non_blocking=True)
-        kernels.zero(self.scratch)
+        if self.scratch is not None:
+            kernels.zero(self.scratch)
         a = self.x
         last = len(self.layers) - 1
         for i, L in enumerate(self.layers):
             kw = self._gemm_kwargs(i, L)
-            kw["pdl"] = i > 0 and self.pdl       # layer i's prologue overlaps layer i-1
-            if i == last and self.global_ids:
+            kw["pdl"] = i > 0 and self.pdl and not _NO_PDL      # layer i's prologue overlaps layer i-1
+            if i == last and self.global_ids and self.shared is None:
                 # deferred verification of every layer's (lhs, rhs), fused into the last layer's
                 # launch (its last CTA); layers without the global scheme hold (0, 0), never flag
                 kw["verify"] = (self.sums, self._ks_all, self.vdone, self.verdict_buf, self.counters[1:2])
@@ -181,3 +193,56 @@ class GraphedForward:
 
     def replay(self):
         self.graph.replay()
+
+
+class ChainGroup:
+    """Independent chains (e.g. the requests of one serving step) sharing one accumulator block:
+    ONE memset clears every member's (lhs, rhs) sums and counters, the members run their
+    layers (on any streams), and ONE launch then forms the verdicts of every global layer of
+    every member — the reference's deferred verification (checksum.py:207-211) batched across
+    the group, instead of a done-count round trip at the end of each member's last kernel."""
+
+    def __init__(self, specs, **chain_kw):
+        """specs: [(weights, batch, schemes)]; chain_kw: ProtectedChain fields shared by all."""
+        t = D.torch()
+        nls = [len(w) for w, _, _ in specs]
+        total = sum(nls)
+        off_cnt = 16 * total
+        self.block = t.zeros(off_cnt + 16 * len(specs), dtype=t.uint8, device="cuda")
+        self.sums = self.block[:off_cnt].view(t.float64).view(total, 2)
+        cnt = self.block[off_cnt:].view(t.int32).view(len(specs), 4)
+        self.chains = []
+        o = 0
+        for (w, b, sch), nl in zip(specs, nls):
+            self.chains.append(ProtectedChain(w, b, sch, shared=(self.sums[o:o + nl], cnt[len(self.chains), 0:2],
+                                                                 cnt[len(self.chains), 2:3]), **chain_kw))
+            o += nl
+        self.counters = cnt
+        ks = [L.k for ch in self.chains for L in ch.layers]
+        self.has_global = any(ch.global_ids for ch in self.chains)
+        self.ks = t.tensor(ks, dtype=t.int32, device="cuda")
+        self.verdicts = t.zeros(total * 32, dtype=t.uint8, device="cuda")
+        self.flagged = t.zeros(1, dtype=t.int32, device="cuda")
+        self.numeric = self.chains[0].numeric
+
+    def begin(self) -> None:
+        """Clear every member's per-forward accumulators (one memset)."""
+        kernels.zero(self.block)
+        kernels.zero(self.flagged)
+
+    def end(self) -> None:
+        """One verification launch over all members' layers (non-global layers hold (0, 0))."""
+        if self.has_global:
+            kernels.verify_sums(self.sums, self.ks, self.ks.numel(), self.numeric, out=self.verdicts,
+                                detected_count=self.flagged)
+
+    def forward(self) -> None:
+        self.begin()
+        for ch in self.chains:
+            ch.forward()
+        self.end()
+
+    def flags(self) -> tuple:
+        """(fired thread tiles over all members, flagged global layers over all members)."""
+        c = self.counters.cpu()
+        return int(c[:, 0].sum()), int(self.flagged.item())

@@ -115,3 +115,47 @@ def test_sharded_partials_reduce_to_full_batch_verdict(P):
     assert torch.equal(red, full.global_partials())
     vs = sharding.verdicts_from_sums(red.cpu(), [16, 512, 256], P.EXACT_INT)
     assert not any(v.detected for v in vs)
+
+
+def test_chain_group_batched_verification_matches_members(P):
+    """A ChainGroup (one memset, members on their own streams, ONE verification launch) gives
+    the same per-layer verdict values as each member's fused deferred verification, counts the
+    flagged global layers of all members, and the fired thread tiles."""
+    import torch
+    from paper_2104_09455_b200.network import ChainGroup, ProtectedChain
+    ws = _weights(True)
+    wt = [torch.from_numpy(w.astype(np.float16)).cuda() for w in ws]
+    S = P.Scheme
+    specs = [(wt, 1, [S.GLOBAL_ABFT] * 3), (wt, 64, [S.GLOBAL_ABFT, S.THREAD_ONE_SIDED, S.GLOBAL_ABFT]),
+             (wt, 300, [S.UNPROTECTED, S.GLOBAL_ABFT, S.THREAD_ONE_SIDED])]
+    faults = [None, {0: [(5, 3, 9.0)], 1: [(60, 100, 7.0)]}, {1: [(299, 2, 5.0)]}]
+    rng = np.random.default_rng(3)
+    xs = [torch.from_numpy(rng.integers(-2, 3, size=(b, DIMS[0])).astype(np.float16)).cuda() for _, b, _ in specs]
+    grp = ChainGroup([(w, b, s) for (w, b, s) in specs], dtype=P.EXACT_INT)
+    for ch, f, x in zip(grp.chains, faults, xs):
+        ch.faults = f
+        ch._fault_dev = {int(i): P.device.faults_tensor(list(v)) for i, v in (f or {}).items()}
+        ch.x.copy_(x)
+    for _ in range(2):                        # replayable: the accumulators are cleared each time
+        grp.forward()
+        torch.cuda.synchronize()
+    raw = grp.verdicts.cpu().numpy().view(np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"),
+                                                   ("det", "<i4"), ("k", "<i4")]))
+    o = 0
+    n_global_flagged = 0
+    for (w, b, sch), f, x in zip(specs, faults, xs):
+        solo = ProtectedChain(w, b, sch, P.EXACT_INT, faults=f)
+        solo.forward(x)
+        torch.cuda.synchronize()
+        sv = _verdicts(solo)
+        for i in range(3):
+            if sch[i] is S.GLOBAL_ABFT:
+                assert (raw[o + i]["lhs"], raw[o + i]["rhs"], raw[o + i]["det"]) == \
+                    (sv[i]["lhs"], sv[i]["rhs"], sv[i]["det"]), (b, i)
+                n_global_flagged += int(sv[i]["det"])
+            else:
+                assert raw[o + i]["det"] == 0
+        o += 3
+    fired, flagged = grp.flags()
+    assert flagged == n_global_flagged == 2
+    assert fired == 1                          # the one thread-level fault, one tile

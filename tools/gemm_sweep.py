@@ -75,7 +75,12 @@ def stamps(m, n, k):
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     buf = (ctypes.c_ulonglong * (160 * 8))()
-    for name, sch, kw in [("unprot", P.Scheme.UNPROTECTED, {}),
+    osum = torch.zeros(2, dtype=torch.float64, device="cuda")
+    gk = dict(out_sum=osum[1:2], out_lhs=osum[0:1])
+    gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True,
+                         ck_layout=1, out=out, ldc=n, out_kind="f16", relu=True, **gk)
+    gk["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
+    for name, sch, kw in [("unprot", P.Scheme.UNPROTECTED, {}), ("global", P.Scheme.GLOBAL_ABFT, gk),
                           ("onesided", P.Scheme.THREAD_ONE_SIDED,
                            dict(m_ext=-(-m // 16) * 16, n_ext=n, fired_count=cnt))]:
         for _ in range(3):
@@ -95,6 +100,10 @@ def stamps(m, n, k):
 if __name__ == "__main__":
     if "--stamps" in sys.argv:
         stamps(2048, 512, 512)
-        stamps(256, 256, 256)
+        stamps(2048, 512, 16)
+        stamps(64, 512, 16)
+        stamps(2048, 256, 512)
+        if "--only-stamps" in sys.argv:
+            sys.exit(0)
     for s in SHAPES:
         run(*s)
