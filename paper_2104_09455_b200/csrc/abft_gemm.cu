@@ -50,6 +50,7 @@ enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
 
 // bring-up instrumentation (ABFT_DEBUG & 2048): per-CTA %globaltimer stamps
 __device__ unsigned long long g_dbg_ts[160][8];
+__device__ unsigned long long g_dbg_kb[3][64];   // CTA 0, first tile: [0] load issued, [1] full seen by MMA, [2] empty seen
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -418,10 +419,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // the whole warp runs the loop (warp-uniform state); one elected lane issues ("_w" calls)
+    {
       // the operands may be the previous kernel's outputs: wait for its completion (no-op
       // unless launched as a programmatic dependent)
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (stamp && lane == 0 && blockIdx.x == 0) g_dbg_kb[2][63] = gtimer();
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b) +
@@ -429,15 +432,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (b_res && blockIdx.x < p.num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
-        ptx::mbar_arrive_expect_tx(bres, (uint32_t)p.nkb * (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b);
+        ptx::mbar_arrive_expect_tx_w(bres, (uint32_t)p.nkb * (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b);
         for (int kb = 0; kb < p.nkb; ++kb) {
           if (halo) {
             const int r = kb / p.cv_chunks, cc = kb - (kb / p.cv_chunks) * p.cv_chunks;
             for (int si = 0; si < p.cv_S; ++si)
-              ptx::tma_load_2d(sm_b + kb * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, bres,
+              ptx::tma_load_2d_w(sm_b + kb * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, bres,
                                (r * p.cv_S + si) * p.cv_kstride + cc * BK, 0);
           } else {
-            ptx::tma_load_2d(sm_b + kb * p.stage_b_bytes, &tmB, bres, kb * BK, 0);
+            ptx::tma_load_2d_w(sm_b + kb * p.stage_b_bytes, &tmB, bres, kb * BK, 0);
           }
         }
       }
@@ -461,7 +464,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], txt);
+          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[2][kb] = gtimer();
+          ptx::mbar_arrive_expect_tx_w(&full[s], txt);
           uint8_t* a_dst = sm_a + s * p.stage_a_bytes;
           uint8_t* w_dst = smem + p.off_w + s * p.stage_w_bytes;
           if (halo) {
@@ -469,35 +473,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int r = kb / p.cv_chunks;
             const int cc = kb - r * p.cv_chunks;
             if (p.debug & 4194304)
-              ptx::tma_load_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
+              ptx::tma_load_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
             else   // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
-              ptx::tma_load_im2col_4d(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
+              ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
             const int brow = ck_aug ? nb * p.b_rows_blk : n0;
             if (w_tile) {
 #pragma unroll 1
               for (int si = 0; si < p.cv_S; ++si)
-                ptx::bulk_load(w_dst + si * 256, p.lhs_w + (r * p.cv_S + si) * p.cv_kstride + cc * BK, 256u, &full[s]);
+                ptx::bulk_load_w(w_dst + si * 256, p.lhs_w + (r * p.cv_S + si) * p.cv_kstride + cc * BK, 256u, &full[s]);
             }
             if (!b_res) {
 #pragma unroll 1
               for (int si = 0; si < p.cv_S; ++si) {
                 uint8_t* bdst = sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes;
                 const int kx = (r * p.cv_S + si) * p.cv_kstride + cc * BK;
-                ptx::tma_load_2d(bdst, &tmB, &full[s], kx, brow);
+                ptx::tma_load_2d_w(bdst, &tmB, &full[s], kx, brow);
                 if (ck_loaded)
-                  ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes + si * p.nck_pad * 128, &tmCK, &full[s], kx,
+                  ptx::tma_load_2d_w(sm_ck + s * p.stage_ck_bytes + si * p.nck_pad * 128, &tmCK, &full[s], kx,
                                    nb * p.ck_rstride + p.ck_roff);
               }
             }
             if (++s == p.stages) { s = 0; ph ^= 1; }
             continue;
           } else if (p.a_mode == 0) {
-            ptx::tma_load_2d(a_dst, &tmA, &full[s], kb * BK, m0);
+            ptx::tma_load_2d_w(a_dst, &tmA, &full[s], kb * BK, m0);
           } else if (p.a_mode == 1) {
             const int tap = kb / p.cv_chunks;
             const int c0 = (kb - tap * p.cv_chunks) * BK;
             const int r = tap / p.cv_S;
-            ptx::tma_load_im2col_4d(a_dst, &tmA, &full[s], c0, wo, ho, img, (uint16_t)(tap - r * p.cv_S), (uint16_t)r);
+            ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], c0, wo, ho, img, (uint16_t)(tap - r * p.cv_S), (uint16_t)r);
           } else {
 #pragma unroll 1
             for (int j = 0; j < 8; ++j) {
@@ -509,13 +513,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 r = tap / p.cv_S;
                 sx = tap - r * p.cv_S;
               }
-              ptx::tma_load_im2col_4d(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
+              ptx::tma_load_im2col_4d_w(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
             }
           }
-          ptx::tma_load_2d(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
-          if (w_tile) ptx::bulk_load(w_dst, p.lhs_w + kb * BK, 256u, &full[s]);
+          ptx::tma_load_2d_w(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
+          if (w_tile) ptx::bulk_load_w(w_dst, p.lhs_w + kb * BK, 256u, &full[s]);
           if (ck_loaded)
-            ptx::tma_load_2d(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.ck_rstride + p.ck_roff);
+            ptx::tma_load_2d_w(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.ck_rstride + p.ck_roff);
+          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[0][kb] = gtimer();
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
       }
@@ -530,8 +535,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     : ptx::desc_kmajor_sw128(base + (uint32_t)k * 32u);
     };
     // The checksum N-slice of a stage generated on chip is issued one stage late, so the
-    // main MMAs never wait for the checksum warps.
-    if (lane == 0) {
+    // main MMAs never wait for the checksum warps.  Whole-warp loop, elected-lane issue.
+    // Descriptor bases of stage 0; a stage / k-step adds a constant to the address field
+    // (smem byte address >> 4, 14 bits, never carries for addresses below 256 KB).
+    const bool fast = !halo && !ck_onchip && !has_shadow && p.acolck_mode != 1 && !(p.debug & 4);
+    const uint64_t a_base = a_none ? ptx::desc_kmajor_none(ptx::smem_u32(sm_a), 2048u, 128u)
+                                   : ptx::desc_kmajor_sw128(ptx::smem_u32(sm_a));
+    const uint64_t a_kstep = a_none ? 256ull : 2ull;
+    const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4, c_sstep = p.stage_ck_bytes >> 4;
+    const uint64_t b_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_b));
+    const uint64_t c_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_ck));
+    const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
+    {
       int s = 0, ps = 0;
       uint32_t ph = 0, pph = 0;
       int db = 0;
@@ -545,9 +560,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.cols_per_acc);
+        if (fast) {
+          // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
+#pragma unroll 1
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            ptx::mbar_wait(&full[s], ph);
+            if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
+            ptx::tc_fence_after();
+            const uint64_t ad = a_base + (uint64_t)s * a_sstep;
+            const uint64_t bd = b_base + (uint64_t)s * b_sstep;
+            const uint64_t cd = c_base + (uint64_t)s * c_sstep;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t accum = (kb | k) != 0;
+              ptx::mma_f16_ss_w(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
+              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, p.idesc_ck, accum);
+            }
+            ptx::mma_commit_w(&empty[s]);
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+          }
+          ptx::mma_commit_w(&tfull[acc]);
+          continue;
+        }
 #pragma unroll 1
         for (int kb = 0; kb < p.nkb; ++kb) {
           ptx::mbar_wait(&full[s], ph);
+          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
           const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * p.stage_b_bytes);
@@ -564,14 +602,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t bt_addr = b_addr + (uint32_t)si * p.b_tile_bytes;
                 const uint64_t bdesc = ptx::desc_kmajor_sw128(bt_addr + k * 32);
                 const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
-                ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
+                ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
                 if (ck_loaded)
-                  ptx::mma_f16_ss(d + bn, adesc,
+                  ptx::mma_f16_ss_w(d + bn, adesc,
                                   ptx::desc_kmajor_sw128(c_addr + (uint32_t)(si * p.nck_pad * 128) + k * 32),
                                   p.idesc_ck, accum);
               }
             }
-            ptx::mma_commit(&empty[s]);
+            ptx::mma_commit_w(&empty[s]);
             if (++s == p.stages) { s = 0; ph ^= 1; }
             continue;
           }
@@ -580,9 +618,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t adesc = a_desc(a_addr, k);
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
-            ptx::mma_f16_ss(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
-            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
-            if (has_shadow) ptx::mma_f16_ss(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
+            ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
+            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss_w(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
+            if (has_shadow) ptx::mma_f16_ss_w(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
           }
           if (p.acolck_mode == 1 && count_tile) {
             // colck[kb*64 + j] += sum_rows A_tile[row][j] on the tensor cores:
@@ -595,9 +633,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int r = 0; r < BM / 16; ++r) {
               const uint64_t adesc2 = a_none ? ptx::desc_mnmajor_none(a_addr + r * 256, 128, 2048)
                                              : ptx::desc_mnmajor_sw128(a_addr + r * 2048, 1024);
-              ptx::mma_f16_ss(dd, adesc2, odesc, p.idesc_ones, r > 0 ? 1u : 0u);
+              ptx::mma_f16_ss_w(dd, adesc2, odesc, p.idesc_ones, r > 0 ? 1u : 0u);
             }
-            ptx::mma_commit(&dfull[db]);
+            ptx::mma_commit_w(&dfull[db]);
             if (++db == DCK_BUFS) { db = 0; dph ^= 1; }
           }
           if (ck_onchip) {
@@ -609,13 +647,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
-                ptx::mma_f16_ss(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
+                ptx::mma_f16_ss_w(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
                                 p.idesc_ck, (kb - 1 > 0 || k > 0) ? 1u : 0u);
-              ptx::mma_commit(&empty[ps]);
+              ptx::mma_commit_w(&empty[ps]);
             }
             ps = s; pph = ph;
           } else {
-            ptx::mma_commit(&empty[s]);
+            ptx::mma_commit_w(&empty[s]);
           }
           if (++s == p.stages) { s = 0; ph ^= 1; }
         }
@@ -626,11 +664,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            ptx::mma_f16_ss(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
+            ptx::mma_f16_ss_w(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
                             p.idesc_ck, (p.nkb - 1 > 0 || k > 0) ? 1u : 0u);
-          ptx::mma_commit(&empty[ps]);
+          ptx::mma_commit_w(&empty[ps]);
         }
-        ptx::mma_commit(&tfull[acc]);
+        ptx::mma_commit_w(&tfull[acc]);
       }
     }
   } else if (warp >= CK_WARP0) {
@@ -927,14 +965,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
 
-      if (p.gck && h == 0 && !(p.debug & 524288)) {
-        // global lhs: this row's A . rowck(B tile) = checksum column hi + lo
-        float ck_hi, ck_lo;
-        __syncwarp();
-        ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
-        ptx::tmem_ld_wait();
-        if (row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
-      }
+      // global lhs: this row's A . rowck(B tile) = checksum column hi + lo, loaded with the
+      // h = 0 warps' first chunk (one TMEM load wait)
+      const bool gck_ld = p.gck && h == 0 && !(p.debug & 524288);
+      float ck_hi = 0.f, ck_lo = 0.f;
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
       const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
       uint32_t fmask = 0;
@@ -949,6 +983,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float v[32], sh[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
+        if (gck_ld && c0 == c_first) ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
         if constexpr (has_shadow) ptx::tmem_ld32(tacc + p.shadow_off + c0, sh);
         // static group width: this chunk's checksum columns straight from TMEM (hi, then lo)
         constexpr int GPCK = NT > 0 ? 32 / NT : 1;
@@ -958,6 +993,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (p.split) ptx::tmem_ldn<GPCK>(tacc + bn + p.groups + c0 / NT, ckl);
         }
         ptx::tmem_ld_wait();
+        if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
         if (stamp && et == 0 && t_local == 0 && c0 == 0) g_dbg_ts[blockIdx.x][5] = gtimer();
         const int gc0 = n0 + c0;
         const int cmax = p.bn_eff - c0;
@@ -1183,11 +1219,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (lane == 0) { red_d[et >> 5] = x; red_d[8 + (et >> 5)] = y; }
       ptx::named_bar_sync(3, 256);
-      if (et == 0) {
-        double tx = 0.0, ty = 0.0;
-        for (int w = 0; w < 8; ++w) { tx += red_d[w]; ty += red_d[8 + w]; }
-        if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
-        if (p.gck) atomicAdd(p.out_lhs, ty);
+      if (et < 32) {
+        // the first epilogue warp folds the 8 warp partials (lanes 0-7) and adds them once
+        double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
+#pragma unroll
+        for (int o = 4; o >= 1; o >>= 1) {
+          tx += __shfl_xor_sync(0xffffffffu, tx, o);
+          ty += __shfl_xor_sync(0xffffffffu, ty, o);
+        }
+        if (lane == 0) {
+          if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
+          if (p.gck) atomicAdd(p.out_lhs, ty);
+        }
       }
     }
     // the staging buffers must stay valid until the bulk stores have READ them; the writes
@@ -1727,8 +1770,10 @@ extern "C" __attribute__((visibility("default"))) int abft_aug_weights(const voi
   return cuda_check(cudaGetLastError(), "aug_weights launch");
 }
 
-extern "C" __attribute__((visibility("default"))) int abft_debug_timestamps(unsigned long long* host_out /*[160*8]*/) {
-  return cuda_check(cudaMemcpyFromSymbol(host_out, g_dbg_ts, sizeof(g_dbg_ts)), "debug timestamps");
+extern "C" __attribute__((visibility("default"))) int abft_debug_timestamps(unsigned long long* host_out /*[160*8 + 3*64]*/) {
+  int rc = cuda_check(cudaMemcpyFromSymbol(host_out, g_dbg_ts, sizeof(g_dbg_ts)), "debug timestamps");
+  if (rc != ABFT_OK) return rc;
+  return cuda_check(cudaMemcpyFromSymbol(host_out + 160 * 8, g_dbg_kb, sizeof(g_dbg_kb)), "debug timestamps");
 }
 
 extern "C" __attribute__((visibility("default"))) int abft_gemm_plan(const abft_gemm_args_t* a, int32_t* out) {

@@ -213,6 +213,67 @@ __host__ __device__ __forceinline__ uint32_t idesc_f16(uint32_t ab_fmt, uint32_t
   return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
+// ---------------------------------------------------------------------------------------
+// Warp-collective issue (the "_w" forms): every lane of the warp executes the call with the
+// same (warp-uniform) operands and one elected lane issues the instruction.  Running the
+// producer / MMA loops on the whole warp keeps their addresses and coordinates in uniform
+// registers; a loop confined to lane 0 makes ptxas wrap every TMA / MMA operand in a
+// per-instruction uniformity loop (ELECT / R2UR.BROADCAST / BRA.U.ANY).
+#define ABFT_ELECT_PRED "elect.sync _|P, 0xffffffff;\n\t"
+__device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_w(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                              int32_t c1) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+               "[%2];\n\t}" ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_w(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                              int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+               "%5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_4d_w(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c,
+                                                     int32_t w, int32_t h, int32_t n, uint16_t off_w,
+                                                     uint16_t off_h) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n\t}" ::"r"(smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+               "h"(off_w), "h"(off_h)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_w(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::
+                   "r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma_f16_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile("{\n\t.reg .pred P;\n\t.reg .pred p;\n\t" ABFT_ELECT_PRED
+               "setp.ne.b32 p, %4, 0;\n\t"
+               "@P tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+               "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+               : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
+               "@P tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -74,7 +74,7 @@ def stamps(m, n, k):
     pw = D.prepare_weight(b, P.BINARY16)
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-    buf = (ctypes.c_ulonglong * (160 * 8))()
+    buf = (ctypes.c_ulonglong * (160 * 8 + 3 * 64))()
     osum = torch.zeros(2, dtype=torch.float64, device="cuda")
     gk = dict(out_sum=osum[1:2], out_lhs=osum[0:1])
     gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True,
@@ -88,7 +88,14 @@ def stamps(m, n, k):
                          relu=True, **kw)
             torch.cuda.synchronize()
         lib.abft_debug_timestamps(buf)
-        ts = np.frombuffer(buf, dtype=np.uint64).reshape(160, 8).astype(np.int64)
+        allts = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+        ts = allts[:160 * 8].reshape(160, 8)
+        kbt = allts[160 * 8:].reshape(3, 64)
+        nkb = min(64, -(-k // 64))
+        t00 = ts[0, 0]
+        print(f"  cta0 per-kb (ns from entry): issued {(kbt[0, :nkb] - t00).tolist()}", flush=True)
+        print(f"  cta0 per-kb full seen by MMA {(kbt[1, :nkb] - t00).tolist()}", flush=True)
+        print(f"  cta0 per-kb empty passed     {(kbt[2, :nkb] - t00).tolist()} after griddep.wait {kbt[2, 63] - t00}", flush=True)
         nct = min(160, int((ts[:, 0] > 0).sum()))
         ts = ts[:nct]
         rel = ts[:, :7] - ts[:, 0].min()
@@ -100,9 +107,8 @@ def stamps(m, n, k):
 if __name__ == "__main__":
     if "--stamps" in sys.argv:
         stamps(2048, 512, 512)
+        stamps(128, 64, 512)
         stamps(2048, 512, 16)
-        stamps(64, 512, 16)
-        stamps(2048, 256, 512)
         if "--only-stamps" in sys.argv:
             sys.exit(0)
     for s in SHAPES:
