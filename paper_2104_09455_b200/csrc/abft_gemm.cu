@@ -357,6 +357,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  {
+    // warm the constant cache with every 64-byte line of the parameter block in parallel
+    // (one load per thread) instead of a chain of dependent misses in each role's prologue
+    constexpr int kLines = (int)((sizeof(GemmParams) + 63) / 64);
+    if (threadIdx.x < kLines) {
+      const uint32_t x = reinterpret_cast<const uint32_t*>(&p)[threadIdx.x * 16];
+      if (x == 0x9E3779B9u && p.debug == 0x7fffffff) g_dbg_ts[0][7] = x;   // keeps the load (never true)
+    }
+  }
   constexpr bool has_ck = CLASS == CLASS_CHECKSUM;
   constexpr bool has_shadow = CLASS == CLASS_REPLICA;
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
@@ -419,6 +428,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+    // loop-invariant parameters in registers (the asm memory clobbers would otherwise reload them)
+    const auto L_a_mode = p.a_mode;
+    const auto L_b_rows_blk = p.b_rows_blk;
+    const auto L_b_tile_bytes = p.b_tile_bytes;
+    const auto L_bm_eff = p.bm_eff;
+    const auto L_bn_eff = p.bn_eff;
+    const auto L_ck_roff = p.ck_roff;
+    const auto L_ck_rstride = p.ck_rstride;
+    const auto L_cv_chunks = p.cv_chunks;
+    const auto L_cv_kstride = p.cv_kstride;
+    const auto L_cv_S = p.cv_S;
+    const auto L_nck_pad = p.nck_pad;
+    const auto L_nkb = p.nkb;
+    const auto L_num_n_blocks = p.num_n_blocks;
+    const auto L_num_tiles = p.num_tiles;
+    const auto L_stage_a_bytes = p.stage_a_bytes;
+    const auto L_stage_b_bytes = p.stage_b_bytes;
+    const auto L_stage_ck_bytes = p.stage_ck_bytes;
+    const auto L_stage_w_bytes = p.stage_w_bytes;
+    const auto L_stages = p.stages;
+    const auto L_tx_b = p.tx_b;
+    const auto L_cv_P = p.cv_P;
+    const auto L_cv_Q = p.cv_Q;
     // the whole warp runs the loop (warp-uniform state); one elected lane issues ("_w" calls)
     {
       // the operands may be the previous kernel's outputs: wait for its completion (no-op
@@ -427,109 +459,126 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (stamp && lane == 0 && blockIdx.x == 0) g_dbg_kb[2][63] = gtimer();
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = (halo ? p.tx_a : p.stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b) +
-                          (ck_loaded ? (halo ? (uint32_t)p.cv_S : 1u) * (uint32_t)p.nck_pad * 128u : 0u);
-      if (b_res && blockIdx.x < p.num_tiles) {
+      const uint32_t tx = (halo ? p.tx_a : L_stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)L_cv_S : 1u) * L_tx_b) +
+                          (ck_loaded ? (halo ? (uint32_t)L_cv_S : 1u) * (uint32_t)L_nck_pad * 128u : 0u);
+      if (b_res && blockIdx.x < L_num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
-        ptx::mbar_arrive_expect_tx_w(bres, (uint32_t)p.nkb * (halo ? (uint32_t)p.cv_S : 1u) * p.tx_b);
-        for (int kb = 0; kb < p.nkb; ++kb) {
+        ptx::mbar_arrive_expect_tx_w(bres, (uint32_t)L_nkb * (halo ? (uint32_t)L_cv_S : 1u) * L_tx_b);
+        for (int kb = 0; kb < L_nkb; ++kb) {
           if (halo) {
-            const int r = kb / p.cv_chunks, cc = kb - (kb / p.cv_chunks) * p.cv_chunks;
-            for (int si = 0; si < p.cv_S; ++si)
-              ptx::tma_load_2d_w(sm_b + kb * p.stage_b_bytes + si * p.b_tile_bytes, &tmB, bres,
-                               (r * p.cv_S + si) * p.cv_kstride + cc * BK, 0);
+            const int r = kb / L_cv_chunks, cc = kb - (kb / L_cv_chunks) * L_cv_chunks;
+            for (int si = 0; si < L_cv_S; ++si)
+              ptx::tma_load_2d_w(sm_b + kb * L_stage_b_bytes + si * L_b_tile_bytes, &tmB, bres,
+                               (r * L_cv_S + si) * L_cv_kstride + cc * BK, 0);
           } else {
-            ptx::tma_load_2d_w(sm_b + kb * p.stage_b_bytes, &tmB, bres, kb * BK, 0);
+            ptx::tma_load_2d_w(sm_b + kb * L_stage_b_bytes, &tmB, bres, kb * BK, 0);
           }
         }
       }
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int nb = tile % p.num_n_blocks;
-        const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
-        const int n0 = nb * p.bn_eff;
+      for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x) {
+        const int nb = tile % L_num_n_blocks;
+        const int m0 = (tile / L_num_n_blocks) * L_bm_eff;
+        const int n0 = nb * L_bn_eff;
         // global lhs dot: the tile row's first N block also brings each k-block's rowck(B) slice
         const bool w_tile = p.lhs_w != nullptr && nb == 0;
-        const uint32_t txt = tx + (w_tile ? p.stage_w_bytes : 0u);
+        const uint32_t txt = tx + (w_tile ? L_stage_w_bytes : 0u);
         // conv: window origin of the tile's first output pixel (the TMA walks the next 127)
         int img = 0, wo = 0, ho = 0;
-        if (p.a_mode != 0) {
-          const int pq = p.cv_P * p.cv_Q;
+        if (L_a_mode != 0) {
+          const int pq = L_cv_P * L_cv_Q;
           img = m0 / pq;
           const int rem = m0 - img * pq;
-          const int pp = rem / p.cv_Q;
+          const int pp = rem / L_cv_Q;
           ho = pp * p.cv_sh - p.cv_ph;
-          wo = (rem - pp * p.cv_Q) * p.cv_sw - p.cv_pw;
+          wo = (rem - pp * L_cv_Q) * p.cv_sw - p.cv_pw;
         }
 #pragma unroll 1
-        for (int kb = 0; kb < p.nkb; ++kb) {
+        for (int kb = 0; kb < L_nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[2][kb] = gtimer();
           ptx::mbar_arrive_expect_tx_w(&full[s], txt);
-          uint8_t* a_dst = sm_a + s * p.stage_a_bytes;
-          uint8_t* w_dst = smem + p.off_w + s * p.stage_w_bytes;
+          uint8_t* a_dst = sm_a + s * L_stage_a_bytes;
+          uint8_t* w_dst = smem + p.off_w + s * L_stage_w_bytes;
           if (halo) {
             // window of input row (p + r - pad), columns q0 - pad .. q0 - pad + Qt + S - 2
-            const int r = kb / p.cv_chunks;
-            const int cc = kb - r * p.cv_chunks;
+            const int r = kb / L_cv_chunks;
+            const int cc = kb - r * L_cv_chunks;
             if (p.debug & 4194304)
               ptx::tma_load_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
             else   // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
               ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
-            const int brow = ck_aug ? nb * p.b_rows_blk : n0;
+            const int brow = ck_aug ? nb * L_b_rows_blk : n0;
             if (w_tile) {
 #pragma unroll 1
-              for (int si = 0; si < p.cv_S; ++si)
-                ptx::bulk_load_w(w_dst + si * 256, p.lhs_w + (r * p.cv_S + si) * p.cv_kstride + cc * BK, 256u, &full[s]);
+              for (int si = 0; si < L_cv_S; ++si)
+                ptx::bulk_load_w(w_dst + si * 256, p.lhs_w + (r * L_cv_S + si) * L_cv_kstride + cc * BK, 256u, &full[s]);
             }
             if (!b_res) {
 #pragma unroll 1
-              for (int si = 0; si < p.cv_S; ++si) {
-                uint8_t* bdst = sm_b + s * p.stage_b_bytes + si * p.b_tile_bytes;
-                const int kx = (r * p.cv_S + si) * p.cv_kstride + cc * BK;
+              for (int si = 0; si < L_cv_S; ++si) {
+                uint8_t* bdst = sm_b + s * L_stage_b_bytes + si * L_b_tile_bytes;
+                const int kx = (r * L_cv_S + si) * L_cv_kstride + cc * BK;
                 ptx::tma_load_2d_w(bdst, &tmB, &full[s], kx, brow);
                 if (ck_loaded)
-                  ptx::tma_load_2d_w(sm_ck + s * p.stage_ck_bytes + si * p.nck_pad * 128, &tmCK, &full[s], kx,
-                                   nb * p.ck_rstride + p.ck_roff);
+                  ptx::tma_load_2d_w(sm_ck + s * L_stage_ck_bytes + si * L_nck_pad * 128, &tmCK, &full[s], kx,
+                                   nb * L_ck_rstride + L_ck_roff);
               }
             }
-            if (++s == p.stages) { s = 0; ph ^= 1; }
+            if (++s == L_stages) { s = 0; ph ^= 1; }
             continue;
-          } else if (p.a_mode == 0) {
+          } else if (L_a_mode == 0) {
             ptx::tma_load_2d_w(a_dst, &tmA, &full[s], kb * BK, m0);
-          } else if (p.a_mode == 1) {
-            const int tap = kb / p.cv_chunks;
-            const int c0 = (kb - tap * p.cv_chunks) * BK;
-            const int r = tap / p.cv_S;
-            ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], c0, wo, ho, img, (uint16_t)(tap - r * p.cv_S), (uint16_t)r);
+          } else if (L_a_mode == 1) {
+            const int tap = kb / L_cv_chunks;
+            const int c0 = (kb - tap * L_cv_chunks) * BK;
+            const int r = tap / L_cv_S;
+            ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], c0, wo, ho, img, (uint16_t)(tap - r * L_cv_S), (uint16_t)r);
           } else {
 #pragma unroll 1
             for (int j = 0; j < 8; ++j) {
               const int pair = kb * 8 + j;
               int c0 = p.cv_c, r = 0, sx = 0;      // past the last pair: a fully out-of-bounds (zero) column
               if (pair < p.cv_pairs) {
-                const int tap = pair / p.cv_chunks;
-                c0 = (pair - tap * p.cv_chunks) * 8;
-                r = tap / p.cv_S;
-                sx = tap - r * p.cv_S;
+                const int tap = pair / L_cv_chunks;
+                c0 = (pair - tap * L_cv_chunks) * 8;
+                r = tap / L_cv_S;
+                sx = tap - r * L_cv_S;
               }
               ptx::tma_load_im2col_4d_w(a_dst + j * 2048, &tmA, &full[s], c0, wo, ho, img, (uint16_t)sx, (uint16_t)r);
             }
           }
-          ptx::tma_load_2d_w(sm_b + s * p.stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * p.b_rows_blk : n0);
+          ptx::tma_load_2d_w(sm_b + s * L_stage_b_bytes, &tmB, &full[s], kb * BK, ck_aug ? nb * L_b_rows_blk : n0);
           if (w_tile) ptx::bulk_load_w(w_dst, p.lhs_w + kb * BK, 256u, &full[s]);
           if (ck_loaded)
-            ptx::tma_load_2d_w(sm_ck + s * p.stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * p.ck_rstride + p.ck_roff);
+            ptx::tma_load_2d_w(sm_ck + s * L_stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * L_ck_rstride + L_ck_roff);
           if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[0][kb] = gtimer();
-          if (++s == p.stages) { s = 0; ph ^= 1; }
+          if (++s == L_stages) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
+    // loop-invariant parameters in registers (the asm memory clobbers would otherwise reload them)
+    const auto L_a_mode = p.a_mode;
+    const auto L_acc_stages = p.acc_stages;
+    const auto L_b_tile_bytes = p.b_tile_bytes;
+    const auto L_cols_per_acc = p.cols_per_acc;
+    const auto L_cv_S = p.cv_S;
+    const auto L_idesc_aug = p.idesc_aug;
+    const auto L_idesc_ck = p.idesc_ck;
+    const auto L_idesc_main = p.idesc_main;
+    const auto L_nck_pad = p.nck_pad;
+    const auto L_nkb = p.nkb;
+    const auto L_num_n_blocks = p.num_n_blocks;
+    const auto L_num_tiles = p.num_tiles;
+    const auto L_stage_a_bytes = p.stage_a_bytes;
+    const auto L_stage_b_bytes = p.stage_b_bytes;
+    const auto L_stage_ck_bytes = p.stage_ck_bytes;
+    const auto L_stages = p.stages;
     // A operand of MMA k-step k (16 K elements): SW128 rows, or for 8-channel im2col
     // columns two 2 KB [128 x 16 B] boxes, LBO = 2 KB apart
-    const bool a_none = p.a_mode == 2;
+    const bool a_none = L_a_mode == 2;
     auto a_desc = [a_none](uint32_t base, int k) -> uint64_t {
       return a_none ? ptx::desc_kmajor_none(base + (uint32_t)k * 4096u, 2048u, 128u)
                     : ptx::desc_kmajor_sw128(base + (uint32_t)k * 32u);
@@ -542,28 +591,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint64_t a_base = a_none ? ptx::desc_kmajor_none(ptx::smem_u32(sm_a), 2048u, 128u)
                                    : ptx::desc_kmajor_sw128(ptx::smem_u32(sm_a));
     const uint64_t a_kstep = a_none ? 256ull : 2ull;
-    const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4, c_sstep = p.stage_ck_bytes >> 4;
+    const uint64_t a_sstep = L_stage_a_bytes >> 4, b_sstep = L_stage_b_bytes >> 4, c_sstep = L_stage_ck_bytes >> 4;
     const uint64_t b_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_b));
     const uint64_t c_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_ck));
-    const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
+    const uint32_t idesc_m = ck_aug ? L_idesc_aug : L_idesc_main;
     {
       int s = 0, ps = 0;
       uint32_t ph = 0, pph = 0;
       int db = 0;
       uint32_t dph = 0;
       int t_local = 0;
-      if (b_res && blockIdx.x < p.num_tiles) ptx::mbar_wait(bres, 0);
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
-        const bool count_tile = (tile % p.num_n_blocks) == 0;
-        const int acc = t_local % p.acc_stages;
-        const uint32_t aph = (uint32_t)(t_local / p.acc_stages) & 1u;
+      if (b_res && blockIdx.x < L_num_tiles) ptx::mbar_wait(bres, 0);
+      for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x, ++t_local) {
+        const bool count_tile = (tile % L_num_n_blocks) == 0;
+        const int acc = t_local % L_acc_stages;
+        const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * p.cols_per_acc);
+        const uint32_t d = tmem_base + (uint32_t)(acc * L_cols_per_acc);
         if (fast) {
           // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
 #pragma unroll 1
-          for (int kb = 0; kb < p.nkb; ++kb) {
+          for (int kb = 0; kb < L_nkb; ++kb) {
             ptx::mbar_wait(&full[s], ph);
             if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
             ptx::tc_fence_after();
@@ -574,43 +623,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t accum = (kb | k) != 0;
               ptx::mma_f16_ss_w(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
-              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, p.idesc_ck, accum);
+              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
             }
             ptx::mma_commit_w(&empty[s]);
-            if (++s == p.stages) { s = 0; ph ^= 1; }
+            if (++s == L_stages) { s = 0; ph ^= 1; }
           }
           ptx::mma_commit_w(&tfull[acc]);
           continue;
         }
 #pragma unroll 1
-        for (int kb = 0; kb < p.nkb; ++kb) {
+        for (int kb = 0; kb < L_nkb; ++kb) {
           ptx::mbar_wait(&full[s], ph);
           if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(sm_a + s * p.stage_a_bytes);
-          const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * p.stage_b_bytes);
-          const uint32_t c_addr = ptx::smem_u32(sm_ck + s * p.stage_ck_bytes);
+          const uint32_t a_addr = ptx::smem_u32(sm_a + s * L_stage_a_bytes);
+          const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * L_stage_b_bytes);
+          const uint32_t c_addr = ptx::smem_u32(sm_ck + s * L_stage_ck_bytes);
           if (halo) {
             // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile
 #pragma unroll 1
-            for (int si = 0; si < p.cv_S; ++si) {
+            for (int si = 0; si < L_cv_S; ++si) {
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k) {
                 const uint32_t row_off = (p.debug & 2097152) ? 0u : (uint32_t)si * 128u;   // bring-up timing bit
                 const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + row_off + (uint32_t)k * 32u) |
                                        (p.debug & 1048576 ? ((uint64_t)(si & 7) << 49) : 0ull);
-                const uint32_t bt_addr = b_addr + (uint32_t)si * p.b_tile_bytes;
+                const uint32_t bt_addr = b_addr + (uint32_t)si * L_b_tile_bytes;
                 const uint64_t bdesc = ptx::desc_kmajor_sw128(bt_addr + k * 32);
                 const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
-                ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
+                ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? L_idesc_aug : L_idesc_main, accum);
                 if (ck_loaded)
                   ptx::mma_f16_ss_w(d + bn, adesc,
-                                  ptx::desc_kmajor_sw128(c_addr + (uint32_t)(si * p.nck_pad * 128) + k * 32),
-                                  p.idesc_ck, accum);
+                                  ptx::desc_kmajor_sw128(c_addr + (uint32_t)(si * L_nck_pad * 128) + k * 32),
+                                  L_idesc_ck, accum);
               }
             }
             ptx::mma_commit_w(&empty[s]);
-            if (++s == p.stages) { s = 0; ph ^= 1; }
+            if (++s == L_stages) { s = 0; ph ^= 1; }
             continue;
           }
 #pragma unroll
@@ -618,9 +667,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t adesc = a_desc(a_addr, k);
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
-            ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? p.idesc_aug : p.idesc_main, accum);
-            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss_w(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), p.idesc_ck, accum);
-            if (has_shadow) ptx::mma_f16_ss_w(d + p.shadow_off, adesc, bdesc, p.idesc_main, accum);
+            ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? L_idesc_aug : L_idesc_main, accum);
+            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss_w(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), L_idesc_ck, accum);
+            if (has_shadow) ptx::mma_f16_ss_w(d + p.shadow_off, adesc, bdesc, L_idesc_main, accum);
           }
           if (p.acolck_mode == 1 && count_tile) {
             // colck[kb*64 + j] += sum_rows A_tile[row][j] on the tensor cores:
@@ -643,29 +692,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               // checksum slice of the previous stage, then release that stage
               ptx::mbar_wait(&ckfull[ps], pph);
               ptx::tc_fence_after();
-              const uint32_t pa = ptx::smem_u32(sm_a + ps * p.stage_a_bytes);
-              const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
+              const uint32_t pa = ptx::smem_u32(sm_a + ps * L_stage_a_bytes);
+              const uint32_t pc = ptx::smem_u32(sm_ck + ps * L_stage_ck_bytes);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
                 ptx::mma_f16_ss_w(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
-                                p.idesc_ck, (kb - 1 > 0 || k > 0) ? 1u : 0u);
+                                L_idesc_ck, (kb - 1 > 0 || k > 0) ? 1u : 0u);
               ptx::mma_commit_w(&empty[ps]);
             }
             ps = s; pph = ph;
           } else {
             ptx::mma_commit_w(&empty[s]);
           }
-          if (++s == p.stages) { s = 0; ph ^= 1; }
+          if (++s == L_stages) { s = 0; ph ^= 1; }
         }
         if (ck_onchip) {
           ptx::mbar_wait(&ckfull[ps], pph);
           ptx::tc_fence_after();
-          const uint32_t pa = ptx::smem_u32(sm_a + ps * p.stage_a_bytes);
-          const uint32_t pc = ptx::smem_u32(sm_ck + ps * p.stage_ck_bytes);
+          const uint32_t pa = ptx::smem_u32(sm_a + ps * L_stage_a_bytes);
+          const uint32_t pc = ptx::smem_u32(sm_ck + ps * L_stage_ck_bytes);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             ptx::mma_f16_ss_w(d + bn, a_desc(pa, k), ptx::desc_kmajor_sw128(pc + k * 32),
-                            p.idesc_ck, (p.nkb - 1 > 0 || k > 0) ? 1u : 0u);
+                            L_idesc_ck, (L_nkb - 1 > 0 || k > 0) ? 1u : 0u);
           ptx::mma_commit_w(&empty[ps]);
         }
         ptx::mma_commit_w(&tfull[acc]);

@@ -208,9 +208,10 @@ class ChainGroup:
         nls = [len(w) for w, _, _ in specs]
         total = sum(nls)
         off_cnt = 16 * total
-        self.block = t.zeros(off_cnt + 16 * len(specs), dtype=t.uint8, device="cuda")
+        off_flag = off_cnt + 16 * len(specs)
+        self.block = t.zeros(off_flag + 16, dtype=t.uint8, device="cuda")
         self.sums = self.block[:off_cnt].view(t.float64).view(total, 2)
-        cnt = self.block[off_cnt:].view(t.int32).view(len(specs), 4)
+        cnt = self.block[off_cnt:off_flag].view(t.int32).view(len(specs), 4)
         self.chains = []
         o = 0
         for (w, b, sch), nl in zip(specs, nls):
@@ -222,13 +223,12 @@ class ChainGroup:
         self.has_global = any(ch.global_ids for ch in self.chains)
         self.ks = t.tensor(ks, dtype=t.int32, device="cuda")
         self.verdicts = t.zeros(total * 32, dtype=t.uint8, device="cuda")
-        self.flagged = t.zeros(1, dtype=t.int32, device="cuda")
+        self.flagged = self.block[off_flag:off_flag + 4].view(t.int32)
         self.numeric = self.chains[0].numeric
 
     def begin(self) -> None:
-        """Clear every member's per-forward accumulators (one memset)."""
+        """Clear every member's per-forward accumulators and the flag count (one memset)."""
         kernels.zero(self.block)
-        kernels.zero(self.flagged)
 
     def end(self) -> None:
         """One verification launch over all members' layers (non-global layers hold (0, 0))."""
