@@ -224,6 +224,7 @@ class ChainGroup:
         self.ks = t.tensor(ks, dtype=t.int32, device="cuda")
         self.verdicts = t.zeros(total * 32, dtype=t.uint8, device="cuda")
         self.flagged = self.block[off_flag:off_flag + 4].view(t.int32)
+        self.tail = self.block[off_cnt:]            # counters + flag count: one D2H read
         self.numeric = self.chains[0].numeric
 
     def begin(self) -> None:
