@@ -1258,7 +1258,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (stamp && et == 0) g_dbg_ts[blockIdx.x][3] = gtimer();
     // -------- per-CTA flush of the global-ABFT output summation and fused colck
-    if (p.out_sum != nullptr || p.gck) {
+    if ((p.out_sum != nullptr || p.gck) && !(p.debug & 16777216)) {   // bit 24: bring-up, no flush
       // one reduction round for the CTA's global-ABFT partials (rhs, lhs)
       double x = rhs_acc, y = lhs_acc;
 #pragma unroll
@@ -1266,21 +1266,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         x += __shfl_xor_sync(0xffffffffu, x, o);
         y += __shfl_xor_sync(0xffffffffu, y, o);
       }
+      // the first epilogue warp folds the 8 warp partials after the kernel's final barrier
       if (lane == 0) { red_d[et >> 5] = x; red_d[8 + (et >> 5)] = y; }
-      ptx::named_bar_sync(3, 256);
-      if (et < 32) {
-        // the first epilogue warp folds the 8 warp partials (lanes 0-7) and adds them once
-        double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
-#pragma unroll
-        for (int o = 4; o >= 1; o >>= 1) {
-          tx += __shfl_xor_sync(0xffffffffu, tx, o);
-          ty += __shfl_xor_sync(0xffffffffu, ty, o);
-        }
-        if (lane == 0) {
-          if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
-          if (p.gck) atomicAdd(p.out_lhs, ty);
-        }
-      }
     }
     // the staging buffers must stay valid until the bulk stores have READ them; the writes
     // themselves complete before the grid does
@@ -1298,6 +1285,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
+  if ((p.out_sum != nullptr || p.gck) && !(p.debug & 16777216) && warp == EPI_WARP0) {
+    // one add per CTA of its (rhs, lhs) partials, by the thread that then counts the CTA done
+    double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+      tx += __shfl_xor_sync(0xffffffffu, tx, o);
+      ty += __shfl_xor_sync(0xffffffffu, ty, o);
+    }
+    if (lane == 0 && !(p.debug & 8388608)) {     // bit 23: bring-up timing without the adds
+      if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
+      if (p.gck) atomicAdd(p.out_lhs, ty);
+    }
+  }
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
   if (p.vn > 0 && warp == EPI_WARP0) {
     // fused deferred verification: the launch's last CTA to finish (done-count) forms every

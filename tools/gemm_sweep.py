@@ -75,14 +75,18 @@ def stamps(m, n, k):
     out = torch.empty((m, n), dtype=torch.float16, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     buf = (ctypes.c_ulonglong * (160 * 8 + 3 * 64))()
+    one_kw = dict(m_ext=-(-m // 16) * 16, n_ext=n, fired_count=cnt)
+    oplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.THREAD_ONE_SIDED, plan_only=True,
+                         ck_layout=1, out=out, ldc=n, out_kind="f16", relu=True, **one_kw)
+    one_kw["ck_rows"] = kernels.aug_weights(pw.bt, n, k, P.BINARY16, oplan, 8, False)
     osum = torch.zeros(2, dtype=torch.float64, device="cuda")
     gk = dict(out_sum=osum[1:2], out_lhs=osum[0:1])
     gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True,
                          ck_layout=1, out=out, ldc=n, out_kind="f16", relu=True, **gk)
     gk["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
     for name, sch, kw in [("unprot", P.Scheme.UNPROTECTED, {}), ("global", P.Scheme.GLOBAL_ABFT, gk),
-                          ("onesided", P.Scheme.THREAD_ONE_SIDED,
-                           dict(m_ext=-(-m // 16) * 16, n_ext=n, fired_count=cnt))]:
+                          ("global_rhs_only", P.Scheme.GLOBAL_ABFT, dict(out_sum=osum[1:2])),
+                          ("onesided", P.Scheme.THREAD_ONE_SIDED, one_kw)]:
         for _ in range(3):
             kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, out=out, ldc=n, out_kind="f16",
                          relu=True, **kw)
