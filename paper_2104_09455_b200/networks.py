@@ -19,7 +19,9 @@ from typing import List
 
 from .shapes import GemmShape
 
-NETWORKS = ("resnet50", "vgg16", "alexnet", "squeezenet1_0", "shufflenet_v2_x1_0")
+NETWORKS = ("resnet50", "vgg16", "alexnet", "squeezenet1_0", "shufflenet_v2_x1_0",
+            # the paper's remaining Fig 4 workloads
+            "densenet161", "resnext50_32x4d", "wide_resnet50_2")
 
 
 @dataclass(frozen=True)

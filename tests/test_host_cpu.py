@@ -236,9 +236,29 @@ def test_network_layer_lists_reproduce_paper_fig4():
     import paper_2104_09455_b200 as P
     from paper_2104_09455_b200 import networks
     from paper_2104_09455_b200.shapes import PaddingPolicy
-    fig4 = {"squeezenet1_0": 71.1, "shufflenet_v2_x1_0": 76.6, "resnet50": 122.0, "alexnet": 125.5, "vgg16": 155.5}
+    fig4 = {"squeezenet1_0": 71.1, "shufflenet_v2_x1_0": 76.6, "resnet50": 122.0, "alexnet": 125.5, "vgg16": 155.5,
+            "densenet161": 79.0, "resnext50_32x4d": 220.8, "wide_resnet50_2": 220.8}
     for name, ai in fig4.items():
         layers = networks.capture(name, 1, 1080, 1920)
         agg = P.aggregate_intensity([P.pad_gemm(l.gemm(), PaddingPolicy.MULTIPLE_OF_8) for l in layers], P.BINARY16)
         assert agg == pytest.approx(ai, abs=0.05), name
     assert len(networks.capture("resnet50", 1, 224, 224)) == 54
+
+
+def test_fitted_device_profile_recovers_model_choices():
+    """calibrate.fit_device_profile: on timings generated by a known device model, the fitted
+    profile's model-only choices agree with the measured choices on every layer."""
+    import paper_2104_09455_b200 as P
+    from paper_2104_09455_b200 import calibrate
+    from paper_2104_09455_b200.cost import scheme_time
+    truth = P.DeviceProfile(name="truth", tensor_throughput=400e12, alu_throughput=20e12,
+                            memory_bandwidth=3000e9, verification_launch_latency=1e-6)
+    shapes = [P.GemmShape(m, n, k) for m in (1, 64, 2048, 50176) for n in (64, 512) for k in (16, 512, 2304)]
+    S = P.Scheme
+    rows = [calibrate.LayerTiming(s, *(scheme_time(s, P.BINARY16, truth, sch) for sch in
+                                       (S.UNPROTECTED, S.GLOBAL_ABFT, S.THREAD_ONE_SIDED))) for s in shapes]
+    peaks = P.DeviceProfile(name="B200", tensor_throughput=1600e12, alu_throughput=80e12, memory_bandwidth=6000e9,
+                            verification_launch_latency=0.0)
+    fit = calibrate.fit_device_profile(rows, P.BINARY16, peaks)
+    assert fit.agreement == 1.0
+    assert fit.model_plan_time == pytest.approx(fit.measured_plan_time)
