@@ -1125,7 +1125,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
-          const bool relu_in_pack = p.relu && p.tma_store && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr;
+          // whole 32-column chunks go out by bulk tensor stores; a tile's 16-column tail (bn_eff = 240
+          // etc.) by direct stores
+          const bool chunk_tma = p.tma_store && cmax >= 32;
+          const bool relu_in_pack = p.relu && chunk_tma && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr;
           if (p.relu && !relu_in_pack) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
@@ -1134,7 +1137,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = round_out(v[j], p.out_dtype);
           }
-          if (p.tma_store) {
+          if (chunk_tma) {
             // stage the warp's [32 rows x 32 columns] in the TMA swizzle order (fp32: 128-byte
             // rows, SW128; 16-bit: 64-byte rows, SW64), then one lane issues the bulk store
             if (p.debug & 131072) {
@@ -1552,7 +1555,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
       const bool dbuf = 2 * cols + extra_cols <= 512;
       const int eff = (cand / nt) * nt;
       const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
-      const long long waves = (tiles + sms - 1) / sms;
+      // whole waves while a CTA runs few tiles; fractional beyond 4 waves, where the CTAs with one
+      // tile less free L2 bandwidth for the rest (bandwidth-bound big GEMMs)
+      const long long waves = tiles <= 4LL * sms ? 100 * ((tiles + sms - 1) / sms) : (100 * tiles + sms - 1) / sms;
       const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
       const bool asplit = a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256;
       if (asplit && cand != 256) continue;
@@ -1561,9 +1566,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
       // 32-column chunks lose the bulk-tensor output stores (~4 k-blocks of epilogue)
       const int a_rows = (cg != nullptr && (cg->a_mode == 1 || cg->a_mode == 2)) ? 256 : 128;
       const long long rows = a_rows + 2LL * cand + nck + (asplit ? 64 : 0);
-      const int no_tma_store = (a->out_dtype != ABFT_OUT_NONE && !halo && cand % 32 != 0) ? 4 : 0;
+      const int no_tma_store = (a->out_dtype != ABFT_OUT_NONE && !halo && cand % 16 != 0) ? 4 : 0;
       const long long cost = waves * (nkb_plan + no_tma_store) * rows +
-                             (dbuf ? 0 : (waves - 1) * (thread_level ? 8 : 2) * rows);
+                             (dbuf ? 0 : (waves - 100) * (thread_level ? 8 : 2) * rows);
       if (best == 0 || cost < best_cost) { best = cand; best_cost = cost; }
     }
     bn = best;
@@ -1666,10 +1671,10 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const uint32_t stage_bytes_ep = (thread_level && out.ntc == 0) ? (uint32_t)(2 * 32 * BM * 4) : 0;
   const uint32_t colck_bytes = p.colck_in_smem ? (uint32_t)round_up(a->N * 4, 1024) : 0;
   {
-    // bulk tensor stores of the output: whole 128-row tiles, 128-byte row units (32 fp32 / 64
-    // 16-bit columns) that tile bn_eff exactly, 16-byte aligned base and row pitch
+    // bulk tensor stores of the output: whole 128-row tiles in 32-column boxes (a 16-column tail
+    // of the tile is stored directly), 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
-    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 32 == 0 &&
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 16 == 0 &&
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
                    !(dbg_env & 8192)) ? 1 : 0;
   }
@@ -1692,7 +1697,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     const uint32_t stage_bytes0 = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes +
                                   (p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u);
     const int room = smem_cap - (int)extras0 - (p.lhs_w != nullptr ? 1024 : 0);
-    if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo && room / (int)stage_bytes0 < 4 &&
+    if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo &&
         (room - (int)(8u * 2048u)) / (int)stage_bytes0 >= 4 && (room - (int)out_bytes) / (int)stage_bytes0 < 4) {
       p.out_single = 1;
       out_bytes = 8u * 2048u;

@@ -5,6 +5,7 @@ executed through the drop-in ``execute``; a trial is detected / masked-by-tolera
 in campaign.py:213-247; fault-free control trials count false positives.
 usage: python tools/campaign_gpu.py [--trials N] [--out FILE]"""
 import argparse
+import itertools
 import json
 import os
 import sys
@@ -22,12 +23,15 @@ def main():
     from paper_2104_09455_b200 import campaign as C
     schemes = tuple(s for s in P.Scheme if s is not P.Scheme.UNPROTECTED)
     res = {"trials_per_scheme": args.trials, "control_trials_per_scheme": args.trials, "configs": []}
-    for dname, dtype, delta in (("exact-int", P.EXACT_INT, C.INT_DELTAS), ("binary16", P.BINARY16, C.FP_DELTAS)):
+    for (dname, dtype, delta), site in itertools.product(
+            (("exact-int", P.EXACT_INT, C.INT_DELTAS), ("binary16", P.BINARY16, C.FP_DELTAS)),
+            (C.SITE_OUTPUT, C.SITE_THREAD_MMA)):
         cfg = C.CampaignConfig(trials=args.trials, seed=2104, gemm_min=8, gemm_max=96, schemes=schemes, dtype=dtype,
-                               delta=delta, control_trials=args.trials)
+                               delta=delta, control_trials=args.trials, site=site)
         t0 = time.time()
         stats = C.run_campaign(cfg)
-        row = {"dtype": dname, "gemm_extent": [8, 96], "deltas": f"{delta.kind} [{delta.low}, {delta.high}]",
+        row = {"dtype": dname, "site": site, "gemm_extent": [8, 96],
+               "deltas": f"{delta.kind} [{delta.low}, {delta.high}]",
                "wall_s": round(time.time() - t0, 1), "schemes": {}}
         for s, st in stats.items():
             row["schemes"][s.value] = dict(injected=st.injected_trials, detected=st.detected,
