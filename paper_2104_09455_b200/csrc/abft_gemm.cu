@@ -1966,7 +1966,7 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
     const bool ck_ok = c->gemm.scheme == ABFT_UNPROTECTED ||
                        (c->gemm.scheme == ABFT_GLOBAL ? (c->gemm.out_lhs == nullptr || c->gemm.ck_layout == 1 ||
                                                          c->gemm.lhs_rowck != nullptr)
-                                                      : (c->gemm.ck_layout == 1 && c->gemm.ck_rows != nullptr));
+                                                      : c->gemm.ck_layout == 1);   // plan == launch
     const int mt = thread_level ? std::max(1, c->gemm.thread_m) : 1;
     if (mode == 1 && c->stride_h == 1 && c->stride_w == 1 && c->s <= 16 && ck_ok && c->gemm.a_colck == nullptr &&
         c->gemm.scheme != ABFT_REPL_FULL && c->gemm.scheme != ABFT_REPL_SINGLE) {
