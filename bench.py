@@ -427,7 +427,9 @@ def main():
                "sample": f"{reps} x run_protected_pipeline (oracle port) on bottom/b2048, top/b2048, top/b1 "
                          f"({dt:.1f} s, numpy BLAS threads = host cores)"}
 
-    n_launch = sum(len(c.layers) for c in chains["ig"].values())
+    # per timed step: every chain layer's GEMM + the group's one verification launch (if any
+    # layer of the plan is global)
+    n_launch = sum(len(c.layers) for c in chains["ig"].values()) + int(groups["ig"].has_global)
     line = {
         "metric": base["metric"], "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
