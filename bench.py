@@ -259,7 +259,7 @@ def main():
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=main):
             grp.begin()
-            if os.environ.get("BENCH_SERIAL"):
+            if os.environ.get("BENCH_SERIAL"):          # measurement toggle: chains on one stream
                 for ch in cs:
                     ch.forward()
             else:
@@ -290,8 +290,7 @@ def main():
         torch.cuda.synchronize()
         ts = []
         for _ in range(steps):
-            if not os.environ.get("BENCH_NOFLUSH"):
-                flush.fill_(1.0)
+            flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 torch.distributed.barrier()
