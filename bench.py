@@ -309,9 +309,10 @@ def main():
     # interleave policies so clock drift hits all of them alike
     res = {pol: [] for pol in graphs}
     with ClockSampler(local) as clk:
-        for _ in range(2):
+        for half in (args.steps // 2, args.steps - args.steps // 2):     # exactly K timed steps per policy
             for pol in graphs:
-                res[pol] += timed(pol, max(args.steps // 2, 1), args.warmup if not res[pol] else 1)
+                if half > 0:
+                    res[pol] += timed(pol, half, args.warmup if not res[pol] else 1)
     ms = {pol: statistics.median(v) for pol, v in res.items()}
     # headline: IG plan, the mean over its K timed steps, max over ranks
     t_ig = torch.tensor([statistics.mean(res["ig"])], device="cuda")
