@@ -412,7 +412,7 @@ def main():
 
     # ---- CPU baseline: the oracle port of the reference forward on a bounded sample
     cpu = None
-    if rank == 0:
+    if rank == 0 and world == 1:              # rank 0 at N = 1 only (the N > 1 lines carry null)
         from oracle import abft_oracle as O   # cpu_baseline leg only
         sample_keys = [("bottom", 2048), ("top", 2048), ("top", 1)]
         t0 = time.perf_counter()
