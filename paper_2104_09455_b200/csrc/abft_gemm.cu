@@ -97,6 +97,8 @@ struct GemmParams {
   int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
   int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
   int out_single;        // 1: one 2 KB 16-bit staging buffer per epilogue warp (else two)
+  int kpair;             // 1: a pipeline stage carries two consecutive k-blocks (plain GEMM A, one box per
+                         //    operand and k-block, half the barrier round trips and loop iterations)
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
   int rec_stride;
   void* C;
@@ -493,6 +495,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ho = pp * p.cv_sh - p.cv_ph;
           wo = (rem - pp * L_cv_Q) * p.cv_sw - p.cv_pw;
         }
+        if (p.kpair) {
+          // two k-blocks per stage: A (kb, kb+1) and B (kb, kb+1) boxes side by side
+          const uint32_t tx1 = (L_stage_a_bytes >> 1) + L_tx_b;
+          const int brow = ck_aug ? nb * L_b_rows_blk : n0;
+#pragma unroll 1
+          for (int kb = 0; kb < L_nkb; kb += 2) {
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            const bool two = kb + 1 < L_nkb;
+            ptx::mbar_arrive_expect_tx_w(&full[s], two ? 2 * tx1 : tx1);
+            uint8_t* a_dst = sm_a + s * L_stage_a_bytes;
+            uint8_t* b_dst = sm_b + s * L_stage_b_bytes;
+            // A of k-block k: a tiled box (GEMM) or a 64-channel im2col box (conv tap, chunk)
+            auto load_a = [&](uint8_t* dst, int k) {
+              if (L_a_mode == 0) {
+                ptx::tma_load_2d_w(dst, &tmA, &full[s], k * BK, m0);
+              } else {
+                const int tap = k / L_cv_chunks;
+                const int r = tap / L_cv_S;
+                ptx::tma_load_im2col_4d_w(dst, &tmA, &full[s], (k - tap * L_cv_chunks) * BK, wo, ho, img,
+                                          (uint16_t)(tap - r * L_cv_S), (uint16_t)r);
+              }
+            };
+            load_a(a_dst, kb);
+            ptx::tma_load_2d_w(b_dst, &tmB, &full[s], kb * BK, brow);
+            if (two) {
+              load_a(a_dst + (L_stage_a_bytes >> 1), kb + 1);
+              ptx::tma_load_2d_w(b_dst + (L_stage_b_bytes >> 1), &tmB, &full[s], (kb + 1) * BK, brow);
+            }
+            if (++s == L_stages) { s = 0; ph ^= 1; }
+          }
+          continue;
+        }
 #pragma unroll 1
         for (int kb = 0; kb < L_nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -609,6 +643,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * L_cols_per_acc);
+        if (p.kpair) {
+          const uint64_t a_half = (uint64_t)(L_stage_a_bytes >> 5), b_half = (uint64_t)(L_stage_b_bytes >> 5);
+#pragma unroll 1
+          for (int kb = 0; kb < L_nkb; kb += 2) {
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            const uint64_t ad = a_base + (uint64_t)s * a_sstep;
+            const uint64_t bd = b_base + (uint64_t)s * b_sstep;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              ptx::mma_f16_ss_w(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0);
+            if (kb + 1 < L_nkb) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                ptx::mma_f16_ss_w(d, ad + a_half + 2ull * k, bd + b_half + 2ull * k, idesc_m, 1u);
+            }
+            ptx::mma_commit_w(&empty[s]);
+            if (++s == L_stages) { s = 0; ph ^= 1; }
+          }
+          ptx::mma_commit_w(&tfull[acc]);
+          continue;
+        }
         if (fast) {
           // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
 #pragma unroll 1
@@ -1665,6 +1721,21 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     p.stage_b_bytes = p.b_tile_bytes * (uint32_t)cg->S;
   }
   p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2 * (halo ? cg->S : 1), 1024);
+  // two k-blocks per stage for plain-GEMM A with no separately loaded checksum slice
+  p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1) && (p.ck_mode == 0 || p.ck_mode == 3) &&
+             !has_shadow && !want_acolck && a->lhs_rowck == nullptr && p.nkb >= 2 &&
+             !(getenv("ABFT_KPAIR") && atoi(getenv("ABFT_KPAIR")) == 0)) ? 1 : 0;
+  if (p.kpair) {
+    // only while the pipeline keeps >= 3 stages of pairs (tiles up to ~128 columns: the
+    // latency-bound GEMMs); wide tiles keep single k-block stages
+    // (16 KB of output staging: one buffer per warp when that buys a stage, below)
+    const int room_est = max_smem_optin() - 2048 - 16384 - (has_ck ? 16384 : 0);
+    if (room_est / (int)(2 * (p.stage_a_bytes + p.stage_b_bytes)) < 3) p.kpair = 0;
+  }
+  if (p.kpair) {
+    p.stage_a_bytes *= 2;
+    p.stage_b_bytes *= 2;
+  }
   p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
   const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
   const uint32_t rec_bytes = p.rec_stride ? (uint32_t)round_up(BM * p.rec_stride * 8, 1024) : 0;
@@ -1693,12 +1764,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.out_single = 0;
   {
     // 16-bit outputs: one 2 KB staging buffer per epilogue warp instead of two when that buys
-    // a 4th pipeline stage (the stage_w / checksum-box layouts sit just past the 3-stage line)
+    // a pipeline stage (the stage_w / checksum-box / k-pair layouts sit just past a stage line)
     const uint32_t stage_bytes0 = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes +
                                   (p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u);
     const int room = smem_cap - (int)extras0 - (p.lhs_w != nullptr ? 1024 : 0);
     if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo &&
-        (room - (int)(8u * 2048u)) / (int)stage_bytes0 >= 4 && (room - (int)out_bytes) / (int)stage_bytes0 < 4) {
+        (room - (int)(8u * 2048u)) / (int)stage_bytes0 > (room - (int)out_bytes) / (int)stage_bytes0 &&
+        (room - (int)out_bytes) / (int)stage_bytes0 < 8) {
       p.out_single = 1;
       out_bytes = 8u * 2048u;
     }
