@@ -174,13 +174,16 @@ __device__ __forceinline__ float round_out(float y, int out_dtype) {
 
 // |x - y| > r*K*max(|x|,|y|,1) evaluated exactly as the reference does (float64), but
 // decided in fp32 whenever the margin exceeds the fp32 rounding of the operands.
-__device__ __forceinline__ bool exceeds_tol(const GemmParams& p, float x, float y) {
-  if (p.r == 0.0) return x != y;                       // exact-int mode: tau = 0, values exact
+__device__ __forceinline__ bool exceeds_tol_rk(bool exact, float rk, const GemmParams& p, float x, float y) {
+  if (exact) return x != y;                            // exact-int mode: tau = 0, values exact
   const float d = fabsf(x - y);
-  const float t = p.rk * fmaxf(fmaxf(fabsf(x), fabsf(y)), 1.f);
+  const float t = rk * fmaxf(fmaxf(fabsf(x), fabsf(y)), 1.f);
   if (d > t * 1.0001f) return true;
   if (d < t * 0.9999f) return false;
   return fabs((double)x - (double)y) > tolerance(p.r, p.tol_k, x, y);
+}
+__device__ __forceinline__ bool exceeds_tol(const GemmParams& p, float x, float y) {
+  return exceeds_tol_rk(p.r == 0.0, p.rk, p, x, y);
 }
 
 // vector rule: per-row (or per-element) comparisons, worst one reported (tiled.py:203-218)
@@ -1076,6 +1079,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float ck_hi = 0.f, ck_lo = 0.f;
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
       const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
+      const bool exact_mode = p.r == 0.0;   // per-tile constants of the fast compare, in registers
+      const float rk = p.rk;
       uint32_t fmask = 0;
       // generic-Nt running state
       float gsum = 0.f, ssum = 0.f, best_c = 0.f, best_s = 0.f;
@@ -1134,7 +1139,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
               if (flags_fast) {
                 // one-sided flags-only: one fp32 compare per (row, group), folded into a bitmask
-                if (exceeds_tol(p, x, y)) fmask |= 1u << gg;
+                if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << gg;
               } else if (!(p.debug & 1)) {
                 group_done(p, rec, row, lane, gg, x, y, n0, t_row, row_verdict);
               }
@@ -1174,8 +1179,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.out_sum != nullptr) {
           // four independent partial chains instead of one 32-deep dependent FADD chain
           float t4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (cmax >= 32) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) t4[j & 3] += (j < cmax) ? v[j] : 0.f;
+            for (int j = 0; j < 32; ++j) t4[j & 3] += v[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) t4[j & 3] += (j < cmax) ? v[j] : 0.f;
+          }
           tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
         }
         if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
