@@ -282,3 +282,21 @@ def test_augmented_weights_with_full_width_tile(P, scheme, m, n, k):
         assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \
             [(v.thread_row, v.thread_col) for v in v_ref if v.detected]
         assert len([v for v in rep.verdicts if v.detected]) == 2
+
+
+@pytest.mark.parametrize("scheme", ["unprotected", "global-abft", "thread-one-sided"])
+@pytest.mark.parametrize("m,n,k", [(300, 200, 1000), (2048, 64, 576), (130, 120, 136)])
+def test_kblock_pairs_match_single_kblock_stages(P, monkeypatch, scheme, m, n, k):
+    """Pipeline stages of two k-blocks (default for narrow tiles; odd k-block counts end with a
+    single one) and single k-block stages (ABFT_KPAIR=0) give the oracle's exact-int results."""
+    rng = np.random.default_rng(m + 7 * n + k)
+    a = rng.integers(-8, 9, size=(m, k), dtype=np.int64)
+    b = rng.integers(-8, 9, size=(k, n), dtype=np.int64)
+    fr = [("output", m - 1, n // 2, 5)] if scheme != "unprotected" else []
+    out_ref, v_ref = O.execute(a, b, O.Tiling(), scheme, fr)
+    faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
+    for kp in ("0", "2"):
+        monkeypatch.setenv("ABFT_KPAIR", kp)
+        rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults)
+        assert np.array_equal(rep.output, out_ref), kp
+        assert rep.detected == any(v.detected for v in v_ref), kp
