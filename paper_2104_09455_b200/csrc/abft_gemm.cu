@@ -1732,7 +1732,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   }
   p.stage_ck_bytes = p.ck_mode == 3 ? 0u : (uint32_t)round_up(p.nck_pad * BK * 2 * (halo ? cg->S : 1), 1024);
   // two k-blocks per stage for plain-GEMM A with no separately loaded checksum slice
-  p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1) && (p.ck_mode == 0 || p.ck_mode == 3) &&
+  // (conv mode 3 runs the plain GEMM over its im2col workspace: kernel A mode 0)
+  p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1 || cg->a_mode == 3) &&
+             (p.ck_mode == 0 || p.ck_mode == 3) &&
              !has_shadow && !want_acolck && a->lhs_rowck == nullptr && p.nkb >= 2 &&
              !(getenv("ABFT_KPAIR") && atoi(getenv("ABFT_KPAIR")) == 0)) ? 1 : 0;
   if (p.kpair) {
