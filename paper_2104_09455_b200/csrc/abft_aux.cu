@@ -204,7 +204,7 @@ __global__ void conv_pack_weight_kernel(const uint16_t* __restrict__ w, int oc, 
 // A CTA builds IM2COL_PIX output rows in shared memory: each (pixel, filter row) task reads
 // the S input pixels of that window row as 16-byte channel vectors (C is a multiple of 8) and
 // scatters their cr real channels; the finished rows leave as coalesced 16-byte stores.
-constexpr int IM2COL_PIX = 64;
+constexpr int IM2COL_PIX = 128;
 
 __global__ void __launch_bounds__(256) im2col_kernel(const uint16_t* __restrict__ x, int H, int W, int C, int cr,
                                                      int R, int S, int sh, int sw, int ph, int pw, int P, int Q,
