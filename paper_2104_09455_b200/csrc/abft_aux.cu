@@ -204,18 +204,19 @@ __global__ void conv_pack_weight_kernel(const uint16_t* __restrict__ w, int oc, 
 // A CTA builds IM2COL_PIX output rows in shared memory: each (pixel, filter row) task reads
 // the S input pixels of that window row as 16-byte channel vectors (C is a multiple of 8) and
 // scatters their cr real channels; the finished rows leave as coalesced 16-byte stores.
-constexpr int IM2COL_PIX = 128;
+constexpr int IM2COL_PIX = 128;   // pixels per tile for rows up to 384 columns (else 64, 32)
 
 __global__ void __launch_bounds__(256) im2col_kernel(const uint16_t* __restrict__ x, int H, int W, int C, int cr,
                                                      int R, int S, int sh, int sw, int ph, int pw, int P, int Q,
-                                                     long long M, int K, int ld, uint16_t* __restrict__ out) {
-  extern __shared__ uint16_t tile[];          // [IM2COL_PIX][ld]
+                                                     long long M, int K, int ld, int pix_tile,
+                                                     uint16_t* __restrict__ out) {
+  extern __shared__ uint16_t tile[];          // [pix_tile][ld]
   const int cv = C / 8;                        // 16-byte channel vectors per pixel
   const int pq = P * Q;
-  for (long long m0 = (long long)blockIdx.x * IM2COL_PIX; m0 < M; m0 += (long long)gridDim.x * IM2COL_PIX) {
-    const int npix = (int)min((long long)IM2COL_PIX, M - m0);
+  for (long long m0 = (long long)blockIdx.x * pix_tile; m0 < M; m0 += (long long)gridDim.x * pix_tile) {
+    const int npix = (int)min((long long)pix_tile, M - m0);
     // zero the tile (padding taps, channels >= cr, columns >= K)
-    for (int i = threadIdx.x; i < IM2COL_PIX * ld / 8; i += blockDim.x)
+    for (int i = threadIdx.x; i < pix_tile * ld / 8; i += blockDim.x)
       reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     // tasks: (pixel, filter row, channel vector)
@@ -323,17 +324,19 @@ __global__ void __launch_bounds__(256) conv_colck_kernel(const T* __restrict__ x
 int launch_im2col(const void* x, int n, int h, int w, int c, int cr, int r, int s, int sh, int sw, int ph, int pw,
                   int P, int Q, int K, int ld, void* out, cudaStream_t st) {
   const long long M = (long long)n * P * Q;
-  const size_t smem = (size_t)IM2COL_PIX * ld * 2;
+  int pix = IM2COL_PIX;
+  while (pix > 32 && (size_t)pix * ld * 2 > (pix == IM2COL_PIX ? 96u * 1024u : 200u * 1024u)) pix /= 2;
+  const size_t smem = (size_t)pix * ld * 2;
   if (smem > 200 * 1024) return fail(ABFT_E_UNSUPPORTED, "im2col: row too long for the shared-memory tile");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const long long tiles = (M + IM2COL_PIX - 1) / IM2COL_PIX;
+  const long long tiles = (M + pix - 1) / pix;
   int blocks = (int)std::min<long long>(tiles, 8LL * num_sms());
   im2col_kernel<<<blocks, 256, smem, st>>>((const uint16_t*)x, h, w, c, cr, r, s, sh, sw, ph, pw, P, Q, M, K, ld,
-                                          (uint16_t*)out);
+                                          pix, (uint16_t*)out);
   return cuda_check(cudaGetLastError(), "im2col launch");
 }
 }  // namespace abft
