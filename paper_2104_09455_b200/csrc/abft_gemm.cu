@@ -1029,7 +1029,102 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int sbuf = 0;
     uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * (p.out_single ? 2048 : 4096);
     int t_local = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+    // Lean path (unprotected and global ABFT, 16-bit bulk-tensor stores, no faults / fused colck /
+    // bring-up bits): the same results as the generic loop below with its per-chunk scheme
+    // dispatch stripped — the epilogue is the critical path of skinny, many-tile GEMMs.
+    bool lean = false;
+    if constexpr (CLASS == CLASS_PLAIN) {
+      lean = p.tma_store && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) && p.next_colck == nullptr &&
+             p.nfaults == 0 && p.debug == 0 && split;
+    }
+    if (lean) {
+      const bool want_sum = p.out_sum != nullptr;
+      const bool relu = p.relu != 0;
+      const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
+      const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
+      const long long ldc = p.ldc;
+      const bool single = p.out_single != 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+        const int acc = t_local % acc_stages;
+        const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
+        const int mb = tile / nnb;
+        const int m0 = mb * bm_eff;
+        const int n0 = (tile - mb * nnb) * bn_eff;
+        const int gm = m0 + row;
+        const bool row_in_tile = row < bm_eff;
+        ptx::mbar_wait(&tfull[acc], aph);
+        ptx::tc_fence_after();
+        const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
+        const bool gck_ld = p.gck && h == 0;
+        float ck_hi = 0.f, ck_lo = 0.f;
+        float tsum = 0.f;
+#pragma unroll 1
+        for (int c0 = c_first; c0 < bn_eff; c0 += 64) {
+          float v[32];
+          __syncwarp();
+          ptx::tmem_ld32(tacc + c0, v);
+          if (gck_ld && c0 == c_first) ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
+          ptx::tmem_ld_wait();
+          if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
+          const int cmax = bn_eff - c0;
+          const int gc0 = n0 + c0;
+          if (cmax >= 32) {
+            if (want_sum) {
+              float t4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int j = 0; j < 32; ++j) t4[j & 3] += v[j];
+              tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
+            }
+            if (lane == 0) {
+              if (single) ptx::bulk_wait_read<0>();
+              else ptx::bulk_wait_read<1>();
+            }
+            __syncwarp();
+            uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 u;
+              if (relu) {
+                u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
+                u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
+                u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
+                u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
+              } else {
+                u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+                u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+                u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+                u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+              }
+              *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmC, my_stage + sbuf * 2048, gc0, m0 + q * 32);
+              ptx::bulk_commit();
+            }
+            sbuf ^= single ? 0 : 1;
+          } else {
+            // the tile's 16-column tail: direct stores
+            if (want_sum) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
+            }
+            if (row_in_tile && gm < M) {
+              T* dst = reinterpret_cast<T*>(p.C) + (long long)gm * ldc + gc0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < cmax && gc0 + j < N) dst[j] = TR::from_f(relu ? fmaxf(v[j], 0.f) : v[j]);
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        if (row_in_tile) rhs_acc += (double)tsum;
+      }
+    }
+    for (int tile = lean ? p.num_tiles : (int)blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
       const uint32_t aph = (uint32_t)(t_local / p.acc_stages) & 1u;
       const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
