@@ -1124,6 +1124,111 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (row_in_tile) rhs_acc += (double)tsum;
       }
     }
+    // Lean one-sided path (static group width, flags-only verdicts, 16-bit bulk-tensor stores,
+    // no faults / fused colck / bring-up bits): the generic loop's checks, without its dispatch.
+    if constexpr (CLASS == CLASS_CHECKSUM && NT > 0) {
+      const bool flags_only = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
+      if (flags_only && p.tma_store && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) &&
+          p.next_colck == nullptr && p.nfaults == 0 && p.debug == 0 && split) {
+        lean = true;
+        constexpr int GPC = 32 / NT;
+        constexpr int GPCK = 32 / NT;
+        const bool relu = p.relu != 0;
+        const bool exact_mode = p.r == 0.0;
+        const float rk = p.rk;
+        const bool ck_split = p.split != 0;
+        const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
+        const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M, mt = p.mt, groups = p.groups;
+        const long long ldc = p.ldc;
+        const bool single = p.out_single != 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+          const int acc = t_local % acc_stages;
+          const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
+          const int mb = tile / nnb;
+          const int m0 = mb * bm_eff;
+          const int n0 = (tile - mb * nnb) * bn_eff;
+          const int gm = m0 + row;
+          const bool row_in_tile = row < bm_eff;
+          const int t_row = gm / mt;
+          const bool row_verdict = row_in_tile && t_row < p.n_trows;
+          ptx::mbar_wait(&tfull[acc], aph);
+          ptx::tc_fence_after();
+          const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
+          uint32_t fmask = 0;
+#pragma unroll 1
+          for (int c0 = c_first; c0 < bn_eff; c0 += 64) {
+            float v[32], ckh[GPCK], ckl[GPCK];
+            __syncwarp();
+            ptx::tmem_ld32(tacc + c0, v);
+            ptx::tmem_ldn<GPCK>(tacc + bn + c0 / NT, ckh);
+            if (ck_split) ptx::tmem_ldn<GPCK>(tacc + bn + groups + c0 / NT, ckl);
+            ptx::tmem_ld_wait();
+            const int cmax = bn_eff - c0;
+            const int gc0 = n0 + c0;
+#pragma unroll
+            for (int gi = 0; gi < GPC; ++gi) {
+              if (gi * NT < cmax) {
+                float y = 0.f;
+#pragma unroll
+                for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
+                const float x = ck_split ? ckh[gi] + ckl[gi] : ckh[gi];
+                if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << (c0 / NT + gi);
+              }
+            }
+            if (cmax >= 32) {
+              if (lane == 0) {
+                if (single) ptx::bulk_wait_read<0>();
+                else ptx::bulk_wait_read<1>();
+              }
+              __syncwarp();
+              uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 u;
+                if (relu) {
+                  u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
+                  u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
+                  u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
+                  u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
+                } else {
+                  u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+                  u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+                  u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+                  u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+                }
+                *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+              }
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_2d(&tmC, my_stage + sbuf * 2048, gc0, m0 + q * 32);
+                ptx::bulk_commit();
+              }
+              sbuf ^= single ? 0 : 1;
+            } else if (row_in_tile && gm < M) {
+              T* dst = reinterpret_cast<T*>(p.C) + (long long)gm * ldc + gc0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < cmax && gc0 + j < N) dst[j] = TR::from_f(relu ? fmaxf(v[j], 0.f) : v[j]);
+            }
+          }
+          // fired groups of the thread tile's Mt rows -> verdicts (rare)
+          uint32_t m = row_verdict ? fmask : 0u;
+          for (int off = 1; off < mt; off <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, off);
+          if ((lane & (mt - 1)) == 0 && m != 0u) {
+            const int t_col0 = n0 / p.nt;
+            while (m != 0u) {
+              const int gbit = __ffs(m) - 1;
+              m &= m - 1u;
+              if (t_col0 + gbit < p.n_tcols) emit_verdict(p, t_row, t_col0 + gbit, true, 0.0, 0.0);
+            }
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+      }
+    }
     for (int tile = lean ? p.num_tiles : (int)blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
       const uint32_t aph = (uint32_t)(t_local / p.acc_stages) & 1u;

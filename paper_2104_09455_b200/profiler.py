@@ -52,8 +52,16 @@ def graph_time_us(fn, iters: int = 40, reps: int = 5) -> float:
 
 
 def profile_layers(weights: Sequence, batch: int, dtype: DType = BINARY16,
-                   tiling: TilingConfig = TilingConfig(), iters: int = 40) -> MeasuredTimings:
-    """Measured per-layer times (seconds) for unprotected / global-abft / thread-one-sided."""
+                   tiling: TilingConfig = TilingConfig(), iters: int = 40, in_chain: bool = False) -> MeasuredTimings:
+    """Measured per-layer times (seconds) for unprotected / global-abft / thread-one-sided.
+
+    in_chain=False: each layer's kernel timed alone (back-to-back launches of that layer).
+    in_chain=True: each layer timed where it runs — inside the chain (programmatic dependent
+    launch from the previous layer, accumulators and verification owned by a ChainGroup as in
+    a serving step): a layer's protected time is the unprotected chain's per-layer time plus
+    the measured change of the whole chain's time when only that layer is protected."""
+    if in_chain:
+        return _profile_layers_in_chain(weights, batch, dtype, tiling, iters)
     n = len(weights)
     chains = {s: ProtectedChain(weights, batch, [s] * n, dtype, tiling) for s in
               (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED)}
@@ -73,4 +81,33 @@ def profile_layers(weights: Sequence, batch: int, dtype: DType = BINARY16,
         out[(i, Scheme.UNPROTECTED)] = entries[(i, Scheme.UNPROTECTED)] * 1e-6
         out[(i, Scheme.GLOBAL_ABFT)] = entries[(i, Scheme.GLOBAL_ABFT)] * 1e-6
         out[(i, Scheme.THREAD_ONE_SIDED)] = entries[(i, Scheme.THREAD_ONE_SIDED)] * 1e-6
+    return MeasuredTimings(entries=out)
+
+
+def _profile_layers_in_chain(weights, batch, dtype, tiling, iters) -> MeasuredTimings:
+    t = D.torch()
+    n = len(weights)
+    S = Scheme
+
+    def chain_us(schemes):
+        nl = len(schemes)
+        block = t.zeros(16 * nl + 16, dtype=t.uint8, device="cuda")
+        shared = (block[:16 * nl].view(t.float64).view(nl, 2), block[16 * nl:16 * nl + 8].view(t.int32),
+                  block[16 * nl + 8:16 * nl + 12].view(t.int32))
+        ch = ProtectedChain(weights, batch, list(schemes), dtype, tiling, shared=shared)
+        return graph_time_us(ch.forward, iters)
+
+    base = chain_us([S.UNPROTECTED] * n)
+    # split the unprotected chain time over its layers by their standalone kernel times
+    alone = profile_layers(weights, batch, dtype, tiling, iters).entries
+    un = [alone[(i, S.UNPROTECTED)] for i in range(n)]
+    scale = base * 1e-6 / sum(un)
+    out = {}
+    for i in range(n):
+        t_un = un[i] * scale
+        out[(i, S.UNPROTECTED)] = t_un
+        for s in (S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
+            sch = [S.UNPROTECTED] * n
+            sch[i] = s
+            out[(i, s)] = max(t_un + (chain_us(sch) - base) * 1e-6, 1e-9)
     return MeasuredTimings(entries=out)
