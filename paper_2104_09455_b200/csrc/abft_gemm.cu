@@ -329,6 +329,38 @@ __device__ __forceinline__ void apply_faults(const abft_fault_t* faults, int nfa
   }
 }
 
+
+// One row's 32-column chunk of a 16-bit output by direct stores (ReLU folded into the pack):
+// four 16-byte stores when the chunk is whole and aligned, else element by element.
+template <typename T>
+__device__ __forceinline__ void lean_store_row(const float (&v)[32], void* C, int gm, long long ldc, int gc0, int cmax,
+                                               int N, bool relu) {
+  using TR = ElemTraits<T>;
+  T* dst = reinterpret_cast<T*>(C) + (long long)gm * ldc + gc0;
+  if (cmax >= 32 && gc0 + 32 <= N && (ldc % 8) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 u;
+      if (relu) {
+        u.x = TR::pack2_relu(v[j], v[j + 1]);
+        u.y = TR::pack2_relu(v[j + 2], v[j + 3]);
+        u.z = TR::pack2_relu(v[j + 4], v[j + 5]);
+        u.w = TR::pack2_relu(v[j + 6], v[j + 7]);
+      } else {
+        u.x = TR::pack2(v[j], v[j + 1]);
+        u.y = TR::pack2(v[j + 2], v[j + 3]);
+        u.z = TR::pack2(v[j + 4], v[j + 5]);
+        u.w = TR::pack2(v[j + 6], v[j + 7]);
+      }
+      *reinterpret_cast<uint4*>(dst + j) = u;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < cmax && gc0 + j < N) dst[j] = TR::from_f(relu ? fmaxf(v[j], 0.f) : v[j]);
+  }
+}
+
 template <typename T, int CLASS, int NT, bool HALO>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1034,7 +1066,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // dispatch stripped — the epilogue is the critical path of skinny, many-tile GEMMs.
     bool lean = false;
     if constexpr (CLASS == CLASS_PLAIN) {
-      lean = p.tma_store && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) && p.next_colck == nullptr &&
+      lean = (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) && p.next_colck == nullptr &&
              p.nfaults == 0 && p.debug == 0 && split;
     }
     if (lean) {
@@ -1044,6 +1076,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
       const long long ldc = p.ldc;
       const bool single = p.out_single != 0;
+      const bool tma = p.tma_store != 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
         const int acc = t_local % acc_stages;
         const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
@@ -1068,7 +1101,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
           const int cmax = bn_eff - c0;
           const int gc0 = n0 + c0;
-          if (cmax >= 32) {
+          if (cmax >= 32 && tma) {
             if (want_sum) {
               float t4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1105,17 +1138,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             sbuf ^= single ? 0 : 1;
           } else {
-            // the tile's 16-column tail: direct stores
+            // direct stores: a tile's 16-column tail, or tiles without bulk-tensor stores (halo
+            // conv tiles of Qt < 128 pixels)
             if (want_sum) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
             }
-            if (row_in_tile && gm < M) {
-              T* dst = reinterpret_cast<T*>(p.C) + (long long)gm * ldc + gc0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j < cmax && gc0 + j < N) dst[j] = TR::from_f(relu ? fmaxf(v[j], 0.f) : v[j]);
-            }
+            if (row_in_tile && gm < M) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
           }
         }
         ptx::tc_fence_before();
@@ -1128,7 +1157,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // no faults / fused colck / bring-up bits): the generic loop's checks, without its dispatch.
     if constexpr (CLASS == CLASS_CHECKSUM && NT > 0) {
       const bool flags_only = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
-      if (flags_only && p.tma_store && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) &&
+      if (flags_only && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) &&
           p.next_colck == nullptr && p.nfaults == 0 && p.debug == 0 && split) {
         lean = true;
         constexpr int GPC = 32 / NT;
@@ -1141,6 +1170,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M, mt = p.mt, groups = p.groups;
         const long long ldc = p.ldc;
         const bool single = p.out_single != 0;
+        const bool tma = p.tma_store != 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
           const int acc = t_local % acc_stages;
           const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
@@ -1175,7 +1205,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << (c0 / NT + gi);
               }
             }
-            if (cmax >= 32) {
+            if (cmax >= 32 && tma) {
               if (lane == 0) {
                 if (single) ptx::bulk_wait_read<0>();
                 else ptx::bulk_wait_read<1>();
@@ -1206,10 +1236,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
               sbuf ^= single ? 0 : 1;
             } else if (row_in_tile && gm < M) {
-              T* dst = reinterpret_cast<T*>(p.C) + (long long)gm * ldc + gc0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j < cmax && gc0 + j < N) dst[j] = TR::from_f(relu ? fmaxf(v[j], 0.f) : v[j]);
+              lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
             }
           }
           // fired groups of the thread tile's Mt rows -> verdicts (rare)
