@@ -370,7 +370,7 @@ def main():
     for _ in range(args.warmup):
         e2e_step()
     e2e_ts = []
-    for _ in range(max(args.steps, 50)):        # host-clock timed: at least 50 steps for a stable median
+    for _ in range(max(args.steps, 100)):       # host-clock timed: at least 100 steps for a stable median
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
