@@ -118,6 +118,12 @@ typedef struct {
    * CTA tile stays as wide as the unprotected one.  ck_rows is not used; excludes a_colck.
    * Works in every A-load mode, the halo conv included. */
   const float* lhs_rowck;
+  /* optional [partials_cap][2] fp64, global scheme: instead of adding its (lhs, rhs) partial to
+   * out_lhs / out_sum with one atomic per CTA, CTA b writes it to out_partials[b] with plain
+   * stores (no contended atomics at the kernel's tail); slots past the launch's grid must hold
+   * zeros.  abft_verify_partials sums the slots and applies the tau rule.  partials_cap must be
+   * >= the plan's grid (abft_gemm_plan out[7]; the SM count always suffices). */
+  double* out_partials; int32_t partials_cap;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
@@ -189,6 +195,10 @@ int abft_global_lhs(const abft_global_task_t* tasks /*device*/, int32_t ntasks, 
                     void* stream);
 int abft_verify_sums(const double* sums /*[n][2]*/, const int32_t* k /*device [n]*/, int32_t ntasks,
                      int32_t numeric, abft_verdict_t* out, int32_t* detected_count, void* stream);
+/* The tau rule over per-CTA partial slots: task i's (lhs, rhs) = the sum of its cap slots
+ * partials[i][0..cap) (written by abft_gemm with out_partials). */
+int abft_verify_partials(const double* partials /*[n][cap][2]*/, int32_t cap, const int32_t* k /*device [n]*/,
+                         int32_t ntasks, int32_t numeric, abft_verdict_t* out, int32_t* detected_count, void* stream);
 /* Single-GPU fast path: abft_global_lhs + abft_verify_sums fused into one launch. */
 int abft_global_verify(const abft_global_task_t* tasks, int32_t ntasks, int32_t numeric, double* sums,
                        abft_verdict_t* out, int32_t* detected_count, void* stream);

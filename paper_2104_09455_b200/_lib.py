@@ -24,6 +24,7 @@ NUM_EXACT, NUM_BINARY16, NUM_BINARY32, NUM_BF16 = 0, 1, 2, 3
 UNPROTECTED, GLOBAL, ONE_SIDED, TWO_SIDED, REPL_FULL, REPL_SINGLE = range(6)
 
 EXPORTED_SYMBOLS = (
+    "abft_verify_partials",
     "abft_struct_size",
     "abft_gemm",
     "abft_gemm_plan",
@@ -97,6 +98,7 @@ class GemmArgs(ctypes.Structure):
         ("vout", ctypes.c_void_p), ("vdetected", ctypes.c_void_p),
         ("pdl", ctypes.c_int32), ("ck_layout", ctypes.c_int32),
         ("lhs_rowck", ctypes.c_void_p),
+        ("out_partials", ctypes.c_void_p), ("partials_cap", ctypes.c_int32),
     ]
 
 
@@ -131,6 +133,7 @@ def _declare(lib):
     lib.abft_global_lhs.argtypes = [vp, i32, vp, vp]
     lib.abft_global_verify.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     lib.abft_verify_sums.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+    lib.abft_verify_partials.argtypes = [vp, i32, vp, i32, i32, vp, vp, vp]
     lib.abft_conv2d.argtypes = [ctypes.POINTER(ConvArgs), vp]
     lib.abft_conv_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]
     lib.abft_conv_gemm_plan.argtypes = [ctypes.POINTER(ConvArgs), vp]

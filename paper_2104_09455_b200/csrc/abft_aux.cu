@@ -178,6 +178,29 @@ __global__ void verify_kernel(const double* __restrict__ sums, const int* __rest
   if (v.detected && detected_count) atomicAdd(detected_count, 1);
 }
 
+// tau rule over per-CTA partial slots: one warp per task sums its cap (lhs, rhs) slots
+__global__ void verify_partials_kernel(const double* __restrict__ part, int cap, const int* __restrict__ ks, int n,
+                                       double r, abft_verdict_t* __restrict__ out, int* __restrict__ detected_count) {
+  const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const double* ti = part + (long long)i * cap * 2;
+  double lhs = 0.0, rhs = 0.0;
+  for (int b = lane; b < cap; b += 32) { lhs += ti[2 * b]; rhs += ti[2 * b + 1]; }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    lhs += __shfl_xor_sync(0xffffffffu, lhs, o);
+    rhs += __shfl_xor_sync(0xffffffffu, rhs, o);
+  }
+  if (lane != 0) return;
+  const double tol = tolerance(r, ks[i], lhs, rhs);
+  abft_verdict_t v;
+  v.lhs = lhs; v.rhs = rhs; v.tol = tol; v.k = ks[i];
+  v.detected = fabs(lhs - rhs) > tol ? 1 : 0;
+  if (out) out[i] = v;
+  if (v.detected && detected_count) atomicAdd(detected_count, 1);
+}
+
 // ------------------------------------------------------- conv companions
 // Weight [OC][Cin][R][S] (torch layout) -> K-major [OC][(r, s, c)] with c padded to ck (zeros):
 // the B^T operand of the implicit-GEMM conv, K ordered like the im2col columns.
@@ -512,4 +535,14 @@ extern "C" __attribute__((visibility("default"))) int abft_verify_sums(const dou
   verify_kernel<<<(ntasks + 127) / 128, 128, 0, as_stream(stream)>>>(sums, k, ntasks, tol_ratio(numeric), out,
                                                                      detected_count);
   return cuda_check(cudaGetLastError(), "verify launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_verify_partials(const double* partials, int32_t cap,
+                                                                          const int32_t* k, int32_t ntasks,
+                                                                          int32_t numeric, abft_verdict_t* out,
+                                                                          int32_t* detected_count, void* stream) {
+  if (ntasks < 1 || cap < 1) return fail(ABFT_E_SHAPE, "verify_partials: ntasks and cap must be >= 1");
+  verify_partials_kernel<<<(ntasks + 3) / 4, 128, 0, as_stream(stream)>>>(partials, cap, k, ntasks, tol_ratio(numeric),
+                                                                         out, detected_count);
+  return cuda_check(cudaGetLastError(), "verify_partials launch");
 }

@@ -80,6 +80,7 @@ struct GemmParams {
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
   double* out_lhs;       // global: += sum_rows A . rowck(B tile) (one checksum N-slice per tile)
+  double* out_partials;  // global: [grid][2] per-CTA (rhs, lhs) partials by plain stores (else atomics)
   const float* lhs_w;    // global: rowck(B) [ceil(K/64)*64]; lhs = sum_rows A . rowck(B) by the checksum warps
   uint32_t off_w, stage_w_bytes;   // per stage: the k-block's rowck(B) slice(s) (S x 256 B in halo mode)
   const double* vsums;   // fused deferred verification (last CTA): [vn][2] (lhs, rhs), K per layer
@@ -1070,7 +1071,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
              p.nfaults == 0 && p.debug == 0 && split;
     }
     if (lean) {
-      const bool want_sum = p.out_sum != nullptr;
+      const bool want_sum = p.out_sum != nullptr || p.out_partials != nullptr;
       const bool relu = p.relu != 0;
       const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
       const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
@@ -1403,7 +1404,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        if (p.out_sum != nullptr) {
+        if (p.out_sum != nullptr || p.out_partials != nullptr) {
           // four independent partial chains instead of one 32-deep dependent FADD chain
           float t4[4] = {0.f, 0.f, 0.f, 0.f};
           if (cmax >= 32) {
@@ -1554,7 +1555,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (stamp && et == 0) g_dbg_ts[blockIdx.x][3] = gtimer();
     // -------- per-CTA flush of the global-ABFT output summation and fused colck
-    if ((p.out_sum != nullptr || p.gck) && !(p.debug & 16777216)) {   // bit 24: bring-up, no flush
+    if ((p.out_sum != nullptr || p.out_partials != nullptr || p.gck) && !(p.debug & 16777216)) {   // bit 24: bring-up, no flush
       // one reduction round for the CTA's global-ABFT partials (rhs, lhs)
       double x = rhs_acc, y = lhs_acc;
 #pragma unroll
@@ -1581,7 +1582,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
-  if ((p.out_sum != nullptr || p.gck) && !(p.debug & 16777216) && warp == EPI_WARP0) {
+  if ((p.out_sum != nullptr || p.out_partials != nullptr || p.gck) && !(p.debug & 16777216) && warp == EPI_WARP0) {
     // one add per CTA of its (rhs, lhs) partials, by the thread that then counts the CTA done
     double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
 #pragma unroll
@@ -1590,8 +1591,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ty += __shfl_xor_sync(0xffffffffu, ty, o);
     }
     if (lane == 0 && !(p.debug & 8388608)) {     // bit 23: bring-up timing without the adds
-      if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
-      if (p.gck) atomicAdd(p.out_lhs, ty);
+      if (p.out_partials != nullptr) {
+        // slot b = (lhs, rhs) of CTA b, like the [n][2] sums
+        p.out_partials[2 * blockIdx.x] = ty;
+        p.out_partials[2 * blockIdx.x + 1] = tx;
+      } else {
+        if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
+        if (p.gck) atomicAdd(p.out_lhs, ty);
+      }
     }
   }
   if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
@@ -1814,8 +1821,11 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   }
   // global lhs: 'gdot' = CUDA-core dot of the staged A tiles with rowck(B) (lhs_rowck), else
   // 'gck' = a checksum N-slice in the MMA (checksum rows, separate or appended to the weights)
-  const bool gdot = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && a->lhs_rowck != nullptr && !as_plain;
-  const bool gck = a->scheme == ABFT_GLOBAL && a->out_lhs != nullptr && !gdot && !as_plain;
+  const bool want_lhs = a->out_lhs != nullptr || a->out_partials != nullptr;
+  const bool gdot = a->scheme == ABFT_GLOBAL && want_lhs && a->lhs_rowck != nullptr && !as_plain;
+  const bool gck = a->scheme == ABFT_GLOBAL && want_lhs && !gdot && !as_plain;
+  if (a->out_partials != nullptr && (a->scheme != ABFT_GLOBAL || a->lhs_rowck != nullptr || a->partials_cap < 1))
+    return fail(ABFT_E_VALUE, "out_partials: global scheme with the checksum-slice lhs and partials_cap >= 1");
   if (gdot && a->a_colck != nullptr) return fail(ABFT_E_VALUE, "lhs_rowck and a_colck are alternatives");
   if (gdot && (reinterpret_cast<uintptr_t>(a->lhs_rowck) & 15)) return fail(ABFT_E_VALUE, "lhs_rowck must be 16-byte aligned");
   const int split = (has_ck && a->ck_split) ? 1 : 0;
@@ -1885,6 +1895,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.nck_pad = (has_ck || gck) ? round_up(p.nck, 16) : 0;
   p.gck = gck ? 1 : 0;
   p.out_lhs = (gck || gdot) ? a->out_lhs : nullptr;
+  p.out_partials = a->scheme == ABFT_GLOBAL ? a->out_partials : nullptr;
   p.lhs_w = gdot ? a->lhs_rowck : nullptr;
   p.num_m_blocks = m_blocks;
   p.num_n_blocks = ceil_div(n_ext, p.bn_eff);
@@ -2183,7 +2194,8 @@ int validate_common(const abft_gemm_args_t* a) {
     return fail(ABFT_E_VALUE, "A and Bt must be 16-byte aligned");
   if (a->out_dtype != ABFT_OUT_NONE && (a->C == nullptr || a->ldc < a->N))
     return fail(ABFT_E_SHAPE, "C must be non-null with ldc >= N");
-  if (a->scheme == ABFT_GLOBAL && a->out_sum == nullptr) return fail(ABFT_E_VALUE, "global scheme needs out_sum");
+  if (a->scheme == ABFT_GLOBAL && a->out_sum == nullptr && a->out_partials == nullptr)
+    return fail(ABFT_E_VALUE, "global scheme needs out_sum or out_partials");
   return ABFT_OK;
 }
 
@@ -2223,6 +2235,8 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   } else {
     mo = mb;   // unused
   }
+  if (p.out_partials != nullptr && pl.grid > a->partials_cap)
+    return fail(ABFT_E_SHAPE, "out_partials: partials_cap is smaller than the launch's grid");
   cudaStream_t st = as_stream(stream);
   if (getenv("ABFT_TRACE"))
     fprintf(stderr, "[abft] M=%d N=%d K=%d scheme=%d bn=%d bn_eff=%d nb=%d tiles=%d stages=%d acc=%d cols=%d tmem=%d "

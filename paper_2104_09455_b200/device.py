@@ -43,6 +43,11 @@ def require_device():
         raise _lib.AbftLibraryError("no CUDA device visible: the B200 path has no CPU fallback")
 
 
+def sm_count() -> int:
+    """SM count of the current device (the persistent grid's upper bound)."""
+    return int(torch().cuda.get_device_properties(torch().cuda.current_device()).multi_processor_count)
+
+
 def stream_handle() -> ctypes.c_void_p:
     return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
 

@@ -24,7 +24,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
                num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
-               ck_layout: int = None, lhs_rowck=None):
+               ck_layout: int = None, lhs_rowck=None, out_partials=None):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -52,6 +52,8 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     args.a_colck = a_colck.data_ptr() if a_colck is not None else None
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
     args.lhs_rowck = lhs_rowck.data_ptr() if lhs_rowck is not None else None
+    if out_partials is not None:     # [cap, 2] fp64 per-CTA (lhs, rhs) slots
+        args.out_partials, args.partials_cap = out_partials.data_ptr(), out_partials.shape[0]
     args.pdl = int(pdl)
     vt = ()
     if verify is not None:
@@ -63,7 +65,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         vt = (vsums, vks, vdone, vout, vdet)
     # the struct holds raw device pointers: keep every tensor it points to alive with it
     args._keep = [x for x in (a, bt, out, faults, out_sum, next_colck, verdicts, fired_count, fired, ck_rows,
-                              a_colck, out_lhs, lhs_rowck) + vt if x is not None]
+                              a_colck, out_lhs, lhs_rowck, out_partials) + vt if x is not None]
     return args
 
 
@@ -214,6 +216,12 @@ def global_verify(tasks_dev, ntasks: int, numeric: int, sums, out=None, detected
 def verify_sums(sums, ks_dev, ntasks: int, numeric: int, out=None, detected_count=None) -> None:
     _lib.call("abft_verify_sums", ptr(sums), ptr(ks_dev), ntasks, numeric, ptr(out), ptr(detected_count),
               stream_handle())
+
+
+def verify_partials(partials, ks_dev, ntasks: int, numeric: int, out=None, detected_count=None) -> None:
+    """abft_verify_partials: partials [n, cap, 2] fp64 per-CTA (lhs, rhs) slots -> verdicts."""
+    _lib.call("abft_verify_partials", ptr(partials), partials.shape[1], ptr(ks_dev), ntasks, numeric, ptr(out),
+              ptr(detected_count), stream_handle())
 
 
 def zero(t) -> None:

@@ -59,8 +59,9 @@ class ProtectedChain:
     ck_split: bool = False
     faults: Optional[dict] = None        # {layer: [(row, col, delta)]}: deltas added to the fp32 accumulator
     pdl: bool = True                     # programmatic dependent launch between consecutive layers
-    # (sums [nl, 2] fp64, counters int32 [2], vdone int32 [1]) views of a ChainGroup's block: the
-    # group clears them and verifies every member's global layers in one launch
+    # (sums [nl, 2] fp64, counters int32 [2], vdone int32 [1][, partials [nl, cap, 2] fp64]) views of
+    # a ChainGroup's block: the group clears them and verifies every member's global layers in one
+    # launch; with partials, each CTA of a global layer writes its (lhs, rhs) to its own slot
     shared: Optional[tuple] = None
     layers: List[_Layer] = field(default_factory=list, init=False)
 
@@ -96,7 +97,8 @@ class ProtectedChain:
             self.vdone = self.scratch[off_cnt + 8:off_cnt + 12].view(t.int32)
         else:
             self.scratch = None
-            self.sums, self.counters, self.vdone = self.shared
+            self.sums, self.counters, self.vdone = self.shared[:3]
+        self.partials = self.shared[3] if self.shared is not None and len(self.shared) > 3 else None
         self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
         self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
         self._ks_all = t.tensor([L.k for L in self.layers], dtype=t.int32, device="cuda")
@@ -123,8 +125,11 @@ class ProtectedChain:
         if i in self._fault_dev:
             kw["faults"], kw["nfaults"] = self._fault_dev[i]
         if L.scheme is Scheme.GLOBAL_ABFT:
-            kw["out_lhs"] = self.sums[i, 0:1]
-            kw["out_sum"] = self.sums[i, 1:2]
+            if getattr(self, "partials", None) is not None:
+                kw["out_partials"] = self.partials[i]
+            else:
+                kw["out_lhs"] = self.sums[i, 0:1]
+                kw["out_sum"] = self.sums[i, 1:2]
         elif L.scheme is not Scheme.UNPROTECTED:
             kw.update(thread_m=t.thread_m, thread_n=t.thread_n, m_ext=-(-m // t.thread_m) * t.thread_m,
                       n_ext=-(-L.n // t.thread_n) * t.thread_n, tol_k=-(-L.k // t.k_step) * t.k_step,
@@ -209,14 +214,19 @@ class ChainGroup:
         total = sum(nls)
         off_cnt = 16 * total
         off_flag = off_cnt + 16 * len(specs)
-        self.block = t.zeros(off_flag + 16, dtype=t.uint8, device="cuda")
+        # per-CTA (lhs, rhs) slots of every layer: plain stores instead of contended atomics
+        self.cap = max(1, D.sm_count())
+        off_part = off_flag + 16
+        self.block = t.zeros(off_part + 16 * self.cap * total, dtype=t.uint8, device="cuda")
         self.sums = self.block[:off_cnt].view(t.float64).view(total, 2)
         cnt = self.block[off_cnt:off_flag].view(t.int32).view(len(specs), 4)
+        self.partials = self.block[off_part:].view(t.float64).view(total, self.cap, 2)
         self.chains = []
         o = 0
         for (w, b, sch), nl in zip(specs, nls):
             self.chains.append(ProtectedChain(w, b, sch, shared=(self.sums[o:o + nl], cnt[len(self.chains), 0:2],
-                                                                 cnt[len(self.chains), 2:3]), **chain_kw))
+                                                                 cnt[len(self.chains), 2:3],
+                                                                 self.partials[o:o + nl]), **chain_kw))
             o += nl
         self.counters = cnt
         ks = [L.k for ch in self.chains for L in ch.layers]
@@ -224,7 +234,7 @@ class ChainGroup:
         self.ks = t.tensor(ks, dtype=t.int32, device="cuda")
         self.verdicts = t.zeros(total * 32, dtype=t.uint8, device="cuda")
         self.flagged = self.block[off_flag:off_flag + 4].view(t.int32)
-        self.tail = self.block[off_cnt:]            # counters + flag count: one D2H read
+        self.tail = self.block[off_cnt:off_part]    # counters + flag count: one D2H read
         self.numeric = self.chains[0].numeric
 
     def begin(self) -> None:
@@ -234,8 +244,8 @@ class ChainGroup:
     def end(self) -> None:
         """One verification launch over all members' layers (non-global layers hold (0, 0))."""
         if self.has_global:
-            kernels.verify_sums(self.sums, self.ks, self.ks.numel(), self.numeric, out=self.verdicts,
-                                detected_count=self.flagged)
+            kernels.verify_partials(self.partials, self.ks, self.ks.numel(), self.numeric, out=self.verdicts,
+                                    detected_count=self.flagged)
 
     def forward(self) -> None:
         self.begin()
