@@ -211,7 +211,7 @@ def main():
                 per_batch[f"{name}/b{b}"] = dict(fixed[f"{name}/b{b}"], source=args.plan_json)
                 continue
             # per-layer times measured in the chain context the step runs them in
-            meas = profiler.profile_layers([torch.from_numpy(w).cuda() for w in ws], b, in_chain=True)
+            meas = profiler.profile_layers([torch.from_numpy(w).cuda() for w in ws], b, iters=200, in_chain=True)
             layers = [(i, GemmShape(b, w.shape[1], w.shape[0])) for i, w in enumerate(ws)]
             plan = P.select(layers, P.BINARY16, dev_profile, measured=meas)
             plans[(name, b)] = [lp.chosen for lp in plan.layers]

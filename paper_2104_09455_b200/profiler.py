@@ -92,8 +92,9 @@ def _profile_layers_in_chain(weights, batch, dtype, tiling, iters) -> MeasuredTi
     def chain_us(schemes):
         nl = len(schemes)
         block = t.zeros(16 * nl + 16, dtype=t.uint8, device="cuda")
+        partials = t.zeros((nl, max(1, D.sm_count()), 2), dtype=t.float64, device="cuda")   # as in a ChainGroup
         shared = (block[:16 * nl].view(t.float64).view(nl, 2), block[16 * nl:16 * nl + 8].view(t.int32),
-                  block[16 * nl + 8:16 * nl + 12].view(t.int32))
+                  block[16 * nl + 8:16 * nl + 12].view(t.int32), partials)
         ch = ProtectedChain(weights, batch, list(schemes), dtype, tiling, shared=shared)
         return graph_time_us(ch.forward, iters)
 
