@@ -124,6 +124,18 @@ typedef struct {
    * zeros.  abft_verify_partials sums the slots and applies the tau rule.  partials_cap must be
    * >= the plan's grid (abft_gemm_plan out[7]; the SM count always suffices). */
   double* out_partials; int32_t partials_cap;
+  /* optional [N] fp32 (16-byte aligned) per-output-column bias — a BN-folded conv / FC bias, which
+   * the reference never models (roofline.py:3-4).  Added to the fp32 accumulator after fault
+   * injection and before every checksum, sum, ReLU and store, with the exact checksum corrections
+   * (SURVEY H3): the global lhs gains sum_{rows < M} sum_j bias_j (= M * sum(bias)) so that
+   * lhs = colck(A) . rowck(B) + M * sum(bias) still equals rhs = sum(C + bias); each one-sided
+   * group's checksum column gains sum_{j in group} bias_j.  Thread-level: one-sided with
+   * thread_n 8 or 16 only (ABFT_E_UNSUPPORTED otherwise). */
+  const float* bias;
+  /* optional residual [M x N] in the storage dtype (ld_res elements, a multiple of 8, 16-byte
+   * aligned base): added after the checks and before the ReLU and the store — the shortcut of a
+   * residual block, outside the checked contraction like the reference's activation (checksum.py:235). */
+  const void* residual; int64_t ld_res;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
@@ -249,6 +261,28 @@ int abft_conv_pack_weight(const void* w, int32_t oc, int32_t cin, int32_t r, int
 int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w, int32_t c, int32_t r, int32_t s,
                     int32_t stride_h, int32_t stride_w, int32_t pad_h, int32_t pad_w, int32_t dtype, float* out,
                     int32_t accumulate, void* stream);
+
+/*
+ * Glue of a protected CNN forward (config C5).  The reference protects linear layers only and
+ * models a network by its linear-layer list (shapes.py:198-212 model_to_gemm_sequence; the
+ * overhead is taken over the linear layers), so these have no reference
+ * counterpart and carry no checks.  16-bit NHWC tensors, channels a multiple of 8, pixel
+ * strides ldx / ldo in elements (>= c, multiples of 8: a channel slice of a wider buffer works).
+ */
+/* max pooling, window k, stride, symmetric pad (<= k/2), PyTorch ceil_mode rule; out [n][P][Q] */
+int abft_nhwc_maxpool(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t k,
+                      int32_t stride, int32_t pad, int32_t ceil_mode, int32_t dtype, void* out, int64_t ldo,
+                      void* stream);
+/* global average pooling: out[n][c] = mean over the hw pixels of image n (fp32 sum) */
+int abft_nhwc_avgpool(const void* x, int32_t n, int32_t hw, int32_t c, int64_t ldx, int32_t dtype, void* out,
+                      int64_t ldo, void* stream);
+/* ShuffleNet v2: out = channel_shuffle(cat(x1, b), 2) for 2*half channels, stored in the "halves"
+ * layout: logical channels [0, half) at physical [0, half), [half, 2*half) at [half_pad, half_pad + half) */
+int abft_nhwc_interleave2(const void* x1, int64_t ld1, const void* b, int64_t ld2, int64_t pixels, int32_t half,
+                          void* out, int64_t ldo, int32_t half_pad, int32_t dtype, void* stream);
+/* per-CTA (lhs, rhs) slots [n][cap][2] (abft_gemm out_partials) -> sums [n][2]: a shard's per-layer
+ * partials, all-reduced across ranks before abft_verify_sums (batch sharding, checksum.py:237) */
+int abft_sum_partials(const double* partials, int32_t cap, int32_t ntasks, double* sums, void* stream);
 
 /* Clear a per-forward accumulator block (one graph memset node instead of a kernel). */
 int abft_zero(void* p, int64_t bytes, void* stream);

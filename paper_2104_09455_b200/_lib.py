@@ -46,6 +46,10 @@ EXPORTED_SYMBOLS = (
     "abft_last_error",
     "abft_version",
     "abft_device_sms",
+    "abft_nhwc_maxpool",
+    "abft_nhwc_avgpool",
+    "abft_nhwc_interleave2",
+    "abft_sum_partials",
 )
 
 
@@ -99,6 +103,7 @@ class GemmArgs(ctypes.Structure):
         ("pdl", ctypes.c_int32), ("ck_layout", ctypes.c_int32),
         ("lhs_rowck", ctypes.c_void_p),
         ("out_partials", ctypes.c_void_p), ("partials_cap", ctypes.c_int32),
+        ("bias", ctypes.c_void_p), ("residual", ctypes.c_void_p), ("ld_res", ctypes.c_int64),
     ]
 
 

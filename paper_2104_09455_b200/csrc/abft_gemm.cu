@@ -48,14 +48,6 @@ constexpr int DCK_BUFS = 4;        // column-sum MMA results in flight (8 TMEM c
 
 enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
 
-// bring-up instrumentation (ABFT_DEBUG & 2048): per-CTA %globaltimer stamps
-__device__ unsigned long long g_dbg_ts[160][8];
-__device__ unsigned long long g_dbg_kb[3][64];   // CTA 0, first tile: [0] load issued, [1] full seen by MMA, [2] empty seen
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 struct GemmParams {
   int M, N, K, m_ext, n_ext, tol_k;
@@ -80,7 +72,7 @@ struct GemmParams {
   float* a_colck;        // global: A column checksum accumulated from the staged A tiles (or null)
   int acolck_in_smem;    // 1: CTA-private [K] partial in smem, flushed once
   double* out_lhs;       // global: += sum_rows A . rowck(B tile) (one checksum N-slice per tile)
-  double* out_partials;  // global: [grid][2] per-CTA (rhs, lhs) partials by plain stores (else atomics)
+  double* out_partials;  // global: [grid][2] per-CTA (lhs, rhs) partials by plain stores (else atomics)
   const float* lhs_w;    // global: rowck(B) [ceil(K/64)*64]; lhs = sum_rows A . rowck(B) by the checksum warps
   uint32_t off_w, stage_w_bytes;   // per stage: the k-block's rowck(B) slice(s) (S x 256 B in halo mode)
   const double* vsums;   // fused deferred verification (last CTA): [vn][2] (lhs, rhs), K per layer
@@ -114,6 +106,13 @@ struct GemmParams {
   int* fired_count;
   int* fired;
   int fired_cap;
+  // BN-folded bias [N] fp32 (added to the accumulator after fault injection, before every check,
+  // sum and store; the checks carry the exact correction) and residual [M x N] (added after the
+  // checks, before the ReLU and the store)
+  const float* bias;
+  const void* residual;
+  long long ld_res;
+  int lhs_epi;           // 1: the epilogue contributes to the global lhs (checksum slice and/or bias term)
   uint32_t idesc_main, idesc_ck;
   // implicit-GEMM convolution (A = NHWC activation through a TMA im2col map):
   // a_mode 0 tiled GEMM A, 1 im2col 64-channel chunks (SW128), 2 im2col 8-channel chunks
@@ -126,7 +125,6 @@ struct GemmParams {
   uint32_t tx_a;         // bytes of one A box (the window), for the full-barrier count
   uint32_t b_tile_bytes; // one [b_rows x 64] B tile (a halo stage holds S of them)
   int cv_kstride;        // packed-weight channel stride (ck)
-  int debug;   // ABFT_DEBUG bits (bring-up experiments only): 1 skip verdicts, 2 skip checksum TMEM load, 4 skip checksum MMA
 };
 
 template <typename T>
@@ -330,6 +328,59 @@ __device__ __forceinline__ void apply_faults(const abft_fault_t* faults, int nfa
   }
 }
 
+// v[j] += bias[gc0 + j] for the chunk's ncols real columns (bias is 16-byte aligned, gc0 a
+// multiple of 32); returns the sum of the added bias values — the exact correction the
+// checks need: Σ_j bias_j per row for the global lhs, Σ_{j in group} bias_j per one-sided group.
+// G = 32 / group width: bg[g] receives the sum of group g's bias values (G = 1: the chunk's).
+template <int G>
+__device__ __forceinline__ void add_bias32(float (&v)[32], const float* __restrict__ bias, int gc0, int ncols,
+                                           float (&bg)[G]) {
+  constexpr int W = 32 / G;
+#pragma unroll
+  for (int g = 0; g < G; ++g) bg[g] = 0.f;
+  if (ncols >= 32) {
+    const float4* b4 = reinterpret_cast<const float4*>(bias + gc0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 t = __ldg(b4 + j);
+      v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+      bg[(4 * j) / W] += (t.x + t.y) + (t.z + t.w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float b = j < ncols ? __ldg(bias + gc0 + j) : 0.f;
+      v[j] += b;
+      bg[j / W] += b;
+    }
+  }
+}
+
+// v[j] += residual[gm][gc0 + j] (16-bit storage) for the chunk's ncols real columns
+template <typename T>
+__device__ __forceinline__ void add_residual32(float (&v)[32], const void* residual, long long ld_res, int gm, int gc0,
+                                               int ncols) {
+  using TR = ElemTraits<T>;
+  const T* src = reinterpret_cast<const T*>(residual) + (long long)gm * ld_res + gc0;
+  if (ncols >= 32) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + j);
+      const float2 f0 = TR::unpack2(u.x), f1 = TR::unpack2(u.y), f2 = TR::unpack2(u.z), f3 = TR::unpack2(u.w);
+      v[8 * j] += f0.x; v[8 * j + 1] += f0.y; v[8 * j + 2] += f1.x; v[8 * j + 3] += f1.y;
+      v[8 * j + 4] += f2.x; v[8 * j + 5] += f2.y; v[8 * j + 6] += f3.x; v[8 * j + 7] += f3.y;
+    }
+  } else {
+    const unsigned short* s16 = reinterpret_cast<const unsigned short*>(src);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < ncols) {
+        const uint32_t u = (uint32_t)__ldg(s16 + j);
+        v[j] += TR::unpack2(u).x;
+      }
+    }
+  }
+}
 
 // One row's 32-column chunk of a 16-bit output by direct stores (ReLU folded into the pack):
 // four 16-byte stores when the chunk is whole and aligned, else element by element.
@@ -401,14 +452,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr int kLines = (int)((sizeof(GemmParams) + 63) / 64);
     if (threadIdx.x < kLines) {
       const uint32_t x = reinterpret_cast<const uint32_t*>(&p)[threadIdx.x * 16];
-      if (x == 0x9E3779B9u && p.debug == 0x7fffffff) g_dbg_ts[0][7] = x;   // keeps the load (never true)
+      asm volatile("" ::"r"(x));     // the load is the point: keep it
     }
   }
   constexpr bool has_ck = CLASS == CLASS_CHECKSUM;
   constexpr bool has_shadow = CLASS == CLASS_REPLICA;
   constexpr bool thread_level = CLASS != CLASS_PLAIN;
-  const bool ck_onchip = has_ck && p.ck_mode == 1 && !(p.debug & 8);
-  const bool ck_loaded = (has_ck || p.gck) && (p.ck_mode == 2 || p.ck_mode == 4) && !(p.debug & 8);
+  const bool ck_onchip = has_ck && p.ck_mode == 1;
+  const bool ck_loaded = (has_ck || p.gck) && (p.ck_mode == 2 || p.ck_mode == 4);
   // augmented weights: B rows of N-block nb start at nb * b_rows_blk (idesc_aug = idesc_main in mode 4)
   const bool ck_aug = p.ck_mode == 3 || p.ck_mode == 4;
   // halo-reuse conv (a_mode 4) and its weight-stationary B exist only in the HALO instances,
@@ -416,8 +467,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool halo = HALO && p.a_mode == 4;
   const bool b_res = HALO && p.b_resident;
   const int bn = p.bn;
-  const bool stamp = (p.debug & 2048) && blockIdx.x < 160;
-  if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][0] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -462,7 +511,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  if (stamp && threadIdx.x == 0) g_dbg_ts[blockIdx.x][1] = gtimer();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -494,7 +542,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // the operands may be the previous kernel's outputs: wait for its completion (no-op
       // unless launched as a programmatic dependent)
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (stamp && lane == 0 && blockIdx.x == 0) g_dbg_kb[2][63] = gtimer();
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = (halo ? p.tx_a : L_stage_a_bytes) + (b_res ? 0u : (halo ? (uint32_t)L_cv_S : 1u) * L_tx_b) +
@@ -566,7 +613,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < L_nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[2][kb] = gtimer();
           ptx::mbar_arrive_expect_tx_w(&full[s], txt);
           uint8_t* a_dst = sm_a + s * L_stage_a_bytes;
           uint8_t* w_dst = smem + p.off_w + s * L_stage_w_bytes;
@@ -574,10 +620,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // window of input row (p + r - pad), columns q0 - pad .. q0 - pad + Qt + S - 2
             const int r = kb / L_cv_chunks;
             const int cc = kb - r * L_cv_chunks;
-            if (p.debug & 4194304)
-              ptx::tma_load_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img);
-            else   // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
-              ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
+            // im2col-mode walk of the padded row: Qt + S - 1 consecutive input pixels
+            ptx::tma_load_im2col_4d_w(a_dst, &tmA, &full[s], cc * BK, wo, ho + r, img, 0, 0);
             const int brow = ck_aug ? nb * L_b_rows_blk : n0;
             if (w_tile) {
 #pragma unroll 1
@@ -622,7 +666,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (w_tile) ptx::bulk_load_w(w_dst, p.lhs_w + kb * BK, 256u, &full[s]);
           if (ck_loaded)
             ptx::tma_load_2d_w(sm_ck + s * L_stage_ck_bytes, &tmCK, &full[s], kb * BK, nb * L_ck_rstride + L_ck_roff);
-          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[0][kb] = gtimer();
           if (++s == L_stages) { s = 0; ph ^= 1; }
         }
       }
@@ -657,7 +700,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // main MMAs never wait for the checksum warps.  Whole-warp loop, elected-lane issue.
     // Descriptor bases of stage 0; a stage / k-step adds a constant to the address field
     // (smem byte address >> 4, 14 bits, never carries for addresses below 256 KB).
-    const bool fast = !halo && !ck_onchip && !has_shadow && p.acolck_mode != 1 && !(p.debug & 4);
+    const bool fast = !halo && !ck_onchip && !has_shadow && p.acolck_mode != 1;
     const uint64_t a_base = a_none ? ptx::desc_kmajor_none(ptx::smem_u32(sm_a), 2048u, 128u)
                                    : ptx::desc_kmajor_sw128(ptx::smem_u32(sm_a));
     const uint64_t a_kstep = a_none ? 256ull : 2ull;
@@ -706,7 +749,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
           for (int kb = 0; kb < L_nkb; ++kb) {
             ptx::mbar_wait(&full[s], ph);
-            if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
             ptx::tc_fence_after();
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
             const uint64_t bd = b_base + (uint64_t)s * b_sstep;
@@ -726,7 +768,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
         for (int kb = 0; kb < L_nkb; ++kb) {
           ptx::mbar_wait(&full[s], ph);
-          if (stamp && lane == 0 && blockIdx.x == 0 && tile == 0 && kb < 64) g_dbg_kb[1][kb] = gtimer();
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sm_a + s * L_stage_a_bytes);
           const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * L_stage_b_bytes);
@@ -737,9 +778,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int si = 0; si < L_cv_S; ++si) {
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k) {
-                const uint32_t row_off = (p.debug & 2097152) ? 0u : (uint32_t)si * 128u;   // bring-up timing bit
-                const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + row_off + (uint32_t)k * 32u) |
-                                       (p.debug & 1048576 ? ((uint64_t)(si & 7) << 49) : 0ull);
+                const uint32_t row_off = (uint32_t)si * 128u;
+                const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + row_off + (uint32_t)k * 32u);
                 const uint32_t bt_addr = b_addr + (uint32_t)si * L_b_tile_bytes;
                 const uint64_t bdesc = ptx::desc_kmajor_sw128(bt_addr + k * 32);
                 const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
@@ -760,7 +800,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bdesc = ptx::desc_kmajor_sw128(b_addr + k * 32);
             const uint32_t accum = (kb | k) != 0;
             ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? L_idesc_aug : L_idesc_main, accum);
-            if (ck_loaded && !(p.debug & 4)) ptx::mma_f16_ss_w(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), L_idesc_ck, accum);
+            if (ck_loaded) ptx::mma_f16_ss_w(d + bn, adesc, ptx::desc_kmajor_sw128(c_addr + k * 32), L_idesc_ck, accum);
             if (has_shadow) ptx::mma_f16_ss_w(d + p.shadow_off, adesc, bdesc, L_idesc_main, accum);
           }
           if (p.acolck_mode == 1 && count_tile) {
@@ -1068,7 +1108,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     bool lean = false;
     if constexpr (CLASS == CLASS_PLAIN) {
       lean = (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) && p.next_colck == nullptr &&
-             p.nfaults == 0 && p.debug == 0 && split;
+             p.nfaults == 0 && split;
     }
     if (lean) {
       const bool want_sum = p.out_sum != nullptr || p.out_partials != nullptr;
@@ -1078,6 +1118,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const long long ldc = p.ldc;
       const bool single = p.out_single != 0;
       const bool tma = p.tma_store != 0;
+      const float* __restrict__ bias = p.bias;
+      const bool bias_lhs = bias != nullptr && p.lhs_epi;
+      const void* resid = p.residual;
+      const long long ld_res = p.ld_res;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
         const int acc = t_local % acc_stages;
         const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
@@ -1086,6 +1130,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int n0 = (tile - mb * nnb) * bn_eff;
         const int gm = m0 + row;
         const bool row_in_tile = row < bm_eff;
+        const bool row_valid = row_in_tile && gm < M;
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
@@ -1102,13 +1147,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
           const int cmax = bn_eff - c0;
           const int gc0 = n0 + c0;
-          if (cmax >= 32 && tma) {
-            if (want_sum) {
-              float t4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (bias != nullptr) {
+            float bs[1];
+            add_bias32<1>(v, bias, gc0, min(cmax, N - gc0), bs);
+            if (bias_lhs && row_valid) lhs_acc += (double)bs[0];
+          }
+          if (want_sum) {
+            float t4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (cmax >= 32) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) t4[j & 3] += v[j];
-              tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) t4[j & 3] += (j < cmax) ? v[j] : 0.f;
             }
+            tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
+          }
+          if (resid != nullptr && row_valid) add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
+          if (cmax >= 32 && tma) {
             if (lane == 0) {
               if (single) ptx::bulk_wait_read<0>();
               else ptx::bulk_wait_read<1>();
@@ -1141,17 +1197,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
             // direct stores: a tile's 16-column tail, or tiles without bulk-tensor stores (halo
             // conv tiles of Qt < 128 pixels)
-            if (want_sum) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) tsum += (j < cmax) ? v[j] : 0.f;
-            }
-            if (row_in_tile && gm < M) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
+            if (row_valid) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
           }
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        if (row_in_tile) rhs_acc += (double)tsum;
+        if (row_valid) rhs_acc += (double)tsum;
       }
     }
     // Lean one-sided path (static group width, flags-only verdicts, 16-bit bulk-tensor stores,
@@ -1159,7 +1211,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if constexpr (CLASS == CLASS_CHECKSUM && NT > 0) {
       const bool flags_only = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
       if (flags_only && (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) &&
-          p.next_colck == nullptr && p.nfaults == 0 && p.debug == 0 && split) {
+          p.next_colck == nullptr && p.nfaults == 0 && split) {
         lean = true;
         constexpr int GPC = 32 / NT;
         constexpr int GPCK = 32 / NT;
@@ -1172,6 +1224,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long ldc = p.ldc;
         const bool single = p.out_single != 0;
         const bool tma = p.tma_store != 0;
+        const float* __restrict__ bias = p.bias;
+        const void* resid = p.residual;
+        const long long ld_res = p.ld_res;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
           const int acc = t_local % acc_stages;
           const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
@@ -1196,16 +1251,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tmem_ld_wait();
             const int cmax = bn_eff - c0;
             const int gc0 = n0 + c0;
+            float bg[GPC];
+            if (bias != nullptr) add_bias32<GPC>(v, bias, gc0, min(cmax, N - gc0), bg);
 #pragma unroll
             for (int gi = 0; gi < GPC; ++gi) {
               if (gi * NT < cmax) {
                 float y = 0.f;
 #pragma unroll
                 for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
-                const float x = ck_split ? ckh[gi] + ckl[gi] : ckh[gi];
+                float x = ck_split ? ckh[gi] + ckl[gi] : ckh[gi];
+                if (bias != nullptr) x += bg[gi];
                 if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << (c0 / NT + gi);
               }
             }
+            if (resid != nullptr && row_in_tile && gm < M)
+              add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
             if (cmax >= 32 && tma) {
               if (lane == 0) {
                 if (single) ptx::bulk_wait_read<0>();
@@ -1275,10 +1335,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
-      if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][2] = gtimer();
       const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * p.cols_per_acc);
 
-      if (has_ck && NT == 0 && !(p.debug & 2) && c_first < p.bn_eff) {
+      if (has_ck && NT == 0 && c_first < p.bn_eff) {
         // checksum column per (row, group) of the groups this warp handles -> cks[slot][row]
         float hi[32], lo[32];
         __syncwarp();
@@ -1303,7 +1362,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
       // global lhs: this row's A . rowck(B tile) = checksum column hi + lo, loaded with the
       // h = 0 warps' first chunk (one TMEM load wait)
-      const bool gck_ld = p.gck && h == 0 && !(p.debug & 524288);
+      const bool gck_ld = p.gck && h == 0;
       float ck_hi = 0.f, ck_lo = 0.f;
       // one-sided, flags only (no per-tile verdict records): bitmask of fired groups of this row
       const bool flags_fast = p.scheme == ABFT_ONE_SIDED && p.verdicts == nullptr && p.shuffle_verdicts;
@@ -1317,7 +1376,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float tsum = 0.f;
 #pragma unroll 1
       for (int c0 = c_first; c0 < p.bn_eff; c0 += c_step) {
-        if (p.debug & 32768) break;      // bring-up: epilogue does nothing but hand TMEM back
         float v[32], sh[32];
         __syncwarp();
         ptx::tmem_ld32(tacc + c0, v);
@@ -1332,12 +1390,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         ptx::tmem_ld_wait();
         if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
-        if (stamp && et == 0 && t_local == 0 && c0 == 0) g_dbg_ts[blockIdx.x][5] = gtimer();
         const int gc0 = n0 + c0;
         const int cmax = p.bn_eff - c0;
         if (row_fault) apply_faults(p.faults, p.nfaults, v, gm, gc0, cmax);
-        if (p.debug & 16) {
-        } else if constexpr (thread_level && NT > 0) {
+        // bias (generic loop: scalar loads, low register pressure); per-group sums for the one-sided check
+        constexpr bool bias_ok = !has_shadow && (!thread_level || NT > 0);
+        constexpr int GB = (thread_level && NT > 0) ? 32 / NT : 1;
+        float bg[GB];
+#pragma unroll
+        for (int g2 = 0; g2 < GB; ++g2) bg[g2] = 0.f;
+        if constexpr (bias_ok) {
+          if (p.bias != nullptr) {
+            const int ncols = min(cmax, p.N - gc0);
+            float bs = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float b = j < ncols ? __ldg(p.bias + gc0 + j) : 0.f;
+              v[j] += b;
+              bg[j / (32 / GB)] += b;
+              bs += b;
+            }
+            if (p.lhs_epi && row_store) lhs_acc += (double)bs;
+          }
+        }
+        if constexpr (thread_level && NT > 0) {
           // static group structure: 32 / NT complete groups per chunk (NT divides 32 and bn_eff)
           constexpr int GPC = 32 / NT;
 #pragma unroll
@@ -1349,6 +1425,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int e = 0; e < NT; ++e) y += v[gi * NT + e];
                 x = p.split ? ckh[gi] + ckl[gi] : ckh[gi];
+                if (p.bias != nullptr) x += bg[gi];
               } else {
                 if (p.scheme == ABFT_REPL_FULL) {
                   float bk = -FLT_MAX;
@@ -1368,7 +1445,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (flags_fast) {
                 // one-sided flags-only: one fp32 compare per (row, group), folded into a bitmask
                 if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << gg;
-              } else if (!(p.debug & 1)) {
+              } else {
                 group_done(p, rec, row, lane, gg, x, y, n0, t_row, row_verdict);
               }
             }
@@ -1416,7 +1493,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
         }
-        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr) && !(p.debug & 16384)) {
+        if (p.residual != nullptr && row_store) {
+          const int ncols = min(cmax, p.N - gc0);
+          const unsigned short* r16 =
+              reinterpret_cast<const unsigned short*>(p.residual) + (long long)gm * p.ld_res + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) v[j] += TR::unpack2((uint32_t)__ldg(r16 + j)).x;
+        }
+        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
           // whole 32-column chunks go out by bulk tensor stores; a tile's 16-column tail (bn_eff = 240
@@ -1434,9 +1519,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (chunk_tma) {
             // stage the warp's [32 rows x 32 columns] in the TMA swizzle order (fp32: 128-byte
             // rows, SW128; 16-bit: 64-byte rows, SW64), then one lane issues the bulk store
-            if (p.debug & 131072) {
-              // bring-up: no staging, no store
-            } else if (p.out_dtype == ABFT_OUT_F32) {
+            if (p.out_dtype == ABFT_OUT_F32) {
               if (lane == 0) ptx::bulk_wait_read<0>();
               __syncwarp();
               uint8_t* rowp = my_stage + lane * 128;
@@ -1473,14 +1556,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
-            if (!(p.debug & (131072 | 262144))) {
-              ptx::fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0,
-                                  m0 + q * 32);
-                ptx::bulk_commit();
-              }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmC, my_stage + (p.out_dtype == ABFT_OUT_F32 ? 0 : sbuf * 2048), gc0,
+                                m0 + q * 32);
+              ptx::bulk_commit();
             }
             sbuf ^= p.out_single ? 0 : 1;
           } else if (row_store && p.out_dtype != ABFT_OUT_NONE) {
@@ -1526,7 +1607,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      if (stamp && et == 0 && t_local == 0) g_dbg_ts[blockIdx.x][6] = gtimer();
       if constexpr (has_ck && NT > 0) {
         if (flags_fast) {
           uint32_t m = row_verdict ? fmask : 0u;
@@ -1545,7 +1625,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-      if (row_in_tile) rhs_acc += (double)tsum;
+      if (row_store) rhs_acc += (double)tsum;
 
       if (thread_level && !p.shuffle_verdicts && h == 0) {
         ptx::named_bar_sync(1, 128);
@@ -1553,9 +1633,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::named_bar_sync(1, 128);
       }
     }
-    if (stamp && et == 0) g_dbg_ts[blockIdx.x][3] = gtimer();
     // -------- per-CTA flush of the global-ABFT output summation and fused colck
-    if ((p.out_sum != nullptr || p.out_partials != nullptr || p.gck) && !(p.debug & 16777216)) {   // bit 24: bring-up, no flush
+    if (p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) {
       // one reduction round for the CTA's global-ABFT partials (rhs, lhs)
       double x = rhs_acc, y = lhs_acc;
 #pragma unroll
@@ -1582,7 +1661,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
-  if ((p.out_sum != nullptr || p.out_partials != nullptr || p.gck) && !(p.debug & 16777216) && warp == EPI_WARP0) {
+  if ((p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) && warp == EPI_WARP0) {
     // one add per CTA of its (rhs, lhs) partials, by the thread that then counts the CTA done
     double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
 #pragma unroll
@@ -1590,14 +1669,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tx += __shfl_xor_sync(0xffffffffu, tx, o);
       ty += __shfl_xor_sync(0xffffffffu, ty, o);
     }
-    if (lane == 0 && !(p.debug & 8388608)) {     // bit 23: bring-up timing without the adds
+    if (lane == 0) {
       if (p.out_partials != nullptr) {
         // slot b = (lhs, rhs) of CTA b, like the [n][2] sums
         p.out_partials[2 * blockIdx.x] = ty;
         p.out_partials[2 * blockIdx.x + 1] = tx;
       } else {
         if (p.out_sum != nullptr) atomicAdd(p.out_sum, tx);
-        if (p.gck) atomicAdd(p.out_lhs, ty);
+        if (p.lhs_epi) atomicAdd(p.out_lhs, ty);
       }
     }
   }
@@ -1638,7 +1717,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (stamp && threadIdx.x == 32) g_dbg_ts[blockIdx.x][4] = gtimer();
 }
 
 // ============================================================== host side
@@ -1800,6 +1878,26 @@ int tile_cols(int bn, int nt, bool has_ck, bool has_shadow, int split) {
   return cols;
 }
 
+// Measurement overrides, read from the environment once per process (never on the launch path):
+// ABFT_NUM_SMS caps the persistent grid, ABFT_KPAIR=0 disables k-block pairs, ABFT_SMEM_CAP (KB)
+// caps the shared-memory carve-up, ABFT_CONV_MODE forces a conv A-load mode, ABFT_TRACE prints plans.
+struct EnvOverrides {
+  int num_sms = 0, kpair = 1, smem_cap_kb = 0, conv_mode = -1;
+  bool trace = false;
+};
+const EnvOverrides& env_overrides() {
+  static const EnvOverrides e = [] {
+    EnvOverrides o;
+    if (const char* v = getenv("ABFT_NUM_SMS")) o.num_sms = std::max(1, atoi(v));
+    if (const char* v = getenv("ABFT_KPAIR")) o.kpair = atoi(v) != 0;
+    if (const char* v = getenv("ABFT_SMEM_CAP")) o.smem_cap_kb = atoi(v);
+    if (const char* v = getenv("ABFT_CONV_MODE")) o.conv_mode = atoi(v);
+    o.trace = getenv("ABFT_TRACE") != nullptr;
+    return o;
+  }();
+  return e;
+}
+
 // Choose the CTA tile and carve shared memory / TMEM for one call.
 int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr) {
   const bool halo = cg != nullptr && cg->a_mode == 4;
@@ -1807,11 +1905,10 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   if (a->M < 1 || a->N < 1 || a->K < 1) return fail(ABFT_E_SHAPE, "GEMM extents must be >= 1");
   if (a->dtype != ABFT_F16 && a->dtype != ABFT_BF16) return fail(ABFT_E_VALUE, "dtype must be ABFT_F16 or ABFT_BF16");
   if (a->scheme < ABFT_UNPROTECTED || a->scheme > ABFT_REPL_SINGLE) return fail(ABFT_E_VALUE, "unknown scheme");
-  const int dbg_env = getenv("ABFT_DEBUG") ? atoi(getenv("ABFT_DEBUG")) : 0;
-  const bool as_plain = (dbg_env & 1024) != 0;
-  const bool thread_level = a->scheme >= ABFT_ONE_SIDED && !as_plain;
-  const bool has_ck = (a->scheme == ABFT_ONE_SIDED || a->scheme == ABFT_TWO_SIDED) && !as_plain;
-  const bool has_shadow = (a->scheme == ABFT_REPL_FULL || a->scheme == ABFT_REPL_SINGLE) && !as_plain;
+  const EnvOverrides& ov = env_overrides();
+  const bool thread_level = a->scheme >= ABFT_ONE_SIDED;
+  const bool has_ck = a->scheme == ABFT_ONE_SIDED || a->scheme == ABFT_TWO_SIDED;
+  const bool has_shadow = a->scheme == ABFT_REPL_FULL || a->scheme == ABFT_REPL_SINGLE;
   const int mt = thread_level ? a->thread_m : 1, nt = thread_level ? a->thread_n : 1;
   const int m_ext = thread_level ? a->m_ext : a->M, n_ext = thread_level ? a->n_ext : a->N;
   if (thread_level) {
@@ -1822,18 +1919,18 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   // global lhs: 'gdot' = CUDA-core dot of the staged A tiles with rowck(B) (lhs_rowck), else
   // 'gck' = a checksum N-slice in the MMA (checksum rows, separate or appended to the weights)
   const bool want_lhs = a->out_lhs != nullptr || a->out_partials != nullptr;
-  const bool gdot = a->scheme == ABFT_GLOBAL && want_lhs && a->lhs_rowck != nullptr && !as_plain;
-  const bool gck = a->scheme == ABFT_GLOBAL && want_lhs && !gdot && !as_plain;
+  const bool gdot = a->scheme == ABFT_GLOBAL && want_lhs && a->lhs_rowck != nullptr;
+  const bool gck = a->scheme == ABFT_GLOBAL && want_lhs && !gdot;
   if (a->out_partials != nullptr && (a->scheme != ABFT_GLOBAL || a->lhs_rowck != nullptr || a->partials_cap < 1))
     return fail(ABFT_E_VALUE, "out_partials: global scheme with the checksum-slice lhs and partials_cap >= 1");
   if (gdot && a->a_colck != nullptr) return fail(ABFT_E_VALUE, "lhs_rowck and a_colck are alternatives");
   if (gdot && (reinterpret_cast<uintptr_t>(a->lhs_rowck) & 15)) return fail(ABFT_E_VALUE, "lhs_rowck must be 16-byte aligned");
   const int split = (has_ck && a->ck_split) ? 1 : 0;
   // global scheme with the activation checksum: 2 x 64 TMEM columns for the column-sum MMA
-  const bool want_acolck = a->a_colck != nullptr && (a->scheme == ABFT_GLOBAL || as_plain) && !(dbg_env & 131072);
+  const bool want_acolck = a->a_colck != nullptr && a->scheme == ABFT_GLOBAL;
   const int extra_cols = want_acolck ? 32 : 0;
   int sms = a->num_sms > 0 ? a->num_sms : num_sms();
-  if (const char* e = getenv("ABFT_NUM_SMS")) sms = std::max(1, atoi(e));     // bring-up: grid cap
+  if (ov.num_sms > 0) sms = ov.num_sms;
   const int bm_eff = halo ? cg->Qt : (BM / mt) * mt;
   if (halo && bm_eff % mt) return fail(ABFT_E_UNSUPPORTED, "halo tile is not a multiple of the thread tile");
   const int m_blocks = ceil_div(m_ext, bm_eff);
@@ -1943,20 +2040,26 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.idesc_ck = (has_ck || gck) ? ptx::idesc_f16(fmt, BM, p.nck_pad) : 0u;
   p.idesc_ones = ptx::idesc_f16(fmt, 64, 8) | (1u << 15);    // M=64, N=8, A MN-major
   p.idesc_aug = p.ck_mode == 4 ? p.idesc_main : ptx::idesc_f16(fmt, BM, (uint32_t)(bn + p.nck_pad));
-  {
-    const char* dbg = getenv("ABFT_DEBUG");
-    p.debug = dbg ? atoi(dbg) : 0;
-    if (p.debug & 32) p.tmem_cols = 512;
-    if (p.debug & 256) {
-      p.cols_per_acc = round_up(p.cols_per_acc, 64);
-      p.acc_stages = (2 * p.cols_per_acc <= 512) ? 2 : 1;
-      p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
-    }
-    if (p.debug & 512) { p.acc_stages = 1; }
-  }
   out.cls = has_ck ? CLASS_CHECKSUM : has_shadow ? CLASS_REPLICA : CLASS_PLAIN;
   // static group width when it divides both the 32-column chunk and the tile
   out.ntc = (thread_level && (nt == 8 || nt == 16) && p.bn_eff % 32 == 0) ? nt : 0;
+  // bias / residual epilogue (BN-folded networks)
+  if (a->bias != nullptr) {
+    if (reinterpret_cast<uintptr_t>(a->bias) & 15) return fail(ABFT_E_VALUE, "bias must be 16-byte aligned");
+    if (a->scheme == ABFT_GLOBAL && !want_lhs)
+      return fail(ABFT_E_UNSUPPORTED, "bias with the global scheme needs the in-kernel lhs (out_lhs / out_partials)");
+    if (thread_level && (a->scheme != ABFT_ONE_SIDED || out.ntc == 0))
+      return fail(ABFT_E_UNSUPPORTED, "bias with a thread-level check needs the one-sided scheme with thread_n 8 or 16");
+  }
+  if (a->residual != nullptr) {
+    if (a->out_dtype == ABFT_OUT_NONE) return fail(ABFT_E_VALUE, "residual needs an output");
+    if ((reinterpret_cast<uintptr_t>(a->residual) & 15) || a->ld_res % 8 || a->ld_res < a->N)
+      return fail(ABFT_E_VALUE, "residual must be 16-byte aligned with ld_res >= N and a multiple of 8");
+  }
+  p.bias = a->bias;
+  p.residual = a->residual;
+  p.ld_res = a->ld_res;
+  p.lhs_epi = (gck || (a->bias != nullptr && a->scheme == ABFT_GLOBAL && want_lhs)) ? 1 : 0;
 
   // ---- shared memory carve-up (all tile buffers 1024-aligned)
   p.stage_a_bytes = BM * BK * 2;
@@ -1974,7 +2077,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1 || cg->a_mode == 3) &&
              (p.ck_mode == 0 || p.ck_mode == 3) &&
              !has_shadow && !want_acolck && a->lhs_rowck == nullptr && p.nkb >= 2 &&
-             !(getenv("ABFT_KPAIR") && atoi(getenv("ABFT_KPAIR")) == 0)) ? 1 : 0;
+             ov.kpair) ? 1 : 0;
   if (p.kpair) {
     // only while the pipeline keeps >= 3 stages of pairs (tiles up to ~128 columns: the
     // latency-bound GEMMs); wide tiles keep single k-block stages
@@ -1996,21 +2099,20 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // of the tile is stored directly), 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
     p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 16 == 0 &&
-                   ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0) &&
-                   !(dbg_env & 8192)) ? 1 : 0;
+                   ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0)) ? 1 : 0;
   }
   uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
   // chunks split across both warps of a quadrant unless a check needs whole rows in one warp
-  p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) && !(dbg_env & 65536) ? 1 : 0;
+  p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) ? 1 : 0;
   if (a->a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
-  p.a_colck = (a->scheme == ABFT_GLOBAL || as_plain) ? a->a_colck : nullptr;
+  p.a_colck = a->scheme == ABFT_GLOBAL ? a->a_colck : nullptr;
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
   const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : 0u;
   const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
   const uint32_t extras0 = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + acolck_bytes + ones_bytes + bar_bytes;
-  const int smem_cap = getenv("ABFT_SMEM_CAP") ? std::min(max_smem_optin() - 1024, atoi(getenv("ABFT_SMEM_CAP")) * 1024)
-                                              : max_smem_optin() - 1024 /*alignment slack*/;
+  const int smem_cap = ov.smem_cap_kb > 0 ? std::min(max_smem_optin() - 1024, ov.smem_cap_kb * 1024)
+                                          : max_smem_optin() - 1024 /*alignment slack*/;
   p.out_single = 0;
   {
     // 16-bit outputs: one 2 KB staging buffer per epilogue warp instead of two when that buys
@@ -2032,7 +2134,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const long long b_all = (long long)p.nkb * p.stage_b_bytes;
   p.b_resident = (halo && p.num_n_blocks == 1 && p.num_tiles > 1 && p.ck_mode != 1 && p.ck_mode != 2 && p.ck_mode != 4 &&
                   !has_shadow &&
-                  b_all + 4LL * p.stage_a_bytes <= budget && !(dbg_env & 262144)) ? 1 : 0;
+                  b_all + 4LL * p.stage_a_bytes <= budget) ? 1 : 0;
   p.stage_w_bytes = p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u;
   const uint32_t stage_bytes =
       p.stage_a_bytes + (p.b_resident ? 0u : p.stage_b_bytes) + p.stage_ck_bytes + p.stage_w_bytes;
@@ -2146,12 +2248,6 @@ extern "C" __attribute__((visibility("default"))) int abft_aug_weights(const voi
   return cuda_check(cudaGetLastError(), "aug_weights launch");
 }
 
-extern "C" __attribute__((visibility("default"))) int abft_debug_timestamps(unsigned long long* host_out /*[160*8 + 3*64]*/) {
-  int rc = cuda_check(cudaMemcpyFromSymbol(host_out, g_dbg_ts, sizeof(g_dbg_ts)), "debug timestamps");
-  if (rc != ABFT_OK) return rc;
-  return cuda_check(cudaMemcpyFromSymbol(host_out + 160 * 8, g_dbg_kb, sizeof(g_dbg_kb)), "debug timestamps");
-}
-
 extern "C" __attribute__((visibility("default"))) int abft_gemm_plan(const abft_gemm_args_t* a, int32_t* out) {
   Plan pl;
   int rc = make_plan(a, pl);
@@ -2238,14 +2334,12 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   if (p.out_partials != nullptr && pl.grid > a->partials_cap)
     return fail(ABFT_E_SHAPE, "out_partials: partials_cap is smaller than the launch's grid");
   cudaStream_t st = as_stream(stream);
-  if (getenv("ABFT_TRACE"))
+  if (env_overrides().trace)
     fprintf(stderr, "[abft] M=%d N=%d K=%d scheme=%d bn=%d bn_eff=%d nb=%d tiles=%d stages=%d acc=%d cols=%d tmem=%d "
             "nck=%d ck_mode=%d gck=%d tma_store=%d split=%d a_mode=%d smem=%zu grid=%d cls=%d ntc=%d\n",
             p.M, p.N, p.K, p.scheme, p.bn, p.bn_eff, p.num_n_blocks, p.num_tiles, p.stages, p.acc_stages,
             p.cols_per_acc, p.tmem_cols, p.nck_pad, p.ck_mode, p.gck, p.tma_store, p.epi_split, p.a_mode, pl.smem,
             pl.grid, pl.cls, pl.ntc);
-  if (p.debug & 64) pl.cls = CLASS_PLAIN;
-  if (p.debug & 4096) pl.smem = (size_t)max_smem_optin();
   if (a->dtype == ABFT_BF16)
     return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
   return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
@@ -2280,7 +2374,7 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   const bool pointwise = c->r == 1 && c->s == 1 && c->stride_h == 1 && c->stride_w == 1 && c->pad_h == 0 && c->pad_w == 0;
   g.cr = c->c_real > 0 ? c->c_real : c->c;
   if (g.cr > c->c) return fail(ABFT_E_SHAPE, "c_real exceeds the physical channel count");
-  const char* force = getenv("ABFT_CONV_MODE");     // bring-up / measurement override
+  const int force = env_overrides().conv_mode;     // measurement override (-1: none)
   int mode = pointwise ? 0 : (c->c % 64 == 0 ? 1 : (c->c >= 48 ? 1 : 3));
   // halo reuse (mode 4): stride 1, a tile of Qt | Q output pixels in one output row, so every
   // filter row's S taps come from one input-row window; needs checksum rows appended to the
@@ -2289,7 +2383,8 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   {
     const bool thread_level = c->gemm.scheme >= ABFT_ONE_SIDED;
     const bool ck_ok = c->gemm.scheme == ABFT_UNPROTECTED ||
-                       (c->gemm.scheme == ABFT_GLOBAL ? (c->gemm.out_lhs == nullptr || c->gemm.ck_layout == 1 ||
+                       (c->gemm.scheme == ABFT_GLOBAL ? ((c->gemm.out_lhs == nullptr && c->gemm.out_partials == nullptr) ||
+                                                         c->gemm.ck_layout == 1 ||
                                                          c->gemm.lhs_rowck != nullptr)
                                                       : c->gemm.ck_layout == 1);   // plan == launch
     const int mt = thread_level ? std::max(1, c->gemm.thread_m) : 1;
@@ -2300,8 +2395,8 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
       if (g.Qt) mode = 4;
     }
   }
-  if (force && !pointwise) {
-    const int fm = atoi(force);
+  if (force >= 0 && !pointwise) {
+    const int fm = force;
     if (fm != 4 || g.Qt) mode = fm;
     if (fm == 4 && !g.Qt) mode = c->c % 64 == 0 || c->c >= 48 ? 1 : 3;
   }
@@ -2438,8 +2533,7 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
     p.cv_kstride = g.ck;
     // A: the input-row window of Qt + S - 1 pixels.  Default: an im2col-mode map whose "filter"
     // is 1x1 over the zero-padded image (bounding box [-pad, W + pad) per row), so the walk of
-    // Qt + S - 1 pixels from (q0 - pw, p + r - ph) stays inside one padded row; debug bit
-    // 4194304: a 4-D tiled map with the same box.
+    // Qt + S - 1 pixels from (q0 - pw, p + r - ph) stays inside one padded row.
     const cuuint64_t C = (cuuint64_t)c->c;
     cuuint64_t dims[4] = {C, (cuuint64_t)c->w, (cuuint64_t)c->h, (cuuint64_t)c->n};
     cuuint64_t strides[3] = {C * 2, C * 2 * (cuuint64_t)c->w, C * 2 * (cuuint64_t)c->w * (cuuint64_t)c->h};
@@ -2447,14 +2541,7 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
     CUresult r;
     const CUtensorMapDataType dt =
         c->gemm.dtype == ABFT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    if (p.debug & 4194304) {
-      auto enc = get_encode_fn();
-      if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)(g.Qt + c->s - 1), 1u, 1u};
-      cuuint32_t estr[4] = {1, 1, 1, 1};
-      r = enc(&ma, dt, 4, const_cast<void*>(c->gemm.A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    } else {
+    {
       auto enc = get_im2col_fn();
       if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeIm2col unavailable from the driver");
       int lower[2] = {-c->pad_w, -c->pad_h};

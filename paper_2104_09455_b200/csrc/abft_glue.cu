@@ -1,0 +1,212 @@
+// abft_glue.cu — the non-linear glue between the protected layers of a CNN forward (config C5),
+// plus the per-CTA partial reduction the batch-sharded verification all-reduces.
+//
+// The reference protects linear layers only and models a network as its linear-layer list
+// (shapes.py:198-212, model_to_gemm_sequence); the layers in between (pooling, channel shuffle)
+// are not checked, here as in the paper (overhead over the linear layers).  They
+// run on the NHWC activations the protected kernels produce, into buffers planned once, so a
+// whole forward is one stream of launches that a CUDA graph captures.  All are HBM-bound:
+// 16-byte (8-channel) vectors per thread where the layout allows it.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "abft_common.cuh"
+
+namespace abft {
+
+template <typename T>
+struct Max2;
+template <>
+struct Max2<__half> {
+  static __device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b) {
+    __half2 r = __hmax2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+  static constexpr uint32_t lowest = 0xFC00FC00u;   // -inf, -inf
+};
+template <>
+struct Max2<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b) {
+    __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+  static constexpr uint32_t lowest = 0xFF80FF80u;
+};
+
+// out[n][p][q][c] = max over the window (padding never wins), one 8-channel vector per thread
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
+                                                           int P, int Q, int k, int s, int pad, T* __restrict__ out,
+                                                           long long ldo, long long total_vec) {
+  const int cv = C / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total_vec;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long long pix = i / cv;
+    const int q = (int)(pix % Q);
+    pix /= Q;
+    const int p = (int)(pix % P);
+    const long long n = pix / P;
+    uint4 m = make_uint4(Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest);
+    const int h0 = p * s - pad, w0 = q * s - pad;
+    for (int dh = 0; dh < k; ++dh) {
+      const int hh = h0 + dh;
+      if (hh < 0 || hh >= H) continue;
+      for (int dw = 0; dw < k; ++dw) {
+        const int ww = w0 + dw;
+        if (ww < 0 || ww >= W) continue;
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + ((n * H + hh) * W + ww) * ldx + c8 * 8));
+        m.x = Max2<T>::op(m.x, u.x);
+        m.y = Max2<T>::op(m.y, u.y);
+        m.z = Max2<T>::op(m.z, u.z);
+        m.w = Max2<T>::op(m.w, u.w);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + ((n * P + p) * Q + q) * ldo + c8 * 8) = m;
+  }
+}
+
+// out[n][c] = mean over the H*W pixels of image n (fp32 sum, rounded once); CTA = (image, 256-vector slab)
+template <typename T>
+__global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const T* __restrict__ x, int HW, int C, long long ldx,
+                                                           T* __restrict__ out, long long ldo) {
+  __shared__ float part[8][8 * 32];
+  const int cv = C / 8;
+  const long long n = blockIdx.x;
+  const int v0 = blockIdx.y * 32;
+  const int vi = threadIdx.x & 31, rg = threadIdx.x >> 5;   // 32 vectors x 8 pixel groups
+  const int v = v0 + vi;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (v < cv) {
+    for (int px = rg; px < HW; px += 8) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + (n * HW + px) * ldx + v * 8));
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += (float)e[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[rg][vi * 8 + j] = acc[j];
+  __syncthreads();
+  const int c = threadIdx.x;   // 256 channels of this slab
+  if (v0 * 8 + c < C) {
+    float s = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) s += part[g][c];
+    out[n * ldo + v0 * 8 + c] = (T)(s / (float)HW);
+  }
+}
+
+// ShuffleNet v2 unit output: channel_shuffle(cat(x1, b), 2) — logical channel 2i + g is x1[i]
+// (g = 0) or b[i] (g = 1); stored in the "halves" layout (logical channels [0, C/2) at physical
+// [0, C/2), [C/2, C) at physical [half_pad, half_pad + C/2)) so the next unit's chunk(2) halves
+// are 16-byte aligned channel slices.  One (x1[i], b[i]) pair -> one 4-byte store per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) interleave2_kernel(const T* __restrict__ x1, long long ld1,
+                                                          const T* __restrict__ b, long long ld2, int half,
+                                                          T* __restrict__ out, long long ldo, int half_pad,
+                                                          long long total) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long pix = t / half;
+    const int i = (int)(t - pix * half);
+    const int l = 2 * i;   // even: the pair never straddles the half boundary (half is even)
+    const int phys = l < half ? l : half_pad + (l - half);
+    T pair[2] = {x1[pix * ld1 + i], b[pix * ld2 + i]};
+    *reinterpret_cast<uint32_t*>(out + pix * ldo + phys) = *reinterpret_cast<uint32_t*>(pair);
+  }
+}
+
+// [n][cap][2] per-CTA (lhs, rhs) slots -> [n][2] sums (fp64), for the batch-sharded all-reduce
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int cap, int ntasks, double* __restrict__ sums) {
+  const int task = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (task >= ntasks) return;
+  double l = 0.0, r = 0.0;
+  for (int i = lane; i < cap; i += 32) {
+    l += partials[((long long)task * cap + i) * 2];
+    r += partials[((long long)task * cap + i) * 2 + 1];
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  if (lane == 0) {
+    sums[2 * task] = l;
+    sums[2 * task + 1] = r;
+  }
+}
+
+int grid_for(long long work) {
+  return (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, 16LL * num_sms()));
+}
+
+}  // namespace abft
+
+using namespace abft;
+
+extern "C" __attribute__((visibility("default"))) int abft_nhwc_maxpool(const void* x, int32_t n, int32_t h, int32_t w,
+                                                                       int32_t c, int64_t ldx, int32_t k, int32_t stride,
+                                                                       int32_t pad, int32_t ceil_mode, int32_t dtype,
+                                                                       void* out, int64_t ldo, void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || k < 1 || stride < 1 || pad < 0 || 2 * pad > k)
+    return fail(ABFT_E_SHAPE, "maxpool: bad extents (channels a multiple of 8, pad <= k/2)");
+  if (ldx < c || ldx % 8 || ldo < c || ldo % 8) return fail(ABFT_E_SHAPE, "maxpool: ldx/ldo must be >= c and a multiple of 8");
+  auto osz = [&](int len) {
+    const int num = len + 2 * pad - k;
+    int o = (ceil_mode ? (num + stride - 1) / stride : num / stride) + 1;
+    if (ceil_mode && (o - 1) * stride >= len + pad) --o;   // the last window must start inside the input
+    return o;
+  };
+  const int P = osz(h), Q = osz(w);
+  if (P < 1 || Q < 1) return fail(ABFT_E_SHAPE, "maxpool: empty output");
+  const long long total = (long long)n * P * Q * (c / 8);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == ABFT_BF16)
+    maxpool_nhwc_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k,
+                                                                         stride, pad, (__nv_bfloat16*)out, ldo, total);
+  else
+    maxpool_nhwc_kernel<__half><<<grid_for(total), 256, 0, st>>>((const __half*)x, h, w, c, ldx, P, Q, k, stride, pad,
+                                                                  (__half*)out, ldo, total);
+  return cuda_check(cudaGetLastError(), "maxpool launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_nhwc_avgpool(const void* x, int32_t n, int32_t hw, int32_t c,
+                                                                       int64_t ldx, int32_t dtype, void* out, int64_t ldo,
+                                                                       void* stream) {
+  if (n < 1 || hw < 1 || c < 8 || c % 8 || ldx < c || ldx % 8 || ldo < c)
+    return fail(ABFT_E_SHAPE, "avgpool: bad extents (channels a multiple of 8)");
+  dim3 grid((unsigned)n, (unsigned)((c / 8 + 31) / 32));
+  cudaStream_t st = as_stream(stream);
+  if (dtype == ABFT_BF16)
+    avgpool_nhwc_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, hw, c, ldx, (__nv_bfloat16*)out, ldo);
+  else
+    avgpool_nhwc_kernel<__half><<<grid, 256, 0, st>>>((const __half*)x, hw, c, ldx, (__half*)out, ldo);
+  return cuda_check(cudaGetLastError(), "avgpool launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(const void* x1, int64_t ld1, const void* b,
+                                                                           int64_t ld2, int64_t pixels, int32_t half,
+                                                                           void* out, int64_t ldo, int32_t half_pad,
+                                                                           int32_t dtype, void* stream) {
+  if (pixels < 1 || half < 2 || half % 2 || half_pad < half || half_pad % 2 || ldo < half_pad + half || ld1 < half ||
+      ld2 < half)
+    return fail(ABFT_E_SHAPE, "interleave2: bad extents (half even, half_pad >= half)");
+  const long long total = pixels * half;
+  cudaStream_t st = as_stream(stream);
+  // 16-bit elements either way: the kernel only moves them
+  (void)dtype;
+  interleave2_kernel<__half><<<grid_for(total), 256, 0, st>>>((const __half*)x1, ld1, (const __half*)b, ld2, half,
+                                                               (__half*)out, ldo, half_pad, total);
+  return cuda_check(cudaGetLastError(), "interleave2 launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_sum_partials(const double* partials, int32_t cap,
+                                                                       int32_t ntasks, double* sums, void* stream) {
+  if (ntasks < 1 || cap < 1) return fail(ABFT_E_SHAPE, "sum_partials: ntasks and cap must be >= 1");
+  sum_partials_kernel<<<(ntasks + 3) / 4, 128, 0, as_stream(stream)>>>(partials, cap, ntasks, sums);
+  return cuda_check(cudaGetLastError(), "sum_partials launch");
+}

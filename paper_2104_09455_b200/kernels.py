@@ -24,7 +24,8 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                tol_k: int = 0, faults=None, nfaults: int = 0, out_sum=None, next_colck=None, verdicts=None,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
                num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
-               ck_layout: int = None, lhs_rowck=None, out_partials=None):
+               ck_layout: int = None, lhs_rowck=None, out_partials=None, bias=None, residual=None,
+               ld_res: int = 0):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -53,7 +54,19 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     args.out_lhs = out_lhs.data_ptr() if out_lhs is not None else None
     args.lhs_rowck = lhs_rowck.data_ptr() if lhs_rowck is not None else None
     if out_partials is not None:     # [cap, 2] fp64 per-CTA (lhs, rhs) slots
+        t = torch()
+        if out_partials.dtype != t.float64 or not out_partials.is_contiguous() or out_partials.dim() != 2 \
+                or out_partials.shape[1] != 2:
+            raise ValueError("out_partials must be a contiguous float64 [cap, 2] tensor")
+        if out_sum is not None or out_lhs is not None:
+            raise ValueError("out_partials replaces out_sum / out_lhs; pass one or the other")
         args.out_partials, args.partials_cap = out_partials.data_ptr(), out_partials.shape[0]
+    if bias is not None:             # [>= N] fp32 per-column bias (BN folded)
+        if bias.dtype != torch().float32 or not bias.is_contiguous():
+            raise ValueError("bias must be a contiguous float32 tensor")
+        args.bias = bias.data_ptr()
+    if residual is not None:         # [M x N] storage-dtype shortcut, added before the ReLU
+        args.residual, args.ld_res = residual.data_ptr(), (ld_res or residual.stride(0))
     args.pdl = int(pdl)
     vt = ()
     if verify is not None:
@@ -65,7 +78,8 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         vt = (vsums, vks, vdone, vout, vdet)
     # the struct holds raw device pointers: keep every tensor it points to alive with it
     args._keep = [x for x in (a, bt, out, faults, out_sum, next_colck, verdicts, fired_count, fired, ck_rows,
-                              a_colck, out_lhs, lhs_rowck, out_partials) + vt if x is not None]
+                              a_colck, out_lhs, lhs_rowck, out_partials, bias, residual) + vt
+                  if x is not None]
     return args
 
 
@@ -227,3 +241,27 @@ def verify_partials(partials, ks_dev, ntasks: int, numeric: int, out=None, detec
 def zero(t) -> None:
     """cudaMemsetAsync of a whole (contiguous) tensor on the current stream."""
     _lib.call("abft_zero", ptr(t), t.numel() * t.element_size(), stream_handle())
+
+
+# ---------------------------------------------------------------- CNN glue (abft_glue.cu)
+def maxpool_nhwc(x, n: int, h: int, w: int, c: int, ldx: int, k: int, stride: int, pad: int, ceil_mode: bool,
+                 dtype: DType, out, ldo: int) -> None:
+    _lib.call("abft_nhwc_maxpool", ptr(x), n, h, w, c, ctypes.c_int64(ldx), k, stride, pad, int(ceil_mode),
+              storage_code(dtype), ptr(out), ctypes.c_int64(ldo), stream_handle())
+
+
+def avgpool_nhwc(x, n: int, hw: int, c: int, ldx: int, dtype: DType, out, ldo: int) -> None:
+    _lib.call("abft_nhwc_avgpool", ptr(x), n, hw, c, ctypes.c_int64(ldx), storage_code(dtype), ptr(out),
+              ctypes.c_int64(ldo), stream_handle())
+
+
+def interleave2(x1, ld1: int, b, ld2: int, pixels: int, half: int, out, ldo: int, half_pad: int,
+                dtype: DType) -> None:
+    _lib.call("abft_nhwc_interleave2", ptr(x1), ctypes.c_int64(ld1), ptr(b), ctypes.c_int64(ld2),
+              ctypes.c_int64(pixels), half, ptr(out), ctypes.c_int64(ldo), half_pad, storage_code(dtype),
+              stream_handle())
+
+
+def sum_partials(partials, ntasks: int, sums) -> None:
+    """[n, cap, 2] per-CTA (lhs, rhs) slots -> sums [n, 2] fp64 (one launch)."""
+    _lib.call("abft_sum_partials", ptr(partials), partials.shape[1], ntasks, ptr(sums), stream_handle())

@@ -38,12 +38,13 @@ from .shapes import BINARY16, DType
 
 @dataclass
 class _Layer:
-    k: int            # padded K (multiple of 8)
+    k: int            # padded K (multiple of 8): the GEMM launch's K
     n: int            # padded N (multiple of 8)
     pw: D.PreparedWeight
     scheme: Scheme
     ck_rows: object = None
     relu: bool = True
+    k_ref: int = 0    # the model's unpadded K: the global scheme's tau K (checksum.py:147-153)
 
 
 @dataclass
@@ -81,7 +82,7 @@ class ProtectedChain:
                 raise ValueError(f"layer {i}: K={k} does not chain with the previous N={prev_n}")
             pw = D.prepare_weight(w, self.dtype)
             self.layers.append(_Layer(k=kp, n=D.round8(n), pw=pw, scheme=sch,
-                                      relu=(i < len(self.weights) - 1) or self.relu_last))
+                                      relu=(i < len(self.weights) - 1) or self.relu_last, k_ref=k))
             prev_n = D.round8(n)
         m = self.batch
         self.x = t.zeros((m, self.layers[0].k), dtype=sd, device="cuda")
@@ -101,8 +102,8 @@ class ProtectedChain:
         self.partials = self.shared[3] if self.shared is not None and len(self.shared) > 3 else None
         self.verdict_buf = t.zeros(max(nl, 1) * 32, dtype=t.uint8, device="cuda")
         self.global_ids = [i for i, L in enumerate(self.layers) if L.scheme is Scheme.GLOBAL_ABFT]
-        self._ks_all = t.tensor([L.k for L in self.layers], dtype=t.int32, device="cuda")
-        self._ks = t.tensor([self.layers[i].k for i in self.global_ids] or [0], dtype=t.int32, device="cuda")
+        self._ks_all = t.tensor([L.k_ref for L in self.layers], dtype=t.int32, device="cuda")
+        self._ks = t.tensor([self.layers[i].k_ref for i in self.global_ids] or [0], dtype=t.int32, device="cuda")
         # offline checksum rows: the global scheme's lhs slice (always), and the one-sided
         # check's rows where the plan says B tiles are re-read by several M-blocks
         for i, L in enumerate(self.layers):
@@ -158,7 +159,10 @@ class ProtectedChain:
 
     # ---- multi-GPU helpers (batch sharding): per-layer partial sums, all-reduced by the caller
     def global_partials(self):
-        """[n_global, 2] fp64 (lhs, rhs) of this shard, valid after forward() on the stream."""
+        """[n_global, 2] fp64 (lhs, rhs) of this shard, valid after forward() on the stream.
+        A ChainGroup member's global layers write per-CTA slots (``partials``), summed here."""
+        if self.partials is not None:
+            return self.partials[self.global_ids].sum(dim=1)
         return self.sums[self.global_ids]
 
     def verify_reduced(self, sums):
@@ -229,7 +233,7 @@ class ChainGroup:
                                                                  self.partials[o:o + nl]), **chain_kw))
             o += nl
         self.counters = cnt
-        ks = [L.k for ch in self.chains for L in ch.layers]
+        ks = [L.k_ref for ch in self.chains for L in ch.layers]
         self.has_global = any(ch.global_ids for ch in self.chains)
         self.ks = t.tensor(ks, dtype=t.int32, device="cuda")
         self.verdicts = t.zeros(total * 32, dtype=t.uint8, device="cuda")

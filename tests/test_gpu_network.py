@@ -1,0 +1,155 @@
+"""Whole-network protected inference (config C5) on the GPU: every protected conv / FC layer
+of a real (BN-folded) torchvision CNN against an fp32 checker of the same layer on the same
+input, the network's logits against the torch fp32 forward of the original model, zero false
+positives on clean runs under every scheme, and injected faults flagged at exactly the layer
+that holds them (deferred verification, checksum.py:198-237; fault model tiled.py:197-200)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+NETS = ["resnet50", "vgg16", "squeezenet1_0", "shufflenet_v2_x1_0", "alexnet"]
+
+
+@pytest.fixture(scope="module")
+def PN():
+    from paper_2104_09455_b200 import device, protected_network
+    device.require_device()
+    return protected_network
+
+
+def _logical(act):
+    """Act -> NCHW fp32 tensor of its logical channels."""
+    import torch
+    idx = torch.as_tensor(act.phys_map(), device=act.buf.device, dtype=torch.long)
+    return act.buf.index_select(3, idx).float().permute(0, 3, 1, 2)
+
+
+def check_layer(L):
+    """The layer's output vs torch fp32 conv of ITS input with the fp16-rounded folded weights:
+    fp32-accumulation reordering + one fp16 rounding of the output."""
+    import torch
+    import torch.nn.functional as F
+    x = _logical(L.x)
+    wq = L.weight.half().float()
+    bias = L.bias if L.bias is not None else None
+    if L.kind == "fc":
+        x = x.reshape(x.shape[0], -1, 1, 1)
+    ref = F.conv2d(x, wq, bias, stride=L.stride, padding=L.pad)
+    bound = F.conv2d(x.abs(), wq.abs(), None, stride=L.stride, padding=L.pad)
+    if bias is not None:
+        bound = bound + bias.abs().view(1, -1, 1, 1)
+    if L.residual is not None:
+        r = _logical(L.residual)
+        ref = ref + r
+        bound = bound + r.abs()
+    if L.relu:
+        ref = torch.relu(ref)
+    out = _logical(L.out)
+    if L.kind == "fc":
+        out = out.reshape(ref.shape)
+    tol = 2e-5 * bound + ref.abs() * 2.0 ** -10 + 1e-6
+    err = (out - ref).abs()
+    bad = (err > tol)
+    assert not bool(bad.any()), (f"{L.name}: {int(bad.sum())} of {bad.numel()} outside tolerance, "
+                                 f"max err {float(err.max()):.3e}, max |ref| {float(ref.abs().max()):.3e}")
+    return float((err / (tol)).max())
+
+
+def _input(batch, seed=0, h=224, w=224):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.rand((batch, 3, h, w), generator=g, device="cuda") * 2 - 1).half()
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_network_layers_logits_and_clean_flags(PN, name):
+    import torch
+    S = PN.Scheme
+    model = PN.build_model(name)
+    batch = 2
+    net = PN.ProtectedNetwork(model, batch)
+    x = _input(batch)
+    # reference: the original (unfolded) model in fp32 on the same fp16-rounded input, and the
+    # torch fp16 forward as the yardstick for fp16 storage error
+    with torch.no_grad():
+        ref32 = model.float().cuda()(x.float()).float()
+        ref16 = model.half().cuda()(x).float()
+    model.float()
+    for scheme in (S.UNPROTECTED, S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
+        net.set_schemes(scheme)
+        out = net.forward(x).float()
+        torch.cuda.synchronize()
+        assert net.flags() == (0, 0), (scheme, net.flags())
+        for L in net.layers:
+            check_layer(L)
+        err = float((out - ref32).abs().max().detach())
+        err16 = float((ref16 - ref32).abs().max())
+        scale = float(ref32.abs().max())
+        assert err <= 4 * err16 + 2e-3 * scale, (scheme, err, err16, scale)
+        if scheme is S.GLOBAL_ABFT:
+            vs = net.verdicts()
+            assert all(v is not None and not v.detected for v in vs)
+            # lhs and rhs agree far inside tau on clean runs (bias correction exact)
+            assert max(abs(v.lhs - v.rhs) / v.tolerance_used for v in vs) < 0.05
+
+
+@pytest.mark.parametrize("scheme", ["global-abft", "thread-one-sided"])
+def test_network_fault_flags_the_right_layer(PN, scheme):
+    """A single-element fault in one layer (K < 1024: above that the reference tau of
+    checksum.py:143-148 grows with the fault itself) is flagged at that layer only."""
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model("resnet50"), 2, schemes=S(scheme))
+    x = _input(2)
+    net.forward(x)
+    clean = net.verdicts()
+    targets = [L for L in net.layers if L.k_ref <= 600 and L.kind == "conv"][:6]
+    assert targets
+    for L in targets:
+        tau = 1.0
+        if scheme == "global-abft":
+            tau = clean[L.index].tolerance_used
+        delta = 8.0 * tau + 64.0
+        row, col = (L.m * 3) // 7, (L.oc * 5) // 9
+        net.inject({L.index: [(row, col, delta)]})
+        net.forward(x)
+        fired, flagged = net.flags()
+        if scheme == "global-abft":
+            vs = net.verdicts()
+            got = [i for i, v in enumerate(vs) if v.detected]
+            assert got == [L.index], (L.name, got)
+            assert flagged == 1 and fired == 0
+        else:
+            assert fired >= 1 and flagged == 0, (L.name, fired, flagged)
+    net.inject({})
+    net.forward(x)
+    assert net.flags() == (0, 0)
+
+
+def test_network_real_extents_resnet50_b32(PN):
+    """ResNet-50 at batch 32: the stem's explicit-im2col mode, halo-reuse 3x3 layers at
+    56x56x64, strided downsamples and the 2048->1000 FC at a real batch, layer by layer."""
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model("resnet50"), 32)
+    x = _input(32, seed=1)
+    for scheme in (S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
+        net.set_schemes(scheme)
+        net.forward(x)
+        assert net.flags() == (0, 0)
+        for L in net.layers:
+            check_layer(L)
+
+
+def test_network_graph_replay_matches_eager(PN):
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model("squeezenet1_0"), 4, schemes=S.GLOBAL_ABFT)
+    x = _input(4, seed=2)
+    eager = net.forward(x).clone()
+    g = PN.GraphedNetwork(net)
+    net.load_input(x)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(net.logits(), eager)
+    assert net.flags() == (0, 0)

@@ -1,6 +1,6 @@
 """Per-shape timing of the sm_100a protected GEMM vs cuBLAS (torch.matmul), graph-replayed.
 
-usage: python tools/gemm_sweep.py [--stamps]   -> one line per shape:
+usage: python tools/gemm_sweep.py   -> one line per shape:
   M N K | cuBLAS us | unprotected | global | one-sided(on-chip) | one-sided(offline ck) | TFLOP/s of unprotected
 """
 import ctypes
@@ -66,54 +66,6 @@ def run(m, n, k):
           f" glob={gplan['tile_n']}/{gplan['stages']}st", flush=True)
 
 
-def stamps(m, n, k):
-    lib = _lib.load()
-    os.environ["ABFT_DEBUG"] = "2048"
-    a = (torch.rand((m, k), device="cuda") - 0.5).half()
-    b = (torch.rand((k, n), device="cuda") - 0.5).half()
-    pw = D.prepare_weight(b, P.BINARY16)
-    out = torch.empty((m, n), dtype=torch.float16, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-    buf = (ctypes.c_ulonglong * (160 * 8 + 3 * 64))()
-    one_kw = dict(m_ext=-(-m // 16) * 16, n_ext=n, fired_count=cnt)
-    oplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.THREAD_ONE_SIDED, plan_only=True,
-                         ck_layout=1, out=out, ldc=n, out_kind="f16", relu=True, **one_kw)
-    one_kw["ck_rows"] = kernels.aug_weights(pw.bt, n, k, P.BINARY16, oplan, 8, False)
-    osum = torch.zeros(2, dtype=torch.float64, device="cuda")
-    gk = dict(out_sum=osum[1:2], out_lhs=osum[0:1])
-    gplan = kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, plan_only=True,
-                         ck_layout=1, out=out, ldc=n, out_kind="f16", relu=True, **gk)
-    gk["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.BINARY16, gplan)
-    for name, sch, kw in [("unprot", P.Scheme.UNPROTECTED, {}), ("global", P.Scheme.GLOBAL_ABFT, gk),
-                          ("global_rhs_only", P.Scheme.GLOBAL_ABFT, dict(out_sum=osum[1:2])),
-                          ("onesided", P.Scheme.THREAD_ONE_SIDED, one_kw)]:
-        for _ in range(3):
-            kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, sch, out=out, ldc=n, out_kind="f16",
-                         relu=True, **kw)
-            torch.cuda.synchronize()
-        lib.abft_debug_timestamps(buf)
-        allts = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
-        ts = allts[:160 * 8].reshape(160, 8)
-        kbt = allts[160 * 8:].reshape(3, 64)
-        nkb = min(64, -(-k // 64))
-        t00 = ts[0, 0]
-        print(f"  cta0 per-kb (ns from entry): issued {(kbt[0, :nkb] - t00).tolist()}", flush=True)
-        print(f"  cta0 per-kb full seen by MMA {(kbt[1, :nkb] - t00).tolist()}", flush=True)
-        print(f"  cta0 per-kb empty passed     {(kbt[2, :nkb] - t00).tolist()} after griddep.wait {kbt[2, 63] - t00}", flush=True)
-        nct = min(160, int((ts[:, 0] > 0).sum()))
-        ts = ts[:nct]
-        rel = ts[:, :7] - ts[:, 0].min()
-        print(f"stamps {name} {m}x{n}x{k}: entry,setup,tfull0,epi_end,exit,ld0,tile0_done (ns) "
-              f"median {np.median(rel, axis=0).astype(int).tolist()} max {rel.max(axis=0).tolist()}", flush=True)
-    os.environ.pop("ABFT_DEBUG")
-
-
 if __name__ == "__main__":
-    if "--stamps" in sys.argv:
-        stamps(2048, 512, 512)
-        stamps(128, 64, 512)
-        stamps(2048, 512, 16)
-        if "--only-stamps" in sys.argv:
-            sys.exit(0)
     for s in SHAPES:
         run(*s)
