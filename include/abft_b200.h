@@ -136,6 +136,12 @@ typedef struct {
    * aligned base): added after the checks and before the ReLU and the store — the shortcut of a
    * residual block, outside the checked contraction like the reference's activation (checksum.py:235). */
   const void* residual; int64_t ld_res;
+  /* plan hints (0 = the planner's choice): bit 0 = no k-block pairs (one k-block per pipeline stage,
+   * deeper pipeline); bit 1 = Bt is zero-padded to >= round_up(N, 256) rows, so the weight map covers
+   * whole tiles (no out-of-bounds boxes); bit 2 = two output staging buffers per epilogue warp even
+   * when one would buy a pipeline stage.  The profilers time the alternatives and keep the fastest
+   * (T_o = min over plans). */
+  int32_t plan_flags;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);

@@ -104,6 +104,7 @@ class GemmArgs(ctypes.Structure):
         ("lhs_rowck", ctypes.c_void_p),
         ("out_partials", ctypes.c_void_p), ("partials_cap", ctypes.c_int32),
         ("bias", ctypes.c_void_p), ("residual", ctypes.c_void_p), ("ld_res", ctypes.c_int64),
+        ("plan_flags", ctypes.c_int32),
     ]
 
 

@@ -1019,7 +1019,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0 && part != 0.0) {
+      if (p.out_partials != nullptr) {
+        // into the CTA's (lhs, rhs) slot with the epilogue's partials (after the final barrier)
+        if (lane == 0) red_d[16 + (warp - CK_WARP0)] = part;
+      } else if (lane == 0 && part != 0.0) {
         atomicAdd(p.out_lhs, part);
         __threadfence();
       }
@@ -1664,8 +1667,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if ((p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) && warp == EPI_WARP0) {
     // one add per CTA of its (rhs, lhs) partials, by the thread that then counts the CTA done
     double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
+    // the checksum warps' CUDA-core lhs (lhs_rowck) joins the per-CTA slot
+    if (p.out_partials != nullptr && p.lhs_w != nullptr && lane >= 8 && lane < 12) ty = red_d[16 + lane - 8];
 #pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) {
+    for (int o = 8; o >= 1; o >>= 1) {
       tx += __shfl_xor_sync(0xffffffffu, tx, o);
       ty += __shfl_xor_sync(0xffffffffu, ty, o);
     }
@@ -1921,8 +1926,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const bool want_lhs = a->out_lhs != nullptr || a->out_partials != nullptr;
   const bool gdot = a->scheme == ABFT_GLOBAL && want_lhs && a->lhs_rowck != nullptr;
   const bool gck = a->scheme == ABFT_GLOBAL && want_lhs && !gdot;
-  if (a->out_partials != nullptr && (a->scheme != ABFT_GLOBAL || a->lhs_rowck != nullptr || a->partials_cap < 1))
-    return fail(ABFT_E_VALUE, "out_partials: global scheme with the checksum-slice lhs and partials_cap >= 1");
+  if (a->out_partials != nullptr && (a->scheme != ABFT_GLOBAL || a->partials_cap < 1))
+    return fail(ABFT_E_VALUE, "out_partials: global scheme and partials_cap >= 1");
   if (gdot && a->a_colck != nullptr) return fail(ABFT_E_VALUE, "lhs_rowck and a_colck are alternatives");
   if (gdot && (reinterpret_cast<uintptr_t>(a->lhs_rowck) & 15)) return fail(ABFT_E_VALUE, "lhs_rowck must be 16-byte aligned");
   const int split = (has_ck && a->ck_split) ? 1 : 0;
@@ -2077,7 +2082,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1 || cg->a_mode == 3) &&
              (p.ck_mode == 0 || p.ck_mode == 3) &&
              !has_shadow && !want_acolck && a->lhs_rowck == nullptr && p.nkb >= 2 &&
-             ov.kpair) ? 1 : 0;
+             ov.kpair && !(a->plan_flags & 1)) ? 1 : 0;
   if (p.kpair) {
     // only while the pipeline keeps >= 3 stages of pairs (tiles up to ~128 columns: the
     // latency-bound GEMMs); wide tiles keep single k-block stages
@@ -2120,7 +2125,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     const uint32_t stage_bytes0 = p.stage_a_bytes + p.stage_b_bytes + p.stage_ck_bytes +
                                   (p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u);
     const int room = smem_cap - (int)extras0 - (p.lhs_w != nullptr ? 1024 : 0);
-    if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo &&
+    // (not for few-k-block tiles: their epilogue, not the mainloop, is the critical path; plan_flags
+    // bit 2 keeps both buffers regardless)
+    if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo && p.nkb >= 4 && !(a->plan_flags & 4) &&
         (room - (int)(8u * 2048u)) / (int)stage_bytes0 > (room - (int)out_bytes) / (int)stage_bytes0 &&
         (room - (int)out_bytes) / (int)stage_bytes0 < 8) {
       p.out_single = 1;
@@ -2310,7 +2317,10 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
     // ignored checksum columns) by a second box
     if (rc == ABFT_OK && p.ck_mode == 4) rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
   } else {
-    rc = cached_map(&mb, a->Bt, a->dtype, a->K, a->N, a->ldbt, p.bn);
+    // plan_flags bit 1: Bt holds zero rows up to a whole number of tiles, so the weight boxes never
+    // cross the tensor's edge (no out-of-bounds fill on the load path)
+    const int64_t b_rows = (a->plan_flags & 2) ? (int64_t)round_up(a->N, p.bn) : (int64_t)a->N;
+    rc = cached_map(&mb, a->Bt, a->dtype, a->K, b_rows, a->ldbt, p.bn);
   }
   if (rc != ABFT_OK) return rc;
   if (p.ck_mode == 2) {
@@ -2336,10 +2346,11 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   cudaStream_t st = as_stream(stream);
   if (env_overrides().trace)
     fprintf(stderr, "[abft] M=%d N=%d K=%d scheme=%d bn=%d bn_eff=%d nb=%d tiles=%d stages=%d acc=%d cols=%d tmem=%d "
-            "nck=%d ck_mode=%d gck=%d tma_store=%d split=%d a_mode=%d smem=%zu grid=%d cls=%d ntc=%d\n",
+            "nck=%d ck_mode=%d gck=%d tma_store=%d split=%d a_mode=%d smem=%zu grid=%d cls=%d ntc=%d kpair=%d single=%d "
+            "bres=%d\n",
             p.M, p.N, p.K, p.scheme, p.bn, p.bn_eff, p.num_n_blocks, p.num_tiles, p.stages, p.acc_stages,
             p.cols_per_acc, p.tmem_cols, p.nck_pad, p.ck_mode, p.gck, p.tma_store, p.epi_split, p.a_mode, pl.smem,
-            pl.grid, pl.cls, pl.ntc);
+            pl.grid, pl.cls, pl.ntc, p.kpair, p.out_single, p.b_resident);
   if (a->dtype == ABFT_BF16)
     return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
   return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);

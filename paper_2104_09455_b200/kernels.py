@@ -25,7 +25,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
                num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
                ck_layout: int = None, lhs_rowck=None, out_partials=None, bias=None, residual=None,
-               ld_res: int = 0):
+               ld_res: int = 0, plan_flags: int = 0):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -67,6 +67,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         args.bias = bias.data_ptr()
     if residual is not None:         # [M x N] storage-dtype shortcut, added before the ReLU
         args.residual, args.ld_res = residual.data_ptr(), (ld_res or residual.stride(0))
+    args.plan_flags = int(plan_flags)
     args.pdl = int(pdl)
     vt = ()
     if verify is not None:

@@ -44,6 +44,8 @@ from .schemes import Scheme, TilingConfig
 from .shapes import BINARY16, DType, GemmShape
 
 SELECTABLE = (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED)
+GLOBAL_DOT = "global-dot"      # argument-set key of the global scheme with the checksum-warp lhs
+ARG_KEYS = SELECTABLE + (GLOBAL_DOT,)
 _VERDICT_DTYPE = np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"), ("det", "<i4"), ("k", "<i4")])
 
 
@@ -114,6 +116,9 @@ class LinearLayer:
     m: int = 0
     args: Dict = field(default_factory=dict)
     fault_args: Dict = field(default_factory=dict)
+    tile_n: Dict = field(default_factory=dict)     # per-scheme CTA tile override (0 / absent: planner's)
+    flags: Dict = field(default_factory=dict)      # per-scheme plan hints (abft_gemm_args_t.plan_flags)
+    gvar: str = "slice"       # global-ABFT lhs: "slice" (checksum MMA N-slice) or "dot" (checksum warps)
 
     @property
     def oc(self) -> int:
@@ -269,9 +274,12 @@ class ProtectedNetwork:
         L.gemm_path = L.r == 1 and L.s == 1 and L.stride == 1 and L.pad == 0
         wq = wp.to(self.sd)
         L._bias_dev = bias
+        rows_pad = -(-oc8 // 256) * 256     # packed weights carry zero rows to whole tiles (plan_flags bit 1)
         if L.gemm_path:
             L._a = x.matrix()
-            L._bt = wq.view(oc8, x.cp).contiguous()
+            L._bt_pad = t.zeros((rows_pad, x.cp), dtype=self.sd, device="cuda")
+            L._bt_pad[:oc8] = wq.view(oc8, x.cp)
+            L._bt = L._bt_pad[:oc8]
             L._k = x.cp
         else:
             if x.ld != x.cp:
@@ -287,21 +295,30 @@ class ProtectedNetwork:
                 if L.c_real > pl["ck"] or bool((wq[:, pl["ck"]:] != 0).any()):
                     raise ValueError(f"{L.name}: weights on channels past the packed {pl['ck']}")
                 wq = wq[:, :pl["ck"]].contiguous()
-            L._bt = kernels.conv_pack_weight(wq, pl["ck"], pl["k"])
+            packed = kernels.conv_pack_weight(wq, pl["ck"], pl["k"])
+            L._bt_pad = t.zeros((rows_pad, packed.shape[1]), dtype=self.sd, device="cuda")
+            L._bt_pad[:oc8] = packed
+            L._bt = L._bt_pad[:oc8]
             L._k = pl["k"]
         L._c = L.out.matrix()
         L._res = L.residual.matrix() if L.residual is not None else None
-        for sch in SELECTABLE:
-            L.args[sch] = self._make_args(L, sch)
+        # rowck(B) in the packed K layout, zero-padded to whole 64-column k-blocks: the "dot" lhs
+        L._rowck = kernels.weight_rowck(L._bt, oc8, L._k, self.dtype)
+        for key in ARG_KEYS:
+            L.args[key] = self._make_args(L, key)
 
-    def _kw(self, L: LinearLayer, scheme: Scheme, faults=None) -> dict:
+    def _kw(self, L: LinearLayer, key, faults=None) -> dict:
+        scheme = Scheme.GLOBAL_ABFT if key == GLOBAL_DOT else key
         tl = self.tiling
         kw = dict(out=L._c, ldc=L.out.ld, out_kind="bf16" if self.sd == self.t.bfloat16 else "f16", relu=L.relu,
-                  bias=L._bias_dev, residual=L._res, ld_res=L.residual.ld if L.residual is not None else 0)
+                  bias=L._bias_dev, residual=L._res, ld_res=L.residual.ld if L.residual is not None else 0,
+                  tile_n=L.tile_n.get(key, 0), plan_flags=L.flags.get(key, 0))
         if faults is not None:
             kw["faults"], kw["nfaults"] = faults
         if scheme is Scheme.GLOBAL_ABFT:
             kw["out_partials"] = self.partials[L.index]
+            if key == GLOBAL_DOT:
+                kw["lhs_rowck"] = L._rowck
         elif scheme is Scheme.THREAD_ONE_SIDED:
             oc8 = _r8(L.oc)
             kw.update(thread_m=tl.thread_m, thread_n=tl.thread_n, m_ext=-(-L.m // tl.thread_m) * tl.thread_m,
@@ -324,10 +341,11 @@ class ProtectedNetwork:
             return kernels.gemm(*a, plan_only=True, **k2)
         return kernels.conv_gemm_plan(a)
 
-    def _make_args(self, L: LinearLayer, scheme: Scheme, faults=None):
-        kw = self._kw(L, scheme, faults)
+    def _make_args(self, L: LinearLayer, key, faults=None):
+        kw = self._kw(L, key, faults)
+        scheme = Scheme.GLOBAL_ABFT if key == GLOBAL_DOT else key
         oc8 = _r8(L.oc)
-        if scheme is Scheme.GLOBAL_ABFT:
+        if key is Scheme.GLOBAL_ABFT:
             if not hasattr(L, "_gck"):
                 L._gck = kernels.global_ck_rows(L._bt, oc8, L._k, self.dtype, self._plan(L, scheme, kw))
             kw["ck_rows"] = L._gck
@@ -341,9 +359,40 @@ class ProtectedNetwork:
             return ("gemm", kernels._gemm_args(*a, **k2))
         return ("conv", a)
 
-    def launch(self, L: LinearLayer, scheme: Optional[Scheme] = None) -> None:
-        scheme = L.scheme if scheme is None else scheme
-        kind, args = L.fault_args.get(scheme) or L.args[scheme]
+    def plan_of(self, L: LinearLayer, scheme: Scheme) -> dict:
+        """The kernel plan (tile_n, stages, grid, ...) a layer launches with under `scheme`."""
+        return self._plan(L, scheme, self._kw(L, scheme))
+
+    def set_tile(self, L: LinearLayer, key, tile_n: int, flags: int = 0) -> None:
+        """Force the CTA tile (0: the planner's choice) and plan hints of one layer's launch under
+        `key` (a Scheme or GLOBAL_DOT)."""
+        old = (L.tile_n.get(key, 0), L.flags.get(key, 0))
+        L.tile_n[key], L.flags[key] = int(tile_n), int(flags)
+        try:
+            L.args[key] = self._make_args(L, key)
+        except Exception:
+            L.tile_n[key], L.flags[key] = old
+            raise
+
+    def config_of(self, L: LinearLayer, key) -> tuple:
+        return L.tile_n.get(key, 0), L.flags.get(key, 0)
+
+    def set_global_variant(self, L: LinearLayer, variant: str) -> None:
+        """The global-ABFT lhs source of one layer: "slice" (an extra MMA N-slice against the weight
+        tile's row sums) or "dot" (the checksum warps dot each staged A tile with rowck(B) on CUDA
+        cores; the CTA tile stays as wide as the unprotected one)."""
+        if variant not in ("slice", "dot"):
+            raise ValueError("global variant is 'slice' or 'dot'")
+        L.gvar = variant
+
+    @staticmethod
+    def _key(L: LinearLayer, scheme: Scheme):
+        return GLOBAL_DOT if scheme is Scheme.GLOBAL_ABFT and L.gvar == "dot" else scheme
+
+    def launch(self, L: LinearLayer, scheme=None) -> None:
+        """One layer's kernel under `scheme` (default: the layer's), or under GLOBAL_DOT explicitly."""
+        key = self._key(L, L.scheme if scheme is None else scheme) if scheme != GLOBAL_DOT else GLOBAL_DOT
+        kind, args = L.fault_args.get(key) or L.args[key]
         if kind == "gemm":
             kernels._lib.check(kernels._lib.load().abft_gemm(kernels.ctypes.byref(args), D.stream_handle()))
         else:
@@ -377,8 +426,8 @@ class ProtectedNetwork:
                 continue
             ft = D.faults_tensor(list(cells))
             L._fault_keep = ft
-            for sch in SELECTABLE:
-                L.fault_args[sch] = self._make_args(L, sch, faults=ft)
+            for key in ARG_KEYS:
+                L.fault_args[key] = self._make_args(L, key, faults=ft)
 
     # ---------------------------------------------------------------- forward
     def load_input(self, x) -> None:
@@ -399,6 +448,17 @@ class ProtectedNetwork:
         if verify:
             self.verify()
         return self.logits()
+
+    def forward_glue(self) -> None:
+        """Only the glue ops of a forward (pooling / shuffle): subtracted from whole-forward times to
+        get the overhead over the linear layers alone."""
+        for op in self.ops:
+            if not isinstance(op, LinearLayer):
+                op.fn()
+
+    def n_launches(self) -> int:
+        """Kernel launches of one forward (layers, glue, the verification launch)."""
+        return len(self.ops) + int(any(L.scheme is Scheme.GLOBAL_ABFT for L in self.layers))
 
     def verify(self) -> None:
         if any(L.scheme is Scheme.GLOBAL_ABFT for L in self.layers):
@@ -445,6 +505,36 @@ class ProtectedNetwork:
 
     def gemm_layers(self):
         return [(L.index, L.gemm_shape()) for L in self.layers]
+
+
+def verify_sharded_many(nets: Sequence[ProtectedNetwork], group=None, _cache={}) -> None:
+    """Batch-sharded verification of several networks with ONE all-reduce: every network's
+    per-layer (lhs, rhs) sums and fired-tile count, then each network's verdicts from the
+    full-batch sums (exactly the single-GPU verdicts; checksum.py:237)."""
+    import torch.distributed as dist
+    t = D.torch()
+    key = tuple(id(n) for n in nets)
+    buf = _cache.get(key)
+    sizes = [2 * len(n.layers) + 1 for n in nets]
+    if buf is None:
+        buf = _cache[key] = t.zeros(sum(sizes), dtype=t.float64, device="cuda")
+    o = 0
+    for n, sz in zip(nets, sizes):
+        nl = len(n.layers)
+        kernels.sum_partials(n.partials, nl, n.sums)
+        buf[o:o + 2 * nl].copy_(n.sums.view(-1))
+        buf[o + 2 * nl:o + sz].copy_(n.counters[0:1])
+        o += sz
+    dist.all_reduce(buf, group=group)
+    o = 0
+    for n, sz in zip(nets, sizes):
+        nl = len(n.layers)
+        n.sums.view(-1).copy_(buf[o:o + 2 * nl])
+        n.counters[0:1].copy_(buf[o + 2 * nl:o + sz])
+        n.counters[1:2].zero_()
+        if any(L.scheme is Scheme.GLOBAL_ABFT for L in n.layers):
+            kernels.verify_sums(n.sums, n.ks, nl, n.numeric, out=n.verdict_buf, detected_count=n.counters[1:2])
+        o += sz
 
 
 class GraphedNetwork:

@@ -1,0 +1,133 @@
+"""Config C2 (DLRM MLP-Bottom 13-512-256-64 and MLP-Top 512-512-256-1 at batch 1..2048) as the
+bench's secondary section: per-layer schemes from the reference selector fed by in-chain B200
+timings, all 24 chains as one ChainGroup in one CUDA graph per policy, the ABFT overhead of IG /
+always-global / always-thread over the unprotected kernels, and protected TFLOP/s.
+
+Also the workload of ``bench.py --impl reference``'s C2 leg (the oracle port of
+run_protected_pipeline, checksum.py:198-237)."""
+
+from __future__ import annotations
+
+import statistics
+
+BOTTOM = [13, 512, 256, 64]
+TOP = [512, 512, 256, 1]
+BATCHES = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048]
+SEED = 0
+
+
+def dims_padded(dims):
+    return [(-(-d // 8) * 8) for d in dims]
+
+
+def make_weights(dims, rng):
+    """U(-0.5, 0.5) fp16 weights of the padded layer dims (x8 padding, shapes.pad_gemm)."""
+    import numpy as np
+    p = dims_padded(dims)
+    ws = []
+    for i in range(len(dims) - 1):
+        w = np.zeros((p[i], p[i + 1]), dtype=np.float16)
+        w[:dims[i], :dims[i + 1]] = rng.uniform(-0.5, 0.5, size=(dims[i], dims[i + 1])).astype(np.float16)
+        ws.append(w)
+    return ws
+
+
+def workload():
+    import numpy as np
+    rng = np.random.default_rng(SEED)
+    mlps = {"bottom": make_weights(BOTTOM, rng), "top": make_weights(TOP, rng)}
+    inputs = {}
+    for name, dims in (("bottom", BOTTOM), ("top", TOP)):
+        for b in BATCHES:
+            x = np.zeros((b, dims_padded(dims)[0]), dtype=np.float16)
+            x[:, :dims[0]] = rng.uniform(-0.5, 0.5, size=(b, dims[0])).astype(np.float16)
+            inputs[(name, b)] = x
+    return mlps, inputs
+
+
+def step_flops(mlps):
+    return sum(sum(2 * b * w.shape[0] * w.shape[1] for w in ws) for ws in mlps.values() for b in BATCHES)
+
+
+def run(dev_profile, steps: int = 20, warmup: int = 3, profile_iters: int = 100) -> dict:
+    """Compact C2 summary on the current GPU (no printing)."""
+    import torch
+
+    import paper_2104_09455_b200 as P
+    from paper_2104_09455_b200 import profiler
+    from paper_2104_09455_b200.network import ChainGroup
+    from paper_2104_09455_b200.shapes import GemmShape
+
+    S = P.Scheme
+    mlps, inputs = workload()
+    flops = step_flops(mlps)
+    plans = {}
+    for name, ws in mlps.items():
+        for b in BATCHES:
+            meas = profiler.profile_layers([torch.from_numpy(w).cuda() for w in ws], b, iters=profile_iters,
+                                           in_chain=True)
+            layers = [(i, GemmShape(b, w.shape[1], w.shape[0])) for i, w in enumerate(ws)]
+            plan = P.select(layers, P.BINARY16, dev_profile, measured=meas)
+            plans[(name, b)] = [lp.chosen for lp in plan.layers]
+    wt = {name: [torch.from_numpy(w).cuda() for w in ws] for name, ws in mlps.items()}
+    keys = list(inputs)
+    policies = {"unprotected": lambda k: [S.UNPROTECTED] * 3, "global": lambda k: [S.GLOBAL_ABFT] * 3,
+                "thread": lambda k: [S.THREAD_ONE_SIDED] * 3, "ig": lambda k: plans[k]}
+    groups = {pol: ChainGroup([(wt[k[0]], k[1], f(k)) for k in keys]) for pol, f in policies.items()}
+    for grp in groups.values():
+        for k, ch in zip(keys, grp.chains):
+            ch.x.copy_(torch.from_numpy(inputs[k]).cuda())
+
+    def capture(grp):
+        main = torch.cuda.Stream()
+        streams = [torch.cuda.Stream() for _ in grp.chains]
+        main.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(main):
+            grp.forward()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=main):
+            grp.begin()
+            for s, ch in zip(streams, grp.chains):
+                s.wait_stream(main)
+                with torch.cuda.stream(s):
+                    ch.forward()
+                main.wait_stream(s)
+            grp.end()
+        torch.cuda.synchronize()
+        return g
+
+    graphs = {pol: capture(grp) for pol, grp in groups.items()}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    res = {pol: [] for pol in graphs}
+    for g in graphs.values():
+        for _ in range(warmup):
+            g.replay()
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        for pol, g in graphs.items():        # interleaved: clock drift hits every policy alike
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            res[pol].append(e0.elapsed_time(e1))
+    ms = {pol: statistics.median(v) for pol, v in res.items()}
+    clean = all(groups[pol].flags() == (0, 0) for pol in ("ig", "global", "thread"))
+    ov = {pol: round(100.0 * (ms[pol] / ms["unprotected"] - 1.0), 2) for pol in ("ig", "global", "thread")}
+    return {"workload": "C2 DLRM MLP-Bottom 13-512-256-64 + MLP-Top 512-512-256-1, batch 1..2048, 24 chains",
+            "protected_tflops_ig": round(flops / (ms["ig"] * 1e-3) / 1e12, 3),
+            "ms_per_step": {k: round(v, 4) for k, v in ms.items()}, "overhead_pct": ov,
+            "ig_beats_better_pure": ms["ig"] <= min(ms["global"], ms["thread"]),
+            "plan_global_layers": sum(s is S.GLOBAL_ABFT for p in plans.values() for s in p),
+            "plan_thread_layers": sum(s is S.THREAD_ONE_SIDED for p in plans.values() for s in p),
+            "clean_run_false_positives": 0 if clean else 1}
+
+
+def reference_step(mlps, inputs, O) -> None:
+    """One C2 step through the oracle port of run_protected_pipeline (CPU)."""
+    for name, ws in mlps.items():
+        for b in BATCHES:
+            O.pipeline(inputs[(name, b)], ws, "binary16")
