@@ -153,3 +153,33 @@ def test_network_graph_replay_matches_eager(PN):
     torch.cuda.synchronize()
     assert torch.equal(net.logits(), eager)
     assert net.flags() == (0, 0)
+
+
+@pytest.mark.parametrize("name,layers", [
+    ("resnet50", ["conv1", "layer1.0.conv2", "layer3.0.downsample"]),     # stem (explicit im2col), halo 3x3 56x56x64
+    ("vgg16", ["features.2", "features.24", "classifier.0"]),             # conv1_2 at 224^2, a 256-wide tile, FC 25088->4096
+])
+def test_benchmarked_layers_at_batch_256(PN, name, layers):
+    """The layers the bench's dominant kernels run, at the bench's batch 256, against the fp32
+    checker, under global and one-sided ABFT: zero false positives, and a fault in the stem /
+    first conv is flagged at that layer."""
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model(name), 256)
+    x = _input(256, seed=3)
+    byname = {L.name: L for L in net.layers}
+    for scheme in (S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
+        net.set_schemes(scheme)
+        net.forward(x)
+        torch.cuda.synchronize()
+        assert net.flags() == (0, 0), scheme
+        for nm in layers:
+            check_layer(byname[nm])
+            torch.cuda.empty_cache()
+    L0 = byname[layers[0]]
+    net.set_schemes(S.GLOBAL_ABFT)
+    net.forward(x)
+    tau = net.verdicts()[L0.index].tolerance_used
+    net.inject({L0.index: [(L0.m - 3, 5, 8.0 * tau + 64.0)]})
+    net.forward(x)
+    assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [L0.index]
