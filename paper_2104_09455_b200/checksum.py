@@ -191,10 +191,12 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
     rowck(w) regrouped as the row sum of the checksum column a . rowck(w tile)
     from one extra MMA N-slice.  Verification of all layers is one batched
     launch after the chain; the host reads the verdicts once.
-    Only ReLU is fused; other activations are rejected.
+    ReLU is fused into the store.  Any other activation (the reference accepts any callable on
+    the accumulate-precision array, checksum.py:201, :235) is applied between the layers: the
+    kernel stores the layer's fp32 result (checks unchanged), the callable maps it, and the
+    result is rounded to storage for the next layer — one host round trip per layer.
     """
-    if activation is not relu:
-        raise ValueError("the fused B200 pipeline implements the ReLU activation of the reference chain")
+    fused = activation is relu
     m, k0 = D.shape2d(a0, "A0")
     D.require_device()
     mode = dtype or D.dtype_of(a0)
@@ -222,14 +224,24 @@ def run_protected_pipeline(a0, weights: Sequence, activation: Callable = relu, d
         nxt = t.empty((m, D.round8(n)), dtype=D.torch_storage_dtype(mode), device="cuda")
         if n % 8:
             nxt.zero_()
+        raw = nxt if fused else t.zeros((m, D.round8(n)), dtype=t.float32, device="cuda")
         f_dev, nf = D.faults_tensor(list(faults.get(idx, ())))
-        kw = dict(out=nxt, ldc=nxt.stride(0), out_kind="bf16" if mode.tag is DTypeTag.BFLOAT16 else "f16",
-                  relu=True, faults=f_dev, nfaults=nf, out_sum=sums[idx, 1:2], out_lhs=sums[idx, 0:1])
+        kind = ("bf16" if mode.tag is DTypeTag.BFLOAT16 else "f16") if fused else "f32"
+        kw = dict(out=raw, ldc=raw.stride(0), out_kind=kind, relu=fused, faults=f_dev, nfaults=nf,
+                  out_sum=sums[idx, 1:2], out_lhs=sums[idx, 0:1])
         plan = kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
                             plan_only=True, ck_layout=1, **kw)
         ckr = kernels.global_ck_rows(pw.bt, n, dims[idx], mode, plan)
         kernels.gemm(act, act.stride(0), pw.bt, pw.ldbt, m, n, dims[idx], mode, numeric, Scheme.GLOBAL_ABFT,
                      ck_rows=ckr, **kw)
+        if not fused:
+            c = raw[:, :n].cpu().numpy()
+            if mode.is_exact:
+                c = np.rint(c).astype(np.int64)
+            y = np.asarray(activation(c))
+            if y.shape != c.shape:
+                raise ShapeMismatchError(f"activation changed the layer {idx} output shape {c.shape} -> {y.shape}")
+            nxt[:, :n].copy_(D.torch().from_numpy(np.ascontiguousarray(y.astype(np.float32))).to("cuda"))
         if mode.is_exact:
             # the next layer consumes these values exactly only inside the fp16 integer range
             if D.max_abs(nxt) > D.FP16_INT_MAX:
