@@ -139,8 +139,9 @@ typedef struct {
   /* plan hints (0 = the planner's choice): bit 0 = no k-block pairs (one k-block per pipeline stage,
    * deeper pipeline); bit 1 = Bt is zero-padded to >= round_up(N, 256) rows, so the weight map covers
    * whole tiles (no out-of-bounds boxes); bit 2 = two output staging buffers per epilogue warp even
-   * when one would buy a pipeline stage.  The profilers time the alternatives and keep the fastest
-   * (T_o = min over plans). */
+   * when one would buy a pipeline stage; bit 3 = direct 16-byte stores of the output from the
+   * epilogue registers instead of shared-memory staging + bulk tensor stores.  The profilers time
+   * the alternatives and keep the fastest (T_o = min over plans). */
   int32_t plan_flags;
 } abft_gemm_args_t;
 

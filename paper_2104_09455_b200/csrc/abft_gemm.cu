@@ -125,6 +125,11 @@ struct GemmParams {
   uint32_t tx_a;         // bytes of one A box (the window), for the full-barrier count
   uint32_t b_tile_bytes; // one [b_rows x 64] B tile (a halo stage holds S of them)
   int cv_kstride;        // packed-weight channel stride (ck)
+  // a_mode 5 (gathered stems, <= 4 real input channels): the checksum warps build each A tile in
+  // shared memory from the NHWC input, K ordered (tap, 4 channels) — 8 bytes per (pixel, tap) —
+  // while B (all k-blocks, one N block) stays resident; no im2col workspace
+  const void* cv_x;
+  int cv_H, cv_W, cv_taps;
 };
 
 template <typename T>
@@ -382,6 +387,30 @@ __device__ __forceinline__ void add_residual32(float (&v)[32], const void* resid
   }
 }
 
+// Prefetch of one row's whole 32-column residual chunk (issued a chunk ahead in the lean
+// epilogues, so the HBM latency overlaps the accumulator wait and the previous chunk); false
+// for partial chunks, which add_residual32 handles element-wise
+template <typename T>
+__device__ __forceinline__ bool residual_prefetch(uint4 (&r)[4], const void* residual, long long ld_res, int gm,
+                                                  int gc0, int ncols) {
+  if (ncols < 32) return false;
+  const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(residual) + (long long)gm * ld_res + gc0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) r[j] = __ldg(src + j);
+  return true;
+}
+
+template <typename T>
+__device__ __forceinline__ void residual_apply(float (&v)[32], const uint4 (&r)[4]) {
+  using TR = ElemTraits<T>;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f0 = TR::unpack2(r[j].x), f1 = TR::unpack2(r[j].y), f2 = TR::unpack2(r[j].z), f3 = TR::unpack2(r[j].w);
+    v[8 * j] += f0.x; v[8 * j + 1] += f0.y; v[8 * j + 2] += f1.x; v[8 * j + 3] += f1.y;
+    v[8 * j + 4] += f2.x; v[8 * j + 5] += f2.y; v[8 * j + 6] += f3.x; v[8 * j + 7] += f3.y;
+  }
+}
+
 // One row's 32-column chunk of a 16-bit output by direct stores (ReLU folded into the pack):
 // four 16-byte stores when the chunk is whole and aligned, else element by element.
 template <typename T>
@@ -413,7 +442,9 @@ __device__ __forceinline__ void lean_store_row(const float (&v)[32], void* C, in
   }
 }
 
-template <typename T, int CLASS, int NT, bool HALO>
+// AM: the A-load family of the instance — 0 TMA tiles / im2col boxes (a_mode 0-2), 1 halo
+// windows (a_mode 4), 2 gathered stems (a_mode 5)
+template <typename T, int CLASS, int NT, int AM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
@@ -464,15 +495,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool ck_aug = p.ck_mode == 3 || p.ck_mode == 4;
   // halo-reuse conv (a_mode 4) and its weight-stationary B exist only in the HALO instances,
   // keeping the GEMM instances' hot loops free of them
+  constexpr bool HALO = AM == 1;
+  constexpr bool gather = AM == 2;
   const bool halo = HALO && p.a_mode == 4;
-  const bool b_res = HALO && p.b_resident;
+  const bool b_res = (HALO || gather) && p.b_resident;
   const int bn = p.bn;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], gather ? 4 : 1);    // gathered A: one arrival per checksum (gather) warp
       ptx::mbar_init(&ckfull[s], 4);    // one arrival per checksum warp
-      ptx::mbar_init(&empty[s], (p.acolck_mode == 2 || p.lhs_w != nullptr) ? 5 : 1);   // + one per CUDA-core A-checksum warp
+      // + one per CUDA-core A-checksum warp (TMA modes; gathered stems dot in their gather loop)
+      ptx::mbar_init(&empty[s], (!gather && (p.acolck_mode == 2 || p.lhs_w != nullptr)) ? 5 : 1);
     }
     ptx::mbar_init(bres, 1);
     for (int a = 0; a < DCK_BUFS; ++a) {
@@ -488,7 +522,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // programmatic dependent launch: let the next kernel on the stream start its prologue now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&tmA);
+    if (!gather) ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
     if (ck_loaded) ptx::tma_prefetch(&tmCK);
     if (p.tma_store) ptx::tma_prefetch(&tmC);
@@ -561,7 +595,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x) {
+      // gathered stems: the checksum warps fill the A stages; B is resident (loaded above)
+      for (int tile = gather ? L_num_tiles : (int)blockIdx.x; tile < L_num_tiles; tile += gridDim.x) {
         const int nb = tile % L_num_n_blocks;
         const int m0 = (tile / L_num_n_blocks) * L_bm_eff;
         const int n0 = nb * L_bn_eff;
@@ -751,7 +786,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
-            const uint64_t bd = b_base + (uint64_t)s * b_sstep;
+            const uint64_t bd = b_base + (uint64_t)(b_res ? kb : s) * b_sstep;   // resident B: by k-block
             const uint64_t cd = c_base + (uint64_t)s * c_sstep;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -773,21 +808,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t b_addr = ptx::smem_u32(sm_b + (b_res ? kb : s) * L_stage_b_bytes);
           const uint32_t c_addr = ptx::smem_u32(sm_ck + s * L_stage_ck_bytes);
           if (halo) {
-            // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile
+            // the S taps of this filter row: A = the window shifted by si rows, B = tap si's tile.
+            // Descriptors advance by constants from the stage's (address field = smem byte address
+            // >> 4: +8 per 128-byte window row, +2 per 32-byte K step)
+            const uint64_t ad0 = a_base + (uint64_t)s * a_sstep;
+            const uint64_t bd0 = b_base + (uint64_t)(b_res ? kb : s) * b_sstep;
+            const uint64_t cd0 = c_base + (uint64_t)s * c_sstep;
+            const uint64_t b_tstep = L_b_tile_bytes >> 4, c_tstep = (uint64_t)(L_nck_pad * 128) >> 4;
 #pragma unroll 1
             for (int si = 0; si < L_cv_S; ++si) {
+              const uint64_t ad = ad0 + 8ull * (uint64_t)si;
+              const uint64_t bdt = bd0 + b_tstep * (uint64_t)si;
+              const uint64_t cdt = cd0 + c_tstep * (uint64_t)si;
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k) {
-                const uint32_t row_off = (uint32_t)si * 128u;
-                const uint64_t adesc = ptx::desc_kmajor_sw128(a_addr + row_off + (uint32_t)k * 32u);
-                const uint32_t bt_addr = b_addr + (uint32_t)si * L_b_tile_bytes;
-                const uint64_t bdesc = ptx::desc_kmajor_sw128(bt_addr + k * 32);
                 const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
-                ptx::mma_f16_ss_w(d, adesc, bdesc, ck_aug ? L_idesc_aug : L_idesc_main, accum);
-                if (ck_loaded)
-                  ptx::mma_f16_ss_w(d + bn, adesc,
-                                  ptx::desc_kmajor_sw128(c_addr + (uint32_t)(si * L_nck_pad * 128) + k * 32),
-                                  L_idesc_ck, accum);
+                ptx::mma_f16_ss_w(d, ad + 2ull * k, bdt + 2ull * k, idesc_m, accum);
+                if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + 2ull * k, cdt + 2ull * k, L_idesc_ck, accum);
               }
             }
             ptx::mma_commit_w(&empty[s]);
@@ -853,6 +890,110 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= CK_WARP0) {
+    if constexpr (gather) {
+      // ------------------------------------------ gathered stem A tiles (a_mode 5)
+      // Thread ct owns tile row ct (output pixel m0 + ct); per k-block it copies the 16 taps'
+      // first 4 channels (8 bytes each; zero-filled outside the image / past the last tap / past
+      // M) into the SW128 K-major stage with cp.async: k = tap * 4 + c, so tap j of the k-block
+      // lands in 16-byte chunk j/2 (XOR row & 7), half j&1.  GDEPTH k-blocks stay in flight per
+      // thread (the copies are latency-bound); a stage is published to the MMA once its copies
+      // have landed.  With a global "dot" lhs the thread re-reads its row of the landed stage
+      // and accumulates sum_k A[row][k] * rowck(B)[k] (fp64), as the dot warps do for TMA modes.
+      constexpr int GDEPTH = 3;
+      const int ct = threadIdx.x - CK_WARP0 * 32;
+      const int M = p.M, P = p.cv_P, Q = p.cv_Q, S = p.cv_S, H = p.cv_H, W = p.cv_W, taps = p.cv_taps;
+      const int sh = p.cv_sh, sw = p.cv_sw, ph0 = p.cv_ph, pw0 = p.cv_pw, nkb = p.nkb, stages = p.stages;
+      const long long pix_bytes = (long long)p.cv_c * 2;
+      const uint8_t* __restrict__ xg = reinterpret_cast<const uint8_t*>(p.cv_x);
+      const float* __restrict__ lw = p.lhs_w;
+      const uint32_t swz = (uint32_t)(ct & 7);
+      const uint32_t a_row0 = ptx::smem_u32(sm_a) + (uint32_t)ct * 128u;
+      double part = 0.0;
+      int s = 0, pend = 0, ws = 0, wkb = 0;
+      uint32_t ph = 0;
+      // publish the oldest in-flight stage (its copies have landed once <= `left` groups remain)
+      auto publish = [&]() {
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&full[ws]);
+        if (lw != nullptr) {
+          const uint8_t* row = sm_a + ws * p.stage_a_bytes + ct * 128;
+          double d = 0.0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint2 a = *reinterpret_cast<const uint2*>(row + ((((uint32_t)j >> 1) ^ swz) << 4) + ((j & 1) << 3));
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(lw + (wkb * 16 + j) * 4));
+            const float2 a01 = TR::unpack2(a.x), a23 = TR::unpack2(a.y);
+            d += (double)a01.x * w4.x + (double)a01.y * w4.y + (double)a23.x * w4.z + (double)a23.y * w4.w;
+          }
+          part += d;
+        }
+        if (++ws == stages) ws = 0;
+        if (++wkb == nkb) wkb = 0;
+        --pend;
+      };
+      // tap t -> byte offset of its input pixel from the window origin, (r * W + s) * pixel; and the
+      // stages zeroed once (positions past the last tap are never written again)
+      int* gtab = reinterpret_cast<int*>(smem + p.off_acolck);
+      if (ct < 64) gtab[ct] = ct < taps ? (int)(((ct / S) * (long long)W + ct % S) * pix_bytes) : 0;
+      for (int i = ct; i < (int)(stages * p.stage_a_bytes / 16); i += 128)
+        reinterpret_cast<uint4*>(sm_a)[i] = make_uint4(0u, 0u, 0u, 0u);
+      ptx::named_bar_sync(2, 128);
+      const int R = taps / S;
+      // the input may be the previous kernel's output
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int m = (tile / p.num_n_blocks) * p.bm_eff + ct;
+        const bool valid = m < M;
+        const int img = valid ? m / (P * Q) : 0;
+        const int rem = m - img * P * Q;
+        const int pp = rem / Q;
+        const int hi0 = pp * sh - ph0, wi0 = (rem - pp * Q) * sw - pw0;
+        // the row's valid taps: bit t = tap t's pixel is inside the image
+        uint64_t vm = 0;
+        if (valid) {
+          uint64_t smask = 0;
+          for (int sx = 0; sx < S; ++sx) smask |= (uint64_t)((unsigned)(wi0 + sx) < (unsigned)W) << sx;
+          for (int r = 0; r < R; ++r)
+            if ((unsigned)(hi0 + r) < (unsigned)H) vm |= smask << (r * S);
+        }
+        const uint8_t* pb = xg + (long long)img * H * W * pix_bytes + ((long long)hi0 * W + wi0) * pix_bytes;
+#pragma unroll 1
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t dst = a_row0 + (uint32_t)s * p.stage_a_bytes;
+          const uint32_t vk = (uint32_t)(vm >> (kb * 16));
+          const int t0 = kb * 16;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (t0 + j < taps) {
+              const bool in = (vk >> j) & 1u;
+              const uint8_t* src = in ? pb + gtab[t0 + j] : xg;
+              ptx::cp_async8(dst + ((((uint32_t)j >> 1) ^ swz) << 4) + ((j & 1) << 3), src, in ? 8u : 0u);
+            }
+          }
+          ptx::cp_async_commit();
+          ++pend;
+          if (pend > GDEPTH) {
+            ptx::cp_async_wait<GDEPTH>();
+            publish();
+          }
+          if (++s == stages) { s = 0; ph ^= 1; }
+        }
+      }
+      ptx::cp_async_wait<0>();
+      while (pend > 0) publish();
+      if (lw != nullptr) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (p.out_partials != nullptr) {
+          if (lane == 0) red_d[16 + (warp - CK_WARP0)] = part;
+        } else if (lane == 0 && part != 0.0) {
+          atomicAdd(p.out_lhs, part);
+          __threadfence();
+        }
+      }
+    } else
     // ----------------------------------------------- checksum-row generator
     if (ck_onchip) {
       const int ct = threadIdx.x - CK_WARP0 * 32;
@@ -1096,6 +1237,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;                          // TMEM lane quadrant of this warp
     const int h = (warp - EPI_WARP0) >> 2;           // chunk parity handled by this warp
     const int row = q * 32 + lane;                   // tile row == TMEM lane
+    // bulk tensor stores cover whole 32-row quadrants inside the tile (halo tiles of Qt = 112 /
+    // 80 pixels: the last, partial quadrant stores its rows directly)
+    const bool q_full = (q + 1) * 32 <= p.bm_eff;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const bool split = p.epi_split != 0;
     const int c_first = split ? h * 32 : (h == 0 ? 0 : 0x7fffffff);
@@ -1120,7 +1264,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
       const long long ldc = p.ldc;
       const bool single = p.out_single != 0;
-      const bool tma = p.tma_store != 0;
+      const bool tma = p.tma_store != 0 && q_full;
       const float* __restrict__ bias = p.bias;
       const bool bias_lhs = bias != nullptr && p.lhs_epi;
       const void* resid = p.residual;
@@ -1134,6 +1278,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int gm = m0 + row;
         const bool row_in_tile = row < bm_eff;
         const bool row_valid = row_in_tile && gm < M;
+        uint4 rb[4];
+        bool have_rb = resid != nullptr && row_valid && c_first < bn_eff &&
+                       residual_prefetch<T>(rb, resid, ld_res, gm, n0 + c_first, min(bn_eff - c_first, N - n0 - c_first));
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
@@ -1166,7 +1313,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             tsum += (t4[0] + t4[1]) + (t4[2] + t4[3]);
           }
-          if (resid != nullptr && row_valid) add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
+          if (resid != nullptr && row_valid) {
+            if (have_rb) residual_apply<T>(v, rb);
+            else add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
+            const int cn = c0 + 64;
+            have_rb = cn < bn_eff && residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
+          }
           if (cmax >= 32 && tma) {
             if (lane == 0) {
               if (single) ptx::bulk_wait_read<0>();
@@ -1226,7 +1378,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M, mt = p.mt, groups = p.groups;
         const long long ldc = p.ldc;
         const bool single = p.out_single != 0;
-        const bool tma = p.tma_store != 0;
+        const bool tma = p.tma_store != 0 && q_full;
         const float* __restrict__ bias = p.bias;
         const void* resid = p.residual;
         const long long ld_res = p.ld_res;
@@ -1240,6 +1392,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool row_in_tile = row < bm_eff;
           const int t_row = gm / mt;
           const bool row_verdict = row_in_tile && t_row < p.n_trows;
+          uint4 rb[4];
+          bool have_rb = resid != nullptr && row_in_tile && gm < M && c_first < bn_eff &&
+                         residual_prefetch<T>(rb, resid, ld_res, gm, n0 + c_first,
+                                              min(bn_eff - c_first, N - n0 - c_first));
           ptx::mbar_wait(&tfull[acc], aph);
           ptx::tc_fence_after();
           const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
@@ -1267,8 +1423,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (exceeds_tol_rk(exact_mode, rk, p, x, y)) fmask |= 1u << (c0 / NT + gi);
               }
             }
-            if (resid != nullptr && row_in_tile && gm < M)
-              add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
+            if (resid != nullptr && row_in_tile && gm < M) {
+              if (have_rb) residual_apply<T>(v, rb);
+              else add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
+              const int cn = c0 + 64;
+              have_rb = cn < bn_eff &&
+                        residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
+            }
             if (cmax >= 32 && tma) {
               if (lane == 0) {
                 if (single) ptx::bulk_wait_read<0>();
@@ -1509,7 +1670,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
           // whole 32-column chunks go out by bulk tensor stores; a tile's 16-column tail (bn_eff = 240
           // etc.) by direct stores
-          const bool chunk_tma = p.tma_store && cmax >= 32;
+          const bool chunk_tma = p.tma_store && cmax >= 32 && q_full;
           const bool relu_in_pack = p.relu && chunk_tma && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr;
           if (p.relu && !relu_in_pack) {
 #pragma unroll
@@ -1782,13 +1943,13 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
   return ABFT_OK;
 }
 
-template <typename T, int CLASS, int NT, bool HALO>
+template <typename T, int CLASS, int NT, int AM>
 int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo,
                 const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
@@ -1803,35 +1964,37 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, HALO>, ma, mb, mc, mo, p),
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM>, ma, mb, mc, mo, p),
                       "abft_gemm_kernel launch (PDL)");
   }
-  abft_gemm_kernel<T, CLASS, NT, HALO><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
+  abft_gemm_kernel<T, CLASS, NT, AM><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
-template <typename T, bool HALO>
+template <typename T, int AM>
 int launch_cls(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, AM>(ma, mb, mc, mo, p, smem, grid, st);
   if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, HALO>(ma, mb, mc, mo, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, HALO>(ma, mb, mc, mo, p, smem, grid, st);
-    return launch_inst<T, CLASS_CHECKSUM, 0, HALO>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, AM>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, AM>(ma, mb, mc, mo, p, smem, grid, st);
+    if constexpr (AM != 2) return launch_inst<T, CLASS_CHECKSUM, 0, AM>(ma, mb, mc, mo, p, smem, grid, st);
+    return fail(ABFT_E_UNSUPPORTED, "gathered stems take thread_n 8 or 16");
   }
-  if constexpr (!HALO) {
+  if constexpr (AM == 0) {
     if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, false>(ma, mb, mc, mo, p, smem, grid, st);
     if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, false>(ma, mb, mc, mo, p, smem, grid, st);
     return launch_inst<T, CLASS_REPLICA, 0, false>(ma, mb, mc, mo, p, smem, grid, st);
   }
-  return fail(ABFT_E_UNSUPPORTED, "replication schemes have no halo conv path");
+  return fail(ABFT_E_UNSUPPORTED, "replication schemes have no halo / gathered conv path");
 }
 
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                  const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (p.a_mode == 4) return launch_cls<T, true>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
-  return launch_cls<T, false>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
+  if (p.a_mode == 4) return launch_cls<T, 1>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
+  if (p.a_mode == 5) return launch_cls<T, 2>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
+  return launch_cls<T, 0>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
 }
 
 // output map for the bulk tensor stores: dims {N, M}, box {32 columns, 32 rows}; fp32 rows are
@@ -1906,6 +2069,7 @@ const EnvOverrides& env_overrides() {
 // Choose the CTA tile and carve shared memory / TMEM for one call.
 int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr) {
   const bool halo = cg != nullptr && cg->a_mode == 4;
+  const bool gather = cg != nullptr && cg->a_mode == 5;
   if (a == nullptr) return fail(ABFT_E_VALUE, "null args");
   if (a->M < 1 || a->N < 1 || a->K < 1) return fail(ABFT_E_SHAPE, "GEMM extents must be >= 1");
   if (a->dtype != ABFT_F16 && a->dtype != ABFT_BF16) return fail(ABFT_E_VALUE, "dtype must be ABFT_F16 or ABFT_BF16");
@@ -1954,6 +2118,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     long long best_cost = 0;
     for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
       if (cand < nt || (thread_level && cand / nt > 32)) continue;
+      if (gather && (cand / nt) * nt < n_ext) continue;    // gathered stems: one N block (resident B)
       if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
       const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
       if (cols + extra_cols > 512) continue;
@@ -2026,6 +2191,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.ck_roff = p.ck_mode == 4 ? bn : 0;
   if (halo && (p.ck_mode == 1 || p.ck_mode == 2 || want_acolck))
     return fail(ABFT_E_UNSUPPORTED, "halo conv mode needs augmented checksum weights");
+  if (gather && (p.ck_mode == 1 || p.ck_mode == 2 || p.ck_mode == 4 || want_acolck || has_shadow ||
+                 p.num_n_blocks != 1 || (thread_level && !((nt == 8 || nt == 16) && p.bn_eff % 32 == 0))))
+    return fail(ABFT_E_UNSUPPORTED, "gathered stem: one N block, augmented checksum weights, thread_n 8 / 16");
   p.shuffle_verdicts = thread_level && (32 % mt == 0) ? 1 : 0;
   p.r = tol_ratio(a->numeric);
   p.rk = (float)(p.r * (double)p.tol_k);
@@ -2103,7 +2271,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // bulk tensor stores of the output: whole 128-row tiles in 32-column boxes (a 16-column tail
     // of the tile is stored directly), 16-byte aligned base and row pitch
     const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
-    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff == BM && p.bn_eff % 16 == 0 &&
+    p.tma_store = (a->out_dtype != ABFT_OUT_NONE && a->C != nullptr && p.bm_eff % 16 == 0 && p.bn_eff % 16 == 0 &&
+                   !(a->plan_flags & 8) &&
                    ((a->ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a->C) & 15) == 0)) ? 1 : 0;
   }
   uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
@@ -2112,7 +2281,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   if (a->a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
   p.a_colck = a->scheme == ABFT_GLOBAL ? a->a_colck : nullptr;
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
-  const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : 0u;
+  // (gathered stems keep their tap -> input-offset table in this region)
+  const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : (gather ? 1024u : 0u);
   const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
   const uint32_t extras0 = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + acolck_bytes + ones_bytes + bar_bytes;
@@ -2139,15 +2309,17 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   // weight-stationary B (halo convs, whose stages carry S weight tiles each): one N-block, several M
   // tiles per CTA, B for all k-blocks fits beside >= 4 A stages
   const long long b_all = (long long)p.nkb * p.stage_b_bytes;
-  p.b_resident = (halo && p.num_n_blocks == 1 && p.num_tiles > 1 && p.ck_mode != 1 && p.ck_mode != 2 && p.ck_mode != 4 &&
-                  !has_shadow &&
-                  b_all + 4LL * p.stage_a_bytes <= budget) ? 1 : 0;
-  p.stage_w_bytes = p.lhs_w != nullptr ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u;
+  p.b_resident = ((halo || gather) && p.num_n_blocks == 1 && (p.num_tiles > 1 || gather) && p.ck_mode != 1 &&
+                  p.ck_mode != 2 && p.ck_mode != 4 && !has_shadow && b_all + 4LL * p.stage_a_bytes <= budget) ? 1 : 0;
+  if (gather && !p.b_resident) return fail(ABFT_E_UNSUPPORTED, "gathered stem: the weights do not fit in shared memory");
+  // (gathered stems read rowck(B) for the dot lhs straight from global memory)
+  p.stage_w_bytes = (p.lhs_w != nullptr && !gather) ? (uint32_t)(halo ? cg->S : 1) * 256u : 0u;
   const uint32_t stage_bytes =
       p.stage_a_bytes + (p.b_resident ? 0u : p.stage_b_bytes) + p.stage_ck_bytes + p.stage_w_bytes;
   int stages = (budget - (p.b_resident ? (int)b_all : 0) - (p.stage_w_bytes ? 1024 : 0)) / (int)stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(ABFT_E_UNSUPPORTED, "shared memory budget too small for a 2-stage pipeline");
+  if (gather && stages < 4) return fail(ABFT_E_UNSUPPORTED, "gathered stem: fewer than 4 pipeline stages");
   p.stages = stages;
   p.off_b = stages * p.stage_a_bytes;
   p.off_ck = p.off_b + (p.b_resident ? (uint32_t)b_all : stages * p.stage_b_bytes);
@@ -2406,14 +2578,29 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
       if (g.Qt) mode = 4;
     }
   }
-  if (force >= 0 && !pointwise) {
+  if (force >= 0 && force != 5 && !pointwise) {
     const int fm = force;
     if (fm != 4 || g.Qt) mode = fm;
     if (fm == 4 && !g.Qt) mode = c->c % 64 == 0 || c->c >= 48 ? 1 : 3;
   }
+  // stems with <= 4 real channels (the networks' 3-channel inputs): K = (tap, 4 channels), the
+  // A tiles gathered in shared memory (mode 5); the explicit im2col (mode 3) keeps the same K
+  // layout so both run on the same packed weights
+  const bool stem4 = mode == 3 && g.cr <= 4 && c->r * c->s <= 64;
+  if (stem4) {
+    const int s = c->gemm.scheme;
+    const bool ok = c->gemm.a_colck == nullptr && s != ABFT_REPL_FULL && s != ABFT_REPL_SINGLE &&
+                    (s == ABFT_UNPROTECTED || c->gemm.ck_layout == 1 || c->gemm.lhs_rowck != nullptr ||
+                     (s == ABFT_GLOBAL && c->gemm.out_lhs == nullptr && c->gemm.out_partials == nullptr));
+    if (ok && force != 3) mode = 5;
+  }
   g.a_mode = mode;
   g.ws = 0;
-  if (mode == 0 || mode == 2) {
+  if (stem4) {
+    g.ck = 4;
+    g.K = (c->r * c->s * 4 + 7) / 8 * 8;
+    if (mode == 3) g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
+  } else if (mode == 0 || mode == 2) {
     g.ck = c->c;
     g.K = c->r * c->s * c->c;
   } else if (mode == 1 || mode == 4) {
@@ -2504,6 +2691,12 @@ static int conv_make_plan(const abft_conv_args_t* c, ConvGeom& g, abft_gemm_args
   rc = validate_common(&ga);
   if (rc != ABFT_OK) return rc;
   rc = make_plan(&ga, pl, &g);
+  if (rc != ABFT_OK && g.a_mode == 5) {
+    // a call the gathered stem cannot take: the explicit im2col on the same (tap, 4-channel) K
+    g.a_mode = 3;
+    g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
+    rc = make_plan(&ga, pl, &g);
+  }
   if (rc != ABFT_OK && g.a_mode == 4) {
     // the halo stages (S weight tiles each) do not fit this tile: per-tap im2col instead
     // (same packed-weight layout: channels padded to 64)
@@ -2573,8 +2766,8 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
     // explicit im2col into the caller's workspace, then the plain GEMM on it
     if (c->workspace == nullptr || c->ws_bytes < g.ws || (reinterpret_cast<uintptr_t>(c->workspace) & 15))
       return fail(ABFT_E_VALUE, "explicit-im2col conv needs a 16-byte aligned workspace of abft_conv_plan out[6] bytes");
-    rc = launch_im2col(c->gemm.A, c->n, c->h, c->w, c->c, g.cr, c->r, c->s, c->stride_h, c->stride_w, c->pad_h,
-                       c->pad_w, g.P, g.Q, c->r * c->s * g.cr, g.K, c->workspace, as_stream(stream));
+    rc = launch_im2col(c->gemm.A, c->n, c->h, c->w, c->c, g.ck, c->r, c->s, c->stride_h, c->stride_w, c->pad_h,
+                       c->pad_w, g.P, g.Q, c->r * c->s * g.ck, g.K, c->workspace, as_stream(stream));
     if (rc != ABFT_OK) return rc;
     ga.A = c->workspace;
     ga.lda = g.K;
@@ -2587,6 +2780,13 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
   p.cv_P = g.P; p.cv_Q = g.Q; p.cv_S = c->s;
   p.cv_sh = c->stride_h; p.cv_sw = c->stride_w; p.cv_ph = c->pad_h; p.cv_pw = c->pad_w;
   p.cv_c = c->c;
+  if (g.a_mode == 5) {
+    // gathered stem: no A tensor map (the checksum warps load the input directly)
+    p.cv_x = c->gemm.A;
+    p.cv_H = c->h; p.cv_W = c->w; p.cv_taps = c->r * c->s;
+    CUtensorMap ma{};
+    return launch_with_a(&ga, pl, ma, stream);
+  }
   p.cv_chunks = g.a_mode == 1 ? g.ck / BK : c->c / 8;
   p.cv_pairs = c->r * c->s * (c->c / 8);
   CUtensorMap ma;

@@ -26,7 +26,8 @@ from .schemes import Scheme
 from .shapes import DeviceProfile
 
 
-PLAN_FLAGS = (0, 1, 4, 5)     # plan hints tried: none, no k-block pairs, double output staging, both
+# plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output stores
+PLAN_FLAGS = (0, 1, 4, 5, 8)
 
 
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,

@@ -21,7 +21,9 @@ from .shapes import GemmShape
 
 NETWORKS = ("resnet50", "vgg16", "alexnet", "squeezenet1_0", "shufflenet_v2_x1_0",
             # the paper's remaining Fig 4 workloads
-            "densenet161", "resnext50_32x4d", "wide_resnet50_2")
+            "densenet161", "resnext50_32x4d", "wide_resnet50_2",
+            # the specialised NoScope CNNs (50x50 frames, batch 64; noscope.py)
+            "noscope_coral", "noscope_roundabout", "noscope_taipei", "noscope_amsterdam")
 
 
 @dataclass(frozen=True)
@@ -63,7 +65,11 @@ def capture(name: str, batch: int, h: int, w: int) -> List[LayerSpec]:
     if name not in NETWORKS:
         raise ValueError(f"unknown network {name!r}; expected one of {NETWORKS}")
     with torch.device("meta"):
-        model = getattr(torchvision.models, name)(weights=None)
+        if name.startswith("noscope_"):
+            from . import noscope
+            model = noscope.build(name)
+        else:
+            model = getattr(torchvision.models, name)(weights=None)
     model.eval()
     layers: List[LayerSpec] = []
 

@@ -625,13 +625,14 @@ def _build(net: ProtectedNetwork, model) -> Act:
     import torchvision.models as tvm
     if isinstance(model, tvm.ResNet):
         return _build_resnet(net, model)
-    if isinstance(model, (tvm.VGG, tvm.AlexNet)):
+    if isinstance(model, (tvm.VGG, tvm.AlexNet)) or type(model).__name__ == "NoScopeCNN":
         return _build_vgg(net, model)
     if isinstance(model, tvm.SqueezeNet):
         return _build_squeezenet(net, model)
     if isinstance(model, tvm.ShuffleNetV2):
         return _build_shufflenet(net, model)
-    raise ValueError(f"unsupported network {type(model).__name__}: ResNet, VGG, AlexNet, SqueezeNet, ShuffleNetV2")
+    raise ValueError(f"unsupported network {type(model).__name__}: ResNet, VGG, AlexNet, SqueezeNet, ShuffleNetV2, "
+                     f"NoScopeCNN")
 
 
 def _build_resnet(net, m) -> Act:
@@ -657,8 +658,9 @@ def _build_resnet(net, m) -> Act:
 
 
 def _build_vgg(net, m) -> Act:
-    """torchvision VGG / AlexNet: conv(+ReLU) / maxpool features, identity adaptive pool at 224,
-    then the classifier's Linear(+ReLU) layers (Dropout is the identity in eval)."""
+    """torchvision VGG / AlexNet (and the NoScope CNNs, which have no adaptive pool): conv(+ReLU) /
+    maxpool features, identity adaptive pool at 224, then the classifier's Linear(+ReLU) layers
+    (Dropout is the identity in eval)."""
     import torch.nn as nn
     a = net.input
     mods = list(m.features)
@@ -670,7 +672,7 @@ def _build_vgg(net, m) -> Act:
             first = False
         elif isinstance(mod, nn.MaxPool2d):
             a = net.maxpool(a, mod.kernel_size, mod.stride, mod.padding, mod.ceil_mode)
-    osz = m.avgpool.output_size
+    osz = m.avgpool.output_size if hasattr(m, "avgpool") else (a.h, a.w)
     osz = (osz, osz) if isinstance(osz, int) else tuple(osz)
     if (a.h, a.w) != osz:
         raise ValueError(f"adaptive pool {osz} on a {a.h}x{a.w} map: only the identity case (224 input) is supported")
@@ -766,6 +768,9 @@ def build_model(name: str, seed: int = 0, calibrate: bool = True):
     """A torchvision model with seeded random weights (no checkpoints offline) and calibrated BN."""
     import torch
     import torchvision
+    if name.startswith("noscope_"):
+        from . import noscope
+        return noscope.build(name, seed)
     torch.manual_seed(seed)
     model = getattr(torchvision.models, name)(weights=None)
     if calibrate:

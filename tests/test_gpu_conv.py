@@ -18,7 +18,10 @@ GEMM_RTOL = 2e-5
 
 # (n, h, w, c, oc, r, s, stride, pad): every A-load mode of the kernel
 CASES = [
-    (2, 20, 22, 3, 64, 7, 7, 2, 3),      # stem: 8-channel im2col columns (mode 2)
+    (2, 20, 22, 3, 64, 7, 7, 2, 3),      # ResNet stem: gathered (tap, 4-channel) A tiles (mode 5)
+    (2, 17, 19, 3, 64, 3, 3, 1, 1),      # VGG stem (mode 5, one k-block)
+    (3, 15, 13, 3, 24, 3, 3, 2, 1),      # ShuffleNet stem: N = 24 (mode 5, 32-wide tile)
+    (1, 23, 21, 3, 96, 7, 7, 2, 0),      # SqueezeNet stem: N = 96, no padding (mode 5)
     (2, 13, 11, 64, 48, 3, 3, 1, 1),     # 64-channel chunks, SW128 (mode 1)
     (3, 9, 10, 16, 40, 3, 3, 2, 1),      # strided, 8-channel columns
     (2, 12, 12, 32, 24, 1, 1, 1, 0),     # pointwise = plain GEMM of the NHWC matrix (mode 0)

@@ -95,6 +95,41 @@ def test_network_layers_logits_and_clean_flags(PN, name):
             assert max(abs(v.lhs - v.rhs) / v.tolerance_used for v in vs) < 0.05
 
 
+@pytest.mark.parametrize("name", ["noscope_coral", "noscope_roundabout", "noscope_taipei", "noscope_amsterdam"])
+def test_noscope_networks_at_batch_64(PN, name):
+    """The specialised NoScope CNNs (50x50 frames at batch 64): every layer against the
+    fp32 checker, logits against the torch fp32 forward, zero false positives under each scheme, and
+    a fault in the first conv flagged at that layer only."""
+    import torch
+    from paper_2104_09455_b200 import noscope
+    S = PN.Scheme
+    model = PN.build_model(name)
+    net = PN.ProtectedNetwork(model, noscope.BATCH, noscope.HW, noscope.HW)
+    x = _input(noscope.BATCH, seed=4, h=noscope.HW, w=noscope.HW)
+    with torch.no_grad():
+        ref32 = model.float().cuda()(x.float()).float()
+        ref16 = model.half().cuda()(x).float()
+    model.float()
+    for scheme in (S.UNPROTECTED, S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
+        net.set_schemes(scheme)
+        out = net.forward(x).float()
+        torch.cuda.synchronize()
+        assert net.flags() == (0, 0), (scheme, net.flags())
+        for L in net.layers:
+            check_layer(L)
+        err = float((out - ref32).abs().max())
+        err16 = float((ref16 - ref32).abs().max())
+        assert err <= 4 * err16 + 2e-3 * float(ref32.abs().max()), (scheme, err, err16)
+    net.set_schemes(S.GLOBAL_ABFT)
+    net.forward(x)
+    L0 = net.layers[0]
+    tau = net.verdicts()[L0.index].tolerance_used
+    net.inject({L0.index: [(L0.m // 3, 7, 8.0 * tau + 64.0)]})
+    net.forward(x)
+    assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [L0.index]
+    net.inject({})
+
+
 @pytest.mark.parametrize("scheme", ["global-abft", "thread-one-sided"])
 def test_network_fault_flags_the_right_layer(PN, scheme):
     """A single-element fault in one layer (K < 1024: above that the reference tau of

@@ -245,6 +245,23 @@ def test_network_layer_lists_reproduce_paper_fig4():
     assert len(networks.capture("resnet50", 1, 224, 224)) == 54
 
 
+def test_noscope_layer_lists_reproduce_paper_aggregate_intensity():
+    # PAPER.md:679-735 / BASELINE.md 1.2: FP16 aggregate AI of the NoScope CNNs at batch 64, x8 padding;
+    # 2-4 conv layers of 16-64 channels, <= 2 FC layers, 50x50 frames
+    pytest.importorskip("torchvision")
+    import paper_2104_09455_b200 as P
+    from paper_2104_09455_b200 import networks, noscope
+    from paper_2104_09455_b200.shapes import PaddingPolicy
+    for name, ai in noscope.PAPER_AI.items():
+        layers = networks.capture(name, noscope.BATCH, noscope.HW, noscope.HW)
+        convs = [l for l in layers if l.kind == "conv"]
+        fcs = [l for l in layers if l.kind == "fc"]
+        assert 2 <= len(convs) <= 4 and len(fcs) <= 2, name
+        assert all(16 <= l.oc <= 64 for l in convs), name
+        agg = P.aggregate_intensity([P.pad_gemm(l.gemm(), PaddingPolicy.MULTIPLE_OF_8) for l in layers], P.BINARY16)
+        assert agg == pytest.approx(ai, abs=0.35), name
+
+
 def test_fitted_device_profile_recovers_model_choices():
     """calibrate.fit_device_profile: on timings generated by a known device model, the fitted
     profile's model-only choices agree with the measured choices on every layer."""

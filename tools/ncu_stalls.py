@@ -6,8 +6,9 @@ rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr = rows[1]
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
+hdr = rows[hi]
+body = [r for r in rows[hi + 1:] if len(r) == len(hdr) and "Instructions Executed" not in r]
 iex, ist, isrc = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 if len(sys.argv) == 2:
@@ -15,10 +16,13 @@ if len(sys.argv) == 2:
     for r in body:
         agg[int(r[iex] or 0)][0] += int(r[ist] or 0)
         agg[int(r[iex] or 0)][1] += 1
-    for ex, (st, n) in sorted(agg.items(), key=lambda x: -x[1][0])[:12]:
+    top = sorted(agg.items(), key=lambda x: -x[1][0])[:12]
+    for ex, (st, n) in top:
         print(f"ex={ex:9d} samples={st:6d} instructions={n}")
-    sys.exit()
-for ex in map(int, sys.argv[2:]):
+    exs = [ex for ex, _ in top[:4]]
+else:
+    exs = list(map(int, sys.argv[2:]))
+for ex in exs:
     tot = defaultdict(int)
     top = []
     for r in body:
