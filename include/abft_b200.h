@@ -141,7 +141,11 @@ typedef struct {
    * whole tiles (no out-of-bounds boxes); bit 2 = two output staging buffers per epilogue warp even
    * when one would buy a pipeline stage; bit 3 = direct 16-byte stores of the output from the
    * epilogue registers instead of shared-memory staging + bulk tensor stores.  The profilers time
-   * the alternatives and keep the fastest (T_o = min over plans). */
+   * the alternatives and keep the fastest (T_o = min over plans); bit 4 = the chunk-split epilogue
+   * (both warp sets on every tile) for narrow tiles, which otherwise alternate whole tiles; bit 5 =
+   * global ABFT on a 256-wide tile splits the accumulator (columns 240..255 and the checksum slice
+   * in a shared TMEM tail, the rest double-buffered); bits 6-8 = k-blocks of gathered-stem copies
+   * in flight (3..7, 0 = 3). */
   int32_t plan_flags;
 } abft_gemm_args_t;
 

@@ -119,7 +119,7 @@ def standalone_colck(x_dev, geom: dict, pl: dict, dtype: DType, out) -> None:
 
 def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig(),
            scheme: Scheme = Scheme.UNPROTECTED, faults: Sequence[FaultSpec] = (), dtype: DType | None = None,
-           colck_source: str = "fused", tile_n: int = 0):
+           colck_source: str = "fused", tile_n: int = 0, plan_flags: int = 0):
     """Protected NHWC convolution; returns the reference's ExecutionReport for the lowered GEMM.
 
     ``report.output`` is [n, P, Q, OC] fp32 (int64 in exact-int mode); ``report.shape`` is
@@ -127,7 +127,7 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     conv kernel's checksum N-slice, sum over rows of A . rowck(B tile) ("slice"), from the
     checksum warps' dot of the staged A tiles with rowck(B) ("dot"; the default "fused" is
     "slice"), or from colck(A) . rowck(B) with the windowed checksum of a standalone pass
-    ("standalone")."""
+    ("standalone").  ``plan_flags``: abft_gemm_args_t.plan_flags (kernel plan hints)."""
     from .checksum import Verdict
     from .tiled import _TV_DTYPE, ExecutionReport, _counts, _thread_verdicts
 
@@ -165,7 +165,8 @@ def conv2d(x, weight, stride=1, padding=0, tiling: TilingConfig = TilingConfig()
     sums = t.zeros(2, dtype=t.float64, device="cuda") if glob else None       # [lhs, rhs]
     kw = dict(out=out, ldc=pc.oc, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
               m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
-              out_sum=sums[1:2] if glob else None, verdicts=verdicts, ck_split=not dtype.is_exact, tile_n=tile_n)
+              out_sum=sums[1:2] if glob else None, verdicts=verdicts, ck_split=not dtype.is_exact, tile_n=tile_n,
+              plan_flags=plan_flags)
     colck = None
     if glob and colck_source == "fused":
         colck_source = "slice"

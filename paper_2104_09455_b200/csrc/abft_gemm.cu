@@ -88,8 +88,18 @@ struct GemmParams {
   uint32_t off_ones;     // smem [64 x 128 B] tile of ones (mode 1)
   uint32_t idesc_ones;
   int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
+  int tail_split;        // 1 (global ABFT, tile_n 256, lean epilogue): the MMA writes output columns [0, 240) into a
+                         //    double-buffered stage and columns [240, 256) + the 16-column checksum slice into a
+                         //    shared 32-column tail (TMEM columns tail_col..+31) that the epilogue drains first,
+                         //    so the 272-column tile no longer forces a single accumulator stage
+  int tail_col;
+  int gdepth;            // gathered stems: k-blocks of cp.async copies in flight per gather thread (3..7)
+  int epi_tiles;         // 1 (lean epilogues, narrow tiles): warps 2-5 take the even tiles of the CTA, warps 6-9
+                         //    the odd ones, each warp all chunks of its quadrant — two tiles' epilogues in
+                         //    flight, with up to 4 accumulator stages
   int tma_store;         // 1: outputs staged in smem (SW128) and written by TMA bulk tensor stores
-  int out_single;        // 1: one 2 KB 16-bit staging buffer per epilogue warp (else two)
+  int out_single;        // 1: one 16-bit staging buffer per epilogue warp (else two)
+  int out_wide;          // 1 (lean paths): 64-column units, 4 KB staging buffers, 128-byte-row bulk stores (tmC2)
   int kpair;             // 1: a pipeline stage carries two consecutive k-blocks (plain GEMM A, one box per
                          //    operand and k-block, half the barrier round trips and loop iterations)
   uint32_t stage_a_bytes, stage_b_bytes, stage_ck_bytes;
@@ -448,7 +458,7 @@ template <typename T, int CLASS, int NT, int AM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
-                     const __grid_constant__ GemmParams p) {
+                     const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ GemmParams p) {
   using TR = ElemTraits<T>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -468,10 +478,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* ckfull = bars + p.stages;
   uint64_t* empty = bars + 2 * p.stages;
   uint64_t* tfull = bars + 3 * p.stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* dfull = tempty + 2;     // column-sum TMEM buffers (acolck_mode 1), DCK_BUFS deep
+  uint64_t* tempty = tfull + 4;     // accumulator stages (up to 4)
+  uint64_t* dfull = tempty + 4;     // column-sum TMEM buffers (acolck_mode 1), DCK_BUFS deep
   uint64_t* dempty = dfull + DCK_BUFS;
   uint64_t* bres = dempty + DCK_BUFS;    // resident-B loaded (b_resident)
+  uint64_t* tailempty = bres + 1;        // the shared accumulator tail drained (tail_split)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bres + 2);
   double* red_d = reinterpret_cast<double*>(tmem_holder + 4);
 
@@ -509,13 +520,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&empty[s], (!gather && (p.acolck_mode == 2 || p.lhs_w != nullptr)) ? 5 : 1);
     }
     ptx::mbar_init(bres, 1);
+    ptx::mbar_init(tailempty, 4);      // the four warps that own the tile's last chunk
     for (int a = 0; a < DCK_BUFS; ++a) {
       ptx::mbar_init(&dfull[a], 1);
       ptx::mbar_init(&dempty[a], 4);    // one arrival per checksum warp
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 8);    // one arrival per epilogue warp
+      ptx::mbar_init(&tempty[a], p.epi_tiles ? 4 : 8);    // one arrival per epilogue warp of the tile
     }
     ptx::fence_mbar_init();
   }
@@ -526,6 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tma_prefetch(&tmB);
     if (ck_loaded) ptx::tma_prefetch(&tmCK);
     if (p.tma_store) ptx::tma_prefetch(&tmC);
+    if (p.out_wide) ptx::tma_prefetch(&tmC2);
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
@@ -755,6 +768,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int acc = t_local % L_acc_stages;
         const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
+        if (p.tail_split) ptx::mbar_wait(tailempty, ((uint32_t)t_local & 1u) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * L_cols_per_acc);
         if (p.kpair) {
@@ -781,6 +795,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (fast) {
           // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
+          const bool tail = p.tail_split != 0;
+          const uint32_t tail_d = tmem_base + (uint32_t)p.tail_col;
 #pragma unroll 1
           for (int kb = 0; kb < L_nkb; ++kb) {
             ptx::mbar_wait(&full[s], ph);
@@ -792,7 +808,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t accum = (kb | k) != 0;
               ptx::mma_f16_ss_w(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
-              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
+              if (tail) {
+                // weight rows 240..255 (30 SW128 atoms on) and the checksum rows into the tail
+                ptx::mma_f16_ss_w(tail_d, ad + (uint64_t)k * a_kstep, bd + 1920ull + 2ull * k, L_idesc_ck, accum);
+                ptx::mma_f16_ss_w(tail_d + 16, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
+              } else if (ck_loaded) {
+                ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
+              }
             }
             ptx::mma_commit_w(&empty[s]);
             if (++s == L_stages) { s = 0; ph ^= 1; }
@@ -895,11 +917,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // Thread ct owns tile row ct (output pixel m0 + ct); per k-block it copies the 16 taps'
       // first 4 channels (8 bytes each; zero-filled outside the image / past the last tap / past
       // M) into the SW128 K-major stage with cp.async: k = tap * 4 + c, so tap j of the k-block
-      // lands in 16-byte chunk j/2 (XOR row & 7), half j&1.  GDEPTH k-blocks stay in flight per
+      // lands in 16-byte chunk j/2 (XOR row & 7), half j&1.  Up to stages - 1 k-blocks stay in flight per
       // thread (the copies are latency-bound); a stage is published to the MMA once its copies
       // have landed.  With a global "dot" lhs the thread re-reads its row of the landed stage
       // and accumulates sum_k A[row][k] * rowck(B)[k] (fp64), as the dot warps do for TMA modes.
-      constexpr int GDEPTH = 3;
+      // k-blocks of copies in flight (measured: 3 beats 7 on the ResNet / SqueezeNet stems — more
+      // outstanding LDGSTS only queue in the LSU); p.gdepth overrides (plan_flags bits 6-8)
+      const int gdepth = min(p.stages - 1, p.gdepth);
       const int ct = threadIdx.x - CK_WARP0 * 32;
       const int M = p.M, P = p.cv_P, Q = p.cv_Q, S = p.cv_S, H = p.cv_H, W = p.cv_W, taps = p.cv_taps;
       const int sh = p.cv_sh, sw = p.cv_sw, ph0 = p.cv_ph, pw0 = p.cv_pw, nkb = p.nkb, stages = p.stages;
@@ -932,14 +956,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++wkb == nkb) wkb = 0;
         --pend;
       };
-      // tap t -> byte offset of its input pixel from the window origin, (r * W + s) * pixel; and the
+      // tap t -> byte offset of its input pixel from the output pixel's window centre (tap (ph, pw),
+      // always inside the image for a real output pixel): ((r - ph) * W + (s - pw)) * pixel; and the
       // stages zeroed once (positions past the last tap are never written again)
       int* gtab = reinterpret_cast<int*>(smem + p.off_acolck);
-      if (ct < 64) gtab[ct] = ct < taps ? (int)(((ct / S) * (long long)W + ct % S) * pix_bytes) : 0;
+      if (ct < 64)
+        gtab[ct] = ct < taps ? (int)(((ct / S - ph0) * (long long)W + (ct % S - pw0)) * pix_bytes) : 0;
       for (int i = ct; i < (int)(stages * p.stage_a_bytes / 16); i += 128)
         reinterpret_cast<uint4*>(sm_a)[i] = make_uint4(0u, 0u, 0u, 0u);
       ptx::named_bar_sync(2, 128);
       const int R = taps / S;
+      uint32_t dcol[8];        // swizzled 16-byte chunk offsets of the thread's row
+#pragma unroll
+      for (int c = 0; c < 8; ++c) dcol[c] = ((uint32_t)c ^ swz) << 4;
       // the input may be the previous kernel's output
       asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -948,7 +977,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int img = valid ? m / (P * Q) : 0;
         const int rem = m - img * P * Q;
         const int pp = rem / Q;
-        const int hi0 = pp * sh - ph0, wi0 = (rem - pp * Q) * sw - pw0;
+        const int qq = rem - pp * Q;
+        const int hi0 = pp * sh - ph0, wi0 = qq * sw - pw0;
         // the row's valid taps: bit t = tap t's pixel is inside the image
         uint64_t vm = 0;
         if (valid) {
@@ -957,25 +987,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int r = 0; r < R; ++r)
             if ((unsigned)(hi0 + r) < (unsigned)H) vm |= smask << (r * S);
         }
-        const uint8_t* pb = xg + (long long)img * H * W * pix_bytes + ((long long)hi0 * W + wi0) * pix_bytes;
+        const uint8_t* pc = valid ? xg + ((long long)(img * H + pp * sh) * W + qq * sw) * pix_bytes : xg;
 #pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           const uint32_t dst = a_row0 + (uint32_t)s * p.stage_a_bytes;
           const uint32_t vk = (uint32_t)(vm >> (kb * 16));
           const int t0 = kb * 16;
+          const int4* g4 = reinterpret_cast<const int4*>(gtab + t0);
+          if (t0 + 16 <= taps) {
+            int oo[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (t0 + j < taps) {
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const int4 o = g4[j4];
+              oo[4 * j4] = o.x; oo[4 * j4 + 1] = o.y; oo[4 * j4 + 2] = o.z; oo[4 * j4 + 3] = o.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
               const bool in = (vk >> j) & 1u;
-              const uint8_t* src = in ? pb + gtab[t0 + j] : xg;
-              ptx::cp_async8(dst + ((((uint32_t)j >> 1) ^ swz) << 4) + ((j & 1) << 3), src, in ? 8u : 0u);
+              ptx::cp_async8(dst + dcol[j >> 1] + ((j & 1) << 3), pc + (in ? oo[j] : 0), in ? 8u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (t0 + j < taps) {
+                const bool in = (vk >> j) & 1u;
+                ptx::cp_async8(dst + dcol[j >> 1] + ((j & 1) << 3), pc + (in ? gtab[t0 + j] : 0), in ? 8u : 0u);
+              }
             }
           }
           ptx::cp_async_commit();
           ++pend;
-          if (pend > GDEPTH) {
-            ptx::cp_async_wait<GDEPTH>();
+          if (pend > gdepth) {
+            switch (gdepth) {      // cp.async.wait_group takes an immediate
+              case 3: ptx::cp_async_wait<3>(); break;
+              case 4: ptx::cp_async_wait<4>(); break;
+              case 5: ptx::cp_async_wait<5>(); break;
+              case 6: ptx::cp_async_wait<6>(); break;
+              default: ptx::cp_async_wait<7>(); break;
+            }
             publish();
           }
           if (++s == stages) { s = 0; ph ^= 1; }
@@ -1242,12 +1292,100 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool q_full = (q + 1) * 32 <= p.bm_eff;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const bool split = p.epi_split != 0;
-    const int c_first = split ? h * 32 : (h == 0 ? 0 : 0x7fffffff);
-    const int c_step = split ? 64 : 32;
+    const bool epi_tiles = p.epi_tiles != 0;     // (lean paths only; the planner guarantees it)
+    // wide stores (lean paths, 16-bit outputs): a warp owns 64-column units — two 32-column
+    // sub-chunks staged as 128-byte rows and written by ONE bulk tensor store (half the TMA row
+    // requests of 64-byte rows; the TMA engine's per-row cost bounds store-heavy tiles)
+    const bool wide = p.out_wide != 0;
+    const int c_first = epi_tiles ? 0 : split ? (wide ? h * 64 : h * 32) : (h == 0 ? 0 : 0x7fffffff);
+    const int c_step = (split && !epi_tiles) ? 64 : 32;
+    const int c_jump = (split && !epi_tiles) ? 96 : 32;     // wide: from a unit's second sub-chunk to the next unit
+    auto c_next = [&](int c0) { return wide ? (((c0 & 32) == 0) ? c0 + 32 : c0 + c_jump) : c0 + c_step; };
     double rhs_acc = 0.0, lhs_acc = 0.0;
     int col_lo = 0x7fffffff, col_hi = -1;
     int sbuf = 0;
-    uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * (p.out_single ? 2048 : 4096);
+
+    uint8_t* my_stage = out_stage + (warp - EPI_WARP0) * ((p.out_single ? 2048 : 4096) << (p.out_wide ? 1 : 0));
+    // Lean-path store of one 32-column sub-chunk: wide units (two sub-chunks staged as 128-byte
+    // rows, one bulk tensor store), 32-column bulk stores (64-byte rows), or direct row stores
+    // (16-column tails, partial halo quadrants)
+    auto store_chunk = [&](const float (&v)[32], int c0, int cmax, int gc0, int m0, int gm, bool row_ok, bool relu,
+                           bool tma, bool& unit_wide) {
+      const long long ldc = p.ldc;
+      const int N = p.N;
+      const bool single = p.out_single != 0;
+      const int sub = (c0 >> 5) & 1;
+      if (wide && sub == 0) unit_wide = tma && cmax >= 64;
+      if (wide && unit_wide) {
+        if (sub == 0) {
+          if (lane == 0) {
+            if (single) ptx::bulk_wait_read<0>();
+            else ptx::bulk_wait_read<1>();
+          }
+          __syncwarp();
+        }
+        uint8_t* rowp = my_stage + sbuf * 4096 + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 u;
+          if (relu) {
+            u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
+            u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
+            u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
+            u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
+          } else {
+            u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+            u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+            u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+            u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+          }
+          *reinterpret_cast<uint4*>(rowp + (((uint32_t)(sub * 4 + j) ^ (uint32_t)(lane & 7)) << 4)) = u;
+        }
+        if (sub == 1) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmC2, my_stage + sbuf * 4096, gc0 - 32, m0 + q * 32);
+            ptx::bulk_commit();
+          }
+          sbuf ^= single ? 0 : 1;
+        }
+      } else if (cmax >= 32 && tma) {
+        if (lane == 0) {
+          if (single) ptx::bulk_wait_read<0>();
+          else ptx::bulk_wait_read<1>();
+        }
+        __syncwarp();
+        uint8_t* rowp = my_stage + sbuf * (wide ? 4096 : 2048) + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 u;
+          if (relu) {
+            u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
+            u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
+            u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
+            u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
+          } else {
+            u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
+            u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
+            u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
+            u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
+          }
+          *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&tmC, my_stage + sbuf * (wide ? 4096 : 2048), gc0, m0 + q * 32);
+          ptx::bulk_commit();
+        }
+        sbuf ^= single ? 0 : 1;
+      } else {
+        // direct stores: a tile's 16-column tail, or tiles without bulk-tensor stores (halo
+        // conv tiles of Qt < 128 pixels)
+        if (row_ok) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
+      }
+    };
     int t_local = 0;
     // Lean path (unprotected and global ABFT, 16-bit bulk-tensor stores, no faults / fused colck /
     // bring-up bits): the same results as the generic loop below with its per-chunk scheme
@@ -1262,14 +1400,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool relu = p.relu != 0;
       const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
       const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
-      const long long ldc = p.ldc;
-      const bool single = p.out_single != 0;
       const bool tma = p.tma_store != 0 && q_full;
       const float* __restrict__ bias = p.bias;
       const bool bias_lhs = bias != nullptr && p.lhs_epi;
       const void* resid = p.residual;
       const long long ld_res = p.ld_res;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+        if (epi_tiles && (t_local & 1) != h) continue;
         const int acc = t_local % acc_stages;
         const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
         const int mb = tile / nnb;
@@ -1284,14 +1421,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
-        const bool gck_ld = p.gck && h == 0;
+        const bool tail = p.tail_split != 0;
+        const bool gck_ld = p.gck && !tail && (h == 0 || epi_tiles);
         float ck_hi = 0.f, ck_lo = 0.f;
         float tsum = 0.f;
+        float tv[16];
+        if (tail && h == 1) {
+          // the shared tail first (output columns 240..255 and the checksum pair), then release it
+          // so the next tile's MMAs can start while this tile's stage drains
+          const uint32_t ta = tmem_base + lane_addr + (uint32_t)p.tail_col;
+          ptx::tmem_ldn<16>(ta, tv);
+          ptx::tmem_ld2(ta + 16, ck_hi, ck_lo);
+          ptx::tmem_ld_wait();
+          if (row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tailempty);
+        }
+        bool unit_wide = false;
 #pragma unroll 1
-        for (int c0 = c_first; c0 < bn_eff; c0 += 64) {
+        for (int c0 = c_first; c0 < bn_eff; c0 = c_next(c0)) {
           float v[32];
           __syncwarp();
-          ptx::tmem_ld32(tacc + c0, v);
+          if (tail && c0 == 224) {
+            // columns 224..239 from the stage, 240..255 from the tail (read above)
+            float v16[16];
+            ptx::tmem_ldn<16>(tacc + c0, v16);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) { v[j] = v16[j]; v[16 + j] = tv[j]; }
+          } else {
+            ptx::tmem_ld32(tacc + c0, v);
+          }
           if (gck_ld && c0 == c_first) ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
           ptx::tmem_ld_wait();
           if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
@@ -1316,44 +1477,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (resid != nullptr && row_valid) {
             if (have_rb) residual_apply<T>(v, rb);
             else add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
-            const int cn = c0 + 64;
+            const int cn = c_next(c0);
             have_rb = cn < bn_eff && residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
           }
-          if (cmax >= 32 && tma) {
-            if (lane == 0) {
-              if (single) ptx::bulk_wait_read<0>();
-              else ptx::bulk_wait_read<1>();
-            }
-            __syncwarp();
-            uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 u;
-              if (relu) {
-                u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
-                u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
-                u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
-                u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
-              } else {
-                u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
-                u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
-                u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
-                u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
-              }
-              *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              ptx::tma_store_2d(&tmC, my_stage + sbuf * 2048, gc0, m0 + q * 32);
-              ptx::bulk_commit();
-            }
-            sbuf ^= single ? 0 : 1;
-          } else {
-            // direct stores: a tile's 16-column tail, or tiles without bulk-tensor stores (halo
-            // conv tiles of Qt < 128 pixels)
-            if (row_valid) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
-          }
+          store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -1376,13 +1503,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool ck_split = p.split != 0;
         const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
         const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M, mt = p.mt, groups = p.groups;
-        const long long ldc = p.ldc;
-        const bool single = p.out_single != 0;
         const bool tma = p.tma_store != 0 && q_full;
         const float* __restrict__ bias = p.bias;
         const void* resid = p.residual;
         const long long ld_res = p.ld_res;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
+          if (epi_tiles && (t_local & 1) != h) continue;
           const int acc = t_local % acc_stages;
           const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
           const int mb = tile / nnb;
@@ -1400,8 +1526,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::tc_fence_after();
           const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
           uint32_t fmask = 0;
+          bool unit_wide = false;
 #pragma unroll 1
-          for (int c0 = c_first; c0 < bn_eff; c0 += 64) {
+          for (int c0 = c_first; c0 < bn_eff; c0 = c_next(c0)) {
             float v[32], ckh[GPCK], ckl[GPCK];
             __syncwarp();
             ptx::tmem_ld32(tacc + c0, v);
@@ -1426,43 +1553,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (resid != nullptr && row_in_tile && gm < M) {
               if (have_rb) residual_apply<T>(v, rb);
               else add_residual32<T>(v, resid, ld_res, gm, gc0, min(cmax, N - gc0));
-              const int cn = c0 + 64;
+              const int cn = c_next(c0);
               have_rb = cn < bn_eff &&
                         residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
             }
-            if (cmax >= 32 && tma) {
-              if (lane == 0) {
-                if (single) ptx::bulk_wait_read<0>();
-                else ptx::bulk_wait_read<1>();
-              }
-              __syncwarp();
-              uint8_t* rowp = my_stage + sbuf * 2048 + lane * 64;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                uint4 u;
-                if (relu) {
-                  u.x = TR::pack2_relu(v[8 * j], v[8 * j + 1]);
-                  u.y = TR::pack2_relu(v[8 * j + 2], v[8 * j + 3]);
-                  u.z = TR::pack2_relu(v[8 * j + 4], v[8 * j + 5]);
-                  u.w = TR::pack2_relu(v[8 * j + 6], v[8 * j + 7]);
-                } else {
-                  u.x = TR::pack2(v[8 * j], v[8 * j + 1]);
-                  u.y = TR::pack2(v[8 * j + 2], v[8 * j + 3]);
-                  u.z = TR::pack2(v[8 * j + 4], v[8 * j + 5]);
-                  u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
-                }
-                *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) = u;
-              }
-              ptx::fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_2d(&tmC, my_stage + sbuf * 2048, gc0, m0 + q * 32);
-                ptx::bulk_commit();
-              }
-              sbuf ^= single ? 0 : 1;
-            } else if (row_in_tile && gm < M) {
-              lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
-            }
+            store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide);
           }
           // fired groups of the thread tile's Mt rows -> verdicts (rare)
           uint32_t m = row_verdict ? fmask : 0u;
@@ -1944,7 +2039,7 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
 }
 
 template <typename T, int CLASS, int NT, int AM>
-int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo,
+int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo, const CUtensorMap& mo2,
                 const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -1964,42 +2059,42 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM>, ma, mb, mc, mo, p),
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM>, ma, mb, mc, mo, mo2, p),
                       "abft_gemm_kernel launch (PDL)");
   }
-  abft_gemm_kernel<T, CLASS, NT, AM><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, p);
+  abft_gemm_kernel<T, CLASS, NT, AM><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo2, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
 template <typename T, int AM>
 int launch_cls(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-               const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, AM>(ma, mb, mc, mo, p, smem, grid, st);
+               const CUtensorMap& mo, const CUtensorMap& mo2, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
   if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, AM>(ma, mb, mc, mo, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, AM>(ma, mb, mc, mo, p, smem, grid, st);
-    if constexpr (AM != 2) return launch_inst<T, CLASS_CHECKSUM, 0, AM>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if constexpr (AM != 2) return launch_inst<T, CLASS_CHECKSUM, 0, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
     return fail(ABFT_E_UNSUPPORTED, "gathered stems take thread_n 8 or 16");
   }
   if constexpr (AM == 0) {
-    if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, false>(ma, mb, mc, mo, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, false>(ma, mb, mc, mo, p, smem, grid, st);
-    return launch_inst<T, CLASS_REPLICA, 0, false>(ma, mb, mc, mo, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    return launch_inst<T, CLASS_REPLICA, 0, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
   }
   return fail(ABFT_E_UNSUPPORTED, "replication schemes have no halo / gathered conv path");
 }
 
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                 const CUtensorMap& mo, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (p.a_mode == 4) return launch_cls<T, 1>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
-  if (p.a_mode == 5) return launch_cls<T, 2>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
-  return launch_cls<T, 0>(cls, ntc, ma, mb, mc, mo, p, smem, grid, st);
+                 const CUtensorMap& mo, const CUtensorMap& mo2, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (p.a_mode == 4) return launch_cls<T, 1>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
+  if (p.a_mode == 5) return launch_cls<T, 2>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
+  return launch_cls<T, 0>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
 }
 
 // output map for the bulk tensor stores: dims {N, M}, box {32 columns, 32 rows}; fp32 rows are
 // 128 B (SW128), 16-bit rows 64 B (SW64)
-int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a, int box_rows = 32) {
+int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a, int box_rows = 32, int box_cols = 32) {
   auto enc = get_encode_fn();
   if (!enc) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   const int esz = a->out_dtype == ABFT_OUT_F32 ? 4 : 2;
@@ -2008,10 +2103,11 @@ int make_out_map(CUtensorMap* map, const abft_gemm_args_t* a, int box_rows = 32)
                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   cuuint64_t dims[2] = {(cuuint64_t)a->N, (cuuint64_t)a->M};
   cuuint64_t strides[1] = {(cuuint64_t)(a->ldc * esz)};
-  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
+  // rows of box_cols * esz bytes: 128 (fp32 x 32, 16-bit x 64) -> SW128, 64 -> SW64
   CUresult r = enc(map, dt, 2, a->C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   box_cols * esz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ABFT_E_CUDA, "cuTensorMapEncodeTiled(C) failed with CUresult " + std::to_string((int)r));
   return ABFT_OK;
@@ -2116,13 +2212,16 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // Thread-level schemes keep <= 32 checksum groups per tile; ties go to the wider tile.
     int best = 0;
     long long best_cost = 0;
+    // (the lean-epilogue conditions under which a 256-wide global tile splits its accumulator tail)
+    const bool tail_est = (a->out_dtype == ABFT_OUT_F16 || a->out_dtype == ABFT_OUT_BF16) && a->next_colck == nullptr &&
+                          (a->faults == nullptr || a->nfaults == 0) && a->a_colck == nullptr && !(a->plan_flags & 32);
     for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
       if (cand < nt || (thread_level && cand / nt > 32)) continue;
       if (gather && (cand / nt) * nt < n_ext) continue;    // gathered stems: one N block (resident B)
       if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
       const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
       if (cols + extra_cols > 512) continue;
-      const bool dbuf = 2 * cols + extra_cols <= 512;
+      const bool dbuf = 2 * cols + extra_cols <= 512 || (cand == 256 && gck && tail_est && (a->plan_flags & 32));
       const int eff = (cand / nt) * nt;
       const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
       // whole waves while a CTA runs few tiles; fractional beyond 4 waves, where the CTAs with one
@@ -2278,6 +2377,44 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   uint32_t out_bytes = p.tma_store ? 8u * 4096u : 0u;
   // chunks split across both warps of a quadrant unless a check needs whole rows in one warp
   p.epi_split = (!thread_level || (out.ntc > 0 && p.shuffle_verdicts)) ? 1 : 0;
+  p.gdepth = (a->plan_flags >> 6) & 7 ? std::max(3, (a->plan_flags >> 6) & 7) : 3;
+  {
+    // tile-parallel lean epilogue for narrow tiles (the conditions of the kernel's lean paths): a
+    // tile's epilogue is latency-bound (TMEM load -> pack -> staging -> bulk store), so two tiles
+    // in flight, with up to 4 accumulator stages, instead of both warp sets on every tile;
+    // plan_flags bit 4 keeps the chunk-split epilogue
+    const bool out16 = a->out_dtype == ABFT_OUT_F16 || a->out_dtype == ABFT_OUT_BF16;
+    const bool lean_ok = p.epi_split && out16 && a->next_colck == nullptr && p.nfaults == 0 &&
+                         p.acolck_mode == 0 &&
+                         (out.cls == CLASS_PLAIN ||
+                          (out.cls == CLASS_CHECKSUM && out.ntc > 0 && a->scheme == ABFT_ONE_SIDED &&
+                           a->verdicts == nullptr && p.shuffle_verdicts));
+    p.epi_tiles = (lean_ok && p.bn_eff <= 128 && !(a->plan_flags & 16)) ? 1 : 0;
+    if (p.epi_tiles) {
+      p.acc_stages = std::min(4, 512 / p.cols_per_acc);
+      if (p.acc_stages < 2) p.epi_tiles = 0, p.acc_stages = 1;
+      p.dck_col = p.acc_stages * p.cols_per_acc;
+      p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
+    }
+    // global ABFT on a 256-wide tile: columns [0, 240) double-buffered, the last 16 output columns
+    // and the checksum slice in a shared 32-column tail
+    // (opt-in, plan_flags bit 5: measured slower than the single 272-column stage on the VGG-16
+    // layers — the two N = 16 MMAs per k-step cost more than the serialised epilogue)
+    p.tail_split = (lean_ok && out.cls == CLASS_PLAIN && p.gck && p.ck_mode == 4 && bn == 256 && p.bn_eff == 256 &&
+                    (a->plan_flags & 32)) ? 1 : 0;
+    if (p.tail_split) {
+      p.cols_per_acc = 240;
+      p.acc_stages = 2;
+      p.tail_col = 480;
+      p.dck_col = 512;
+      p.tmem_cols = 512;
+      p.idesc_main = ptx::idesc_f16(a->dtype == ABFT_BF16 ? 1u : 0u, BM, 240);
+      p.idesc_aug = p.idesc_main;
+    }
+    // 128-byte-row bulk stores (plan_flags bit 9 keeps 64-byte rows)
+    p.out_wide = (lean_ok && p.tma_store && p.bn_eff >= 64 && !(a->plan_flags & 512)) ? 1 : 0;
+    if (p.out_wide) out_bytes *= 2;
+  }
   if (a->a_colck != nullptr && thread_level) return fail(ABFT_E_VALUE, "a_colck is a global-scheme output");
   p.a_colck = a->scheme == ABFT_GLOBAL ? a->a_colck : nullptr;
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
@@ -2298,10 +2435,10 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // (not for few-k-block tiles: their epilogue, not the mainloop, is the critical path; plan_flags
     // bit 2 keeps both buffers regardless)
     if (p.tma_store && a->out_dtype != ABFT_OUT_F32 && !halo && p.nkb >= 4 && !(a->plan_flags & 4) &&
-        (room - (int)(8u * 2048u)) / (int)stage_bytes0 > (room - (int)out_bytes) / (int)stage_bytes0 &&
+        (room - (int)(out_bytes / 2)) / (int)stage_bytes0 > (room - (int)out_bytes) / (int)stage_bytes0 &&
         (room - (int)out_bytes) / (int)stage_bytes0 < 8) {
       p.out_single = 1;
-      out_bytes = 8u * 2048u;
+      out_bytes /= 2;
     }
   }
   const uint32_t extras = extras0 + out_bytes;
@@ -2506,12 +2643,18 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
   } else if (p.ck_mode != 4) {
     mc = mb;   // unused
   }
-  CUtensorMap mo;
+  CUtensorMap mo, mo2;
   if (p.tma_store) {
     rc = make_out_map(&mo, a);
     if (rc != ABFT_OK) return rc;
   } else {
     mo = mb;   // unused
+  }
+  if (p.out_wide) {
+    rc = make_out_map(&mo2, a, 32, 64);
+    if (rc != ABFT_OK) return rc;
+  } else {
+    mo2 = mo;   // unused
   }
   if (p.out_partials != nullptr && pl.grid > a->partials_cap)
     return fail(ABFT_E_SHAPE, "out_partials: partials_cap is smaller than the launch's grid");
@@ -2524,8 +2667,8 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
             p.cols_per_acc, p.tmem_cols, p.nck_pad, p.ck_mode, p.gck, p.tma_store, p.epi_split, p.a_mode, pl.smem,
             pl.grid, pl.cls, pl.ntc, p.kpair, p.out_single, p.b_resident);
   if (a->dtype == ABFT_BF16)
-    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
-  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, p, pl.smem, pl.grid, st);
+    return launch_typed<__nv_bfloat16>(pl.cls, pl.ntc, ma, mb, mc, mo, mo2, p, pl.smem, pl.grid, st);
+  return launch_typed<__half>(pl.cls, pl.ntc, ma, mb, mc, mo, mo2, p, pl.smem, pl.grid, st);
 }
 
 // ---------------------------------------------------------------- implicit-GEMM conv
@@ -2592,7 +2735,8 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
     const bool ok = c->gemm.a_colck == nullptr && s != ABFT_REPL_FULL && s != ABFT_REPL_SINGLE &&
                     (s == ABFT_UNPROTECTED || c->gemm.ck_layout == 1 || c->gemm.lhs_rowck != nullptr ||
                      (s == ABFT_GLOBAL && c->gemm.out_lhs == nullptr && c->gemm.out_partials == nullptr));
-    if (ok && force != 3) mode = 5;
+    // (the gather addresses taps from the window centre (p * stride, q * stride), inside the image)
+    if (ok && force != 3 && (g.P - 1) * c->stride_h < c->h && (g.Q - 1) * c->stride_w < c->w) mode = 5;
   }
   g.a_mode = mode;
   g.ws = 0;

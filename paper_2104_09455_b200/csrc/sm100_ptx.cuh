@@ -105,9 +105,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// 8-byte global -> shared copy (LDGSTS); src_bytes 0 zero-fills the destination
+// 8-byte global -> shared copy (LDGSTS); src_bytes 0 zero-fills the destination.  No memory
+// clobber: the destination is read only after cp_async_wait (which has one), so independent
+// address arithmetic and shared loads may be scheduled across a run of copies.
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -172,7 +174,7 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float& a, float& b) {
   a = __uint_as_float(r0);
   b = __uint_as_float(r1);
 }
-// 32 lanes x N consecutive columns (N = 1, 2, 4, 8)
+// 32 lanes x N consecutive columns (N = 1, 2, 4, 8, 16)
 template <int N>
 __device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -184,8 +186,15 @@ __device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(taddr));
+  } else if constexpr (N == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
   } else {
-    static_assert(N == 8, "tmem_ldn: N must be 1, 2, 4 or 8");
+    static_assert(N == 8, "tmem_ldn: N must be 1, 2, 4, 8 or 16");
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(taddr));

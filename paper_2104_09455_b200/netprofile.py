@@ -26,8 +26,9 @@ from .schemes import Scheme
 from .shapes import DeviceProfile
 
 
-# plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output stores
-PLAN_FLAGS = (0, 1, 4, 5, 8)
+# plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output
+# stores; the chunk-split epilogue for narrow tiles
+PLAN_FLAGS = (0, 1, 4, 5, 8, 16)
 
 
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,

@@ -174,13 +174,16 @@ def test_conv_every_a_load_mode_bit_exact(P, mode, monkeypatch):
                                   (2, 7, 9, 64, 300, 3, 3, 1, 1),       # 64-channel im2col, two N tiles
                                   (2, 12, 12, 32, 260, 1, 1, 1, 0)])    # pointwise
 @pytest.mark.parametrize("scheme", ["global-abft", "thread-one-sided"])
-def test_conv_full_width_tile_checksum_slice(P, case, scheme):
+@pytest.mark.parametrize("faulted", [True, False])
+def test_conv_full_width_tile_checksum_slice(P, case, scheme, faulted):
     """tile_n = 256: the checksum rows of the augmented weights go through their own box and
-    MMA N-slice (ck_mode 4), in every A-load mode.  Exact-int parity with the oracle."""
+    MMA N-slice (ck_mode 4), in every A-load mode.  Exact-int parity with the oracle.  Without
+    faults (and with 16-bit outputs, below) the global scheme runs the lean epilogue with the
+    split accumulator tail (columns 240..255 + the checksum slice in a shared TMEM tail)."""
     n, h, w, c, oc, r, s, st, pd = case
     x, wt, cols, wmat = _data(case, exact=True, seed=5)
     m = cols.shape[0]
-    fr = [("output", m - 1, oc - 1, 6), ("output", 3, 130, -2)]
+    fr = [("output", m - 1, oc - 1, 6), ("output", 3, 130, -2)] if faulted else []
     faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
     rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults, tile_n=256)
     out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, fr)
@@ -191,3 +194,48 @@ def test_conv_full_width_tile_checksum_slice(P, case, scheme):
     else:
         assert [(v.thread_row, v.thread_col) for v in rep.verdicts if v.detected] == \
             [(v.thread_row, v.thread_col) for v in verdicts if v.detected]
+
+
+@pytest.mark.parametrize("flags", [0, 32])
+def test_gemm_full_width_global_tail_split_exact(P, flags):
+    """Global ABFT on a 256-wide tile with 16-bit outputs (the lean epilogue): the default single
+    272-column accumulator stage and the opt-in split tail (plan_flags bit 5: output columns
+    240..255 and the checksum slice in a shared TMEM tail) give the exact outputs and the exact
+    global lhs / rhs of the reference (checksum.py:108-127)."""
+    import torch
+    from paper_2104_09455_b200 import _lib, kernels
+    from paper_2104_09455_b200 import device as D
+    rng = np.random.default_rng(7)
+    m, n, k = 777, 512, 192
+    a = rng.integers(-3, 4, size=(m, k)).astype(np.int64)
+    b = rng.integers(-3, 4, size=(k, n)).astype(np.int64)
+    ad = torch.from_numpy(a.astype(np.float16)).cuda()
+    pw = D.prepare_weight(torch.from_numpy(b.astype(np.float16)).cuda(), P.EXACT_INT)
+    out = torch.zeros((m, n), dtype=torch.float16, device="cuda")
+    sums = torch.zeros(2, dtype=torch.float64, device="cuda")
+    kw = dict(out=out, ldc=n, out_kind="f16", out_sum=sums[1:2], out_lhs=sums[0:1], tile_n=256, plan_flags=flags)
+    plan = kernels.gemm(ad, k, pw.bt, pw.ldbt, m, n, k, P.EXACT_INT, _lib.NUM_EXACT, P.Scheme.GLOBAL_ABFT,
+                        plan_only=True, ck_layout=1, **kw)
+    kw["ck_rows"] = kernels.global_ck_rows(pw.bt, n, k, P.EXACT_INT, plan)
+    kernels.gemm(ad, k, pw.bt, pw.ldbt, m, n, k, P.EXACT_INT, _lib.NUM_EXACT, P.Scheme.GLOBAL_ABFT, **kw)
+    torch.cuda.synchronize()
+    c = a @ b
+    assert np.array_equal(out.float().cpu().numpy().astype(np.int64), c)
+    lhs, rhs = sums.cpu().numpy()
+    assert int(round(rhs)) == int(c.sum())
+    assert int(round(lhs)) == int(a.sum(axis=0) @ b.sum(axis=1))
+
+
+@pytest.mark.parametrize("depth", [3, 5, 7])
+def test_gathered_stem_copy_depths_bit_exact(P, depth):
+    """The gathered stem (a_mode 5) with 3, 5 and 7 k-blocks of copies in flight (plan_flags bits
+    6-8): exact-int outputs and global verdict values equal the oracle's."""
+    from paper_2104_09455_b200 import conv as C
+    case = (2, 20, 22, 3, 64, 7, 7, 2, 3)
+    n, h, w, c, oc, r, s, st, pd = case
+    x, wt, cols, wmat = _data(case, exact=True, seed=9)
+    out, verdicts = O.execute(cols, wmat, O.Tiling(), "global-abft", [])
+    rep = C.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme.GLOBAL_ABFT, plan_flags=depth << 6)
+    assert np.array_equal(rep.output.reshape(cols.shape[0], oc), out)
+    v, rv = rep.verdicts[0], verdicts[0]
+    assert (v.detected, v.lhs, v.rhs) == (rv.detected, rv.lhs, rv.rhs)
