@@ -147,9 +147,28 @@ typedef struct {
    * in a shared TMEM tail, the rest double-buffered); bits 6-8 = k-blocks of gathered-stem copies
    * in flight (3..7, 0 = 3). */
   int32_t plan_flags;
+  /* optional window column sums of THIS layer's stored output (after bias / residual / ReLU /
+   * rounding) for the next layer's global lhs (the fused activation checksum):
+   * wsum [buckets][ws_ld] fp32, accumulated (the caller zeroes it); ws_mode 1 = one bucket, the
+   * column sums (a pointwise / FC consumer); 2 = nine buckets for a 3x3 / stride 1 / pad 1
+   * consumer: all rows, output row p == 0, p == P-1, column q == 0, q == Q-1, and the four corners
+   * (0,0), (0,Q-1), (P-1,0), (P-1,Q-1), where a row is the output pixel (n*P + p)*Q + q.
+   * plan_flags bit 10: the global scheme takes its lhs from outside the kernel (abft_window_lhs
+   * adds it to the partial slots), so no checksum slice / dot runs and the bias correction is the
+   * caller's. */
+  float* wsum; int32_t ws_ld, ws_mode, ws_P, ws_Q;
 } abft_gemm_args_t;
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
+
+/* The global lhs of a layer whose activation checksum came from the producer's window sums
+ * (abft_gemm_args_t.wsum): lhs += sum_{r,s,c<C} colck_im2col(r,s,c) * rowck[(r*S + s)*ck + c]
+ * + M * sum_{j<n_out} bias[j] (bias optional), where colck_im2col is the im2col column sum of the
+ * consumer's (R x S, stride 1, "same" padding) input rebuilt from the nine buckets (R = S = 3) or
+ * the plain column sums (R = S = 1) — the reference's checksum_dot(colck(A), rowck(B))
+ * (checksum.py:108-117) on the lowered GEMM.  fp64 dot, one atomic add into *lhs. */
+int abft_window_lhs(const float* wsum, int32_t ws_ld, int32_t C, int32_t R, int32_t S, int32_t ck,
+                    const float* rowck, const float* bias, int32_t n_out, int64_t M, double* lhs, void* stream);
 
 /* The kernel configuration abft_gemm would use for `args` (no launch):
  * out[0] tile_n, [1] bn_eff, [2] checksum groups per tile, [3] nck_pad, [4] pipeline stages,

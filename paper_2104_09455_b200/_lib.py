@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "abft_last_error",
     "abft_version",
     "abft_device_sms",
+    "abft_window_lhs",
     "abft_nhwc_maxpool",
     "abft_nhwc_avgpool",
     "abft_nhwc_interleave2",
@@ -105,6 +106,8 @@ class GemmArgs(ctypes.Structure):
         ("out_partials", ctypes.c_void_p), ("partials_cap", ctypes.c_int32),
         ("bias", ctypes.c_void_p), ("residual", ctypes.c_void_p), ("ld_res", ctypes.c_int64),
         ("plan_flags", ctypes.c_int32),
+        ("wsum", ctypes.c_void_p), ("ws_ld", ctypes.c_int32), ("ws_mode", ctypes.c_int32),
+        ("ws_P", ctypes.c_int32), ("ws_Q", ctypes.c_int32),
     ]
 
 

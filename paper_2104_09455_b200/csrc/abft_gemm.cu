@@ -140,6 +140,11 @@ struct GemmParams {
   // while B (all k-blocks, one N block) stays resident; no im2col workspace
   const void* cv_x;
   int cv_H, cv_W, cv_taps;
+  // window column sums of the stored output for the next layer's global lhs (abft_gemm_args_t.wsum):
+  // CTA-private [ws_nb][N] fp32 buckets in smem (off_ws), flushed once by atomics into wsum[b * ws_ld + col]
+  float* wsum;
+  int ws_ld, ws_mode, ws_P, ws_Q, ws_nb;
+  uint32_t off_ws;
 };
 
 template <typename T>
@@ -216,6 +221,42 @@ __device__ __forceinline__ float warp_column_sums(float (&v)[32], int lane) {
     }
   }
   return v[0];
+}
+
+// Window column sums of one 32-column chunk of stored outputs (vr: this lane's row, already
+// ReLU'd and rounded to the output type, zero past the chunk's ncols) into the CTA's smem buckets
+// ws_s[b * N + col]: bucket 0 all rows; with ws_mode 2 also the rows on output row p == 0 / P-1,
+// column q == 0 / Q-1 and the four corners (rows are output pixels (n*P + p)*Q + q).  Border
+// buckets only reduce when the warp holds such a row (ballot), so interior chunks pay one
+// transpose-reduce (31 shuffles).
+__device__ __forceinline__ void wsum_chunk(const GemmParams& p, float* ws_s, const float (&vr)[32], int gm, bool row_ok,
+                                           int gc0, int ncols, int lane) {
+  float t[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) t[j] = (row_ok && j < ncols) ? vr[j] : 0.f;
+  {
+    const float x = warp_column_sums(t, lane);
+    if (lane < ncols && x != 0.f) atomicAdd(&ws_s[gc0 + lane], x);
+  }
+  if (p.ws_mode != 2) return;
+  uint32_t bits = 0;
+  if (row_ok) {
+    const int pq = gm % (p.ws_P * p.ws_Q);
+    const int pp = pq / p.ws_Q, qq = pq - (pq / p.ws_Q) * p.ws_Q;
+    bits = (pp == 0 ? 1u : 0u) | (pp == p.ws_P - 1 ? 2u : 0u) | (qq == 0 ? 4u : 0u) | (qq == p.ws_Q - 1 ? 8u : 0u);
+  }
+  if (__ballot_sync(0xffffffffu, bits != 0u) == 0u) return;
+  // bucket b (1..8): the row-condition masks over bits (p0, pL, q0, qL)
+  constexpr uint32_t need[8] = {1u, 2u, 4u, 8u, 1u | 4u, 1u | 8u, 2u | 4u, 2u | 8u};
+#pragma unroll 1
+  for (int b = 0; b < 8; ++b) {
+    const bool in = (bits & need[b]) == need[b];
+    if (__ballot_sync(0xffffffffu, in) == 0u) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = (in && row_ok && j < ncols) ? vr[j] : 0.f;
+    const float x = warp_column_sums(t, lane);
+    if (lane < ncols && x != 0.f) atomicAdd(&ws_s[(b + 1) * p.N + gc0 + lane], x);
+  }
 }
 
 __device__ __forceinline__ void emit_verdict(const GemmParams& p, int t_row, int t_col, bool fired, double diff,
@@ -471,6 +512,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   float2* rec = reinterpret_cast<float2*>(smem + p.off_rec);     // [128][rec_stride] (generic Mt)
   float* stg = reinterpret_cast<float*>(smem + p.off_stage);     // [2][32][128] chunk staging (generic Nt)
   float* colck_s = reinterpret_cast<float*>(smem + p.off_colck);
+  float* ws_s = reinterpret_cast<float*>(smem + p.off_ws);          // [ws_nb][N] window-sum buckets
   uint8_t* out_stage = smem + p.off_out;
   float* acolck_s = reinterpret_cast<float*>(smem + p.off_acolck);  // [K] (acolck_in_smem)                         // [4 warps][2 buffers][32 rows x 128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
@@ -543,6 +585,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 256) colck_s[i] = 0.f;
+  }
+  if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.wsum != nullptr) {
+    for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.ws_nb * p.N; i += 256) ws_s[i] = 0.f;
   }
   if (warp >= CK_WARP0 && p.acolck_in_smem) {
     for (int i = threadIdx.x - CK_WARP0 * 32; i < p.K; i += 128) acolck_s[i] = 0.f;
@@ -1480,6 +1525,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int cn = c_next(c0);
             have_rb = cn < bn_eff && residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
           }
+          if (p.wsum != nullptr) {
+            float vr[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
+            wsum_chunk(p, ws_s, vr, gm, row_valid, gc0, min(cmax, N - gc0), lane);
+          }
           store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide);
         }
         ptx::tc_fence_before();
@@ -1556,6 +1607,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int cn = c_next(c0);
               have_rb = cn < bn_eff &&
                         residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
+            }
+            if (p.wsum != nullptr) {
+              float vr[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
+              wsum_chunk(p, ws_s, vr, gm, row_in_tile && gm < M, gc0, min(cmax, N - gc0), lane);
             }
             store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide);
           }
@@ -1760,18 +1817,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             if (j < ncols) v[j] += TR::unpack2((uint32_t)__ldg(r16 + j)).x;
         }
-        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr)) {
+        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr || p.wsum != nullptr)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
           // whole 32-column chunks go out by bulk tensor stores; a tile's 16-column tail (bn_eff = 240
           // etc.) by direct stores
           const bool chunk_tma = p.tma_store && cmax >= 32 && q_full;
-          const bool relu_in_pack = p.relu && chunk_tma && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr;
+          const bool relu_in_pack = p.relu && chunk_tma && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr &&
+                                    p.wsum == nullptr;
           if (p.relu && !relu_in_pack) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
           }
-          if (p.next_colck != nullptr && p.out_dtype != ABFT_OUT_F32) {
+          if ((p.next_colck != nullptr || p.wsum != nullptr) && p.out_dtype != ABFT_OUT_F32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = round_out(v[j], p.out_dtype);
           }
@@ -1855,6 +1913,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
+          if (p.wsum != nullptr) wsum_chunk(p, ws_s, v, gm, row_store, gc0, min(cmax, p.N - gc0), lane);
           if (p.next_colck != nullptr) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (row_store && j < cmax && gc0 + j < p.N) ? v[j] : 0.f;
@@ -1912,6 +1971,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = col_lo + et; i < col_hi; i += 256) {
         const float x = colck_s[i];
         if (x != 0.f) atomicAdd(&p.next_colck[i], x);
+      }
+    }
+    if (p.wsum != nullptr) {
+      ptx::named_bar_sync(3, 256);
+      for (int i = et; i < p.ws_nb * p.N; i += 256) {
+        const float x = ws_s[i];
+        if (x != 0.f) atomicAdd(&p.wsum[(long long)(i / p.N) * p.ws_ld + (i % p.N)], x);
       }
     }
   }
@@ -2183,7 +2249,10 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   }
   // global lhs: 'gdot' = CUDA-core dot of the staged A tiles with rowck(B) (lhs_rowck), else
   // 'gck' = a checksum N-slice in the MMA (checksum rows, separate or appended to the weights)
-  const bool want_lhs = a->out_lhs != nullptr || a->out_partials != nullptr;
+  // plan_flags bit 10: the lhs comes from outside the kernel (abft_window_lhs over the producer's
+  // window sums): only the output summation (rhs) runs here
+  const bool ext_lhs = (a->plan_flags & 1024) != 0;
+  const bool want_lhs = (a->out_lhs != nullptr || a->out_partials != nullptr) && !ext_lhs;
   const bool gdot = a->scheme == ABFT_GLOBAL && want_lhs && a->lhs_rowck != nullptr;
   const bool gck = a->scheme == ABFT_GLOBAL && want_lhs && !gdot;
   if (a->out_partials != nullptr && (a->scheme != ABFT_GLOBAL || a->partials_cap < 1))
@@ -2301,6 +2370,16 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.out_sum = a->out_sum;
   p.next_colck = a->next_colck;
   p.colck_in_smem = (a->next_colck != nullptr && a->N <= COLCK_SMEM_MAX) ? 1 : 0;
+  p.wsum = a->wsum;
+  p.ws_mode = a->wsum != nullptr ? a->ws_mode : 0;
+  p.ws_ld = a->ws_ld; p.ws_P = a->ws_P; p.ws_Q = a->ws_Q;
+  p.ws_nb = p.ws_mode == 2 ? 9 : 1;
+  if (p.wsum != nullptr) {
+    if (p.ws_mode != 1 && p.ws_mode != 2) return fail(ABFT_E_VALUE, "ws_mode must be 1 (column sums) or 2 (3x3 window buckets)");
+    if (a->ws_ld < a->N || (p.ws_mode == 2 && (a->ws_P < 1 || a->ws_Q < 1 || (long long)a->ws_P * a->ws_Q > a->M)))
+      return fail(ABFT_E_SHAPE, "window sums: ws_ld >= N, and P, Q of the output for ws_mode 2");
+    if ((long long)p.ws_nb * a->N * 4 > 20480) return fail(ABFT_E_UNSUPPORTED, "window sums: N too wide for the smem buckets");
+  }
   p.verdicts = a->verdicts;
   p.vsums = a->vsums; p.vk = a->vk; p.vn = (a->vsums && a->vk && a->vdone) ? a->vn : 0;
   p.vdone = a->vdone; p.vout = a->vout; p.vdetected = a->vdetected;
@@ -2318,7 +2397,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   // bias / residual epilogue (BN-folded networks)
   if (a->bias != nullptr) {
     if (reinterpret_cast<uintptr_t>(a->bias) & 15) return fail(ABFT_E_VALUE, "bias must be 16-byte aligned");
-    if (a->scheme == ABFT_GLOBAL && !want_lhs)
+    if (a->scheme == ABFT_GLOBAL && !want_lhs && !ext_lhs)
       return fail(ABFT_E_UNSUPPORTED, "bias with the global scheme needs the in-kernel lhs (out_lhs / out_partials)");
     if (thread_level && (a->scheme != ABFT_ONE_SIDED || out.ntc == 0))
       return fail(ABFT_E_UNSUPPORTED, "bias with a thread-level check needs the one-sided scheme with thread_n 8 or 16");
@@ -2422,7 +2501,9 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : (gather ? 1024u : 0u);
   const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
-  const uint32_t extras0 = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + acolck_bytes + ones_bytes + bar_bytes;
+  const uint32_t ws_bytes = p.wsum != nullptr ? (uint32_t)round_up(p.ws_nb * a->N * 4, 1024) : 0u;
+  const uint32_t extras0 = cks_bytes + rec_bytes + stage_bytes_ep + colck_bytes + acolck_bytes + ones_bytes + bar_bytes +
+                           ws_bytes;
   const int smem_cap = ov.smem_cap_kb > 0 ? std::min(max_smem_optin() - 1024, ov.smem_cap_kb * 1024)
                                           : max_smem_optin() - 1024 /*alignment slack*/;
   p.out_single = 0;
@@ -2468,7 +2549,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.off_out = p.off_colck + colck_bytes;
   p.off_ones = p.off_out + out_bytes;                 // 1024-aligned (all earlier sizes are)
   p.off_acolck = p.off_ones + ones_bytes;
-  p.off_bar = p.off_acolck + acolck_bytes;
+  p.off_ws = p.off_acolck + acolck_bytes;
+  p.off_bar = p.off_ws + ws_bytes;
   out.smem = (size_t)p.off_bar + bar_bytes + 1024;
   out.grid = std::min(p.num_tiles, sms);
   out.ck_offline_recommended = (has_ck && p.num_m_blocks > 2) ? 1 : 0;

@@ -204,6 +204,57 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
   return cuda_check(cudaGetLastError(), "interleave2 launch");
 }
 
+// The consumer's global lhs from the producer's window sums (abft_window_lhs): one CTA, fp64.
+// colck_im2col(r, s, c) of a 3x3 / stride 1 / pad 1 conv over an H x W input = the sum over the
+// input rows / columns tap (r, s) reads: all of them minus the row the tap never reaches (r = 0
+// misses the last row, r = 2 the first) minus the column likewise, plus their corner (counted
+// twice).  Buckets: 0 all, 1 p0, 2 pL, 3 q0, 4 qL, 5 (p0,q0), 6 (p0,qL), 7 (pL,q0), 8 (pL,qL).
+__global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict__ ws, int ld, int C, int R, int S,
+                                                         int ck, const float* __restrict__ rowck,
+                                                         const float* __restrict__ bias, int n_out, long long M,
+                                                         double* __restrict__ lhs) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  const int taps = R * S;
+  for (int i = threadIdx.x; i < taps * C; i += blockDim.x) {
+    const int tap = i / C, c = i - (i / C) * C;
+    double col = ws[c];
+    if (R == 3) {
+      const int r = tap / 3, sx = tap - (tap / 3) * 3;
+      const int rb = r == 0 ? 2 : (r == 2 ? 1 : 0);     // the row bucket the tap misses
+      const int cb = sx == 0 ? 4 : (sx == 2 ? 3 : 0);    // the column bucket
+      if (rb) col -= ws[(long long)rb * ld + c];
+      if (cb) col -= ws[(long long)cb * ld + c];
+      if (rb && cb) col += ws[(long long)(5 + (rb == 2 ? 2 : 0) + (cb == 4 ? 1 : 0)) * ld + c];
+    }
+    acc += col * (double)rowck[(long long)tap * ck + c];
+  }
+  if (bias != nullptr)
+    for (int j = threadIdx.x; j < n_out; j += blockDim.x) acc += (double)M * (double)bias[j];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    atomicAdd(lhs, t);
+  }
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_window_lhs(const float* wsum, int32_t ws_ld, int32_t C,
+                                                                     int32_t R, int32_t S, int32_t ck,
+                                                                     const float* rowck, const float* bias,
+                                                                     int32_t n_out, int64_t M, double* lhs,
+                                                                     void* stream) {
+  if (wsum == nullptr || rowck == nullptr || lhs == nullptr) return fail(ABFT_E_VALUE, "window_lhs: null pointer");
+  if (!((R == 1 && S == 1) || (R == 3 && S == 3))) return fail(ABFT_E_UNSUPPORTED, "window_lhs: 1x1 or 3x3 consumers");
+  if (C < 1 || ws_ld < C || ck < C || M < 0 || (bias != nullptr && n_out < 1))
+    return fail(ABFT_E_SHAPE, "window_lhs: bad extents");
+  window_lhs_kernel<<<1, 256, 0, as_stream(stream)>>>(wsum, ws_ld, C, R, S, ck, rowck, bias, n_out, M, lhs);
+  return cuda_check(cudaGetLastError(), "window_lhs launch");
+}
+
 extern "C" __attribute__((visibility("default"))) int abft_sum_partials(const double* partials, int32_t cap,
                                                                        int32_t ntasks, double* sums, void* stream) {
   if (ntasks < 1 || cap < 1) return fail(ABFT_E_SHAPE, "sum_partials: ntasks and cap must be >= 1");

@@ -25,7 +25,8 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
                fired_count=None, fired=None, fired_cap: int = 0, ck_split: bool = False, tile_n: int = 0,
                num_sms: int = 0, ck_rows=None, a_colck=None, out_lhs=None, verify=None, pdl: bool = False,
                ck_layout: int = None, lhs_rowck=None, out_partials=None, bias=None, residual=None,
-               ld_res: int = 0, plan_flags: int = 0):
+               ld_res: int = 0, plan_flags: int = 0, wsum=None, ws_ld: int = 0, ws_mode: int = 0, ws_P: int = 0,
+               ws_Q: int = 0):
     args = _lib.GemmArgs()
     args.A, args.lda = a.data_ptr(), lda
     args.Bt, args.ldbt = (bt.data_ptr() if bt is not None else 16), ldbt
@@ -68,6 +69,10 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
     if residual is not None:         # [M x N] storage-dtype shortcut, added before the ReLU
         args.residual, args.ld_res = residual.data_ptr(), (ld_res or residual.stride(0))
     args.plan_flags = int(plan_flags)
+    if wsum is not None:             # fp32 [buckets][ws_ld] window sums of this layer's stored output
+        if wsum.dtype != torch().float32 or not wsum.is_contiguous():
+            raise ValueError("wsum must be a contiguous float32 tensor")
+        args.wsum, args.ws_ld, args.ws_mode, args.ws_P, args.ws_Q = wsum.data_ptr(), ws_ld, ws_mode, ws_P, ws_Q
     args.pdl = int(pdl)
     vt = ()
     if verify is not None:
@@ -79,7 +84,7 @@ def _gemm_args(a, lda: int, bt, ldbt: int, m: int, n: int, k: int, dtype: DType,
         vt = (vsums, vks, vdone, vout, vdet)
     # the struct holds raw device pointers: keep every tensor it points to alive with it
     args._keep = [x for x in (a, bt, out, faults, out_sum, next_colck, verdicts, fired_count, fired, ck_rows,
-                              a_colck, out_lhs, lhs_rowck, out_partials, bias, residual) + vt
+                              a_colck, out_lhs, lhs_rowck, out_partials, bias, residual, wsum) + vt
                   if x is not None]
     return args
 
@@ -266,3 +271,11 @@ def interleave2(x1, ld1: int, b, ld2: int, pixels: int, half: int, out, ldo: int
 def sum_partials(partials, ntasks: int, sums) -> None:
     """[n, cap, 2] per-CTA (lhs, rhs) slots -> sums [n, 2] fp64 (one launch)."""
     _lib.call("abft_sum_partials", ptr(partials), partials.shape[1], ntasks, ptr(sums), stream_handle())
+
+
+def window_lhs(wsum, ws_ld: int, c: int, r: int, s: int, ck: int, rowck, bias, n_out: int, m: int, lhs) -> None:
+    """abft_window_lhs: lhs[0] += colck_im2col(A) . rowck(B) (+ m * sum(bias)) from a producer's
+    window sums (fp32 [buckets][ws_ld]); rowck fp32 in the packed (r, s, ck) K order."""
+    _lib.call("abft_window_lhs", ptr(wsum), int(ws_ld), int(c), int(r), int(s), int(ck), ptr(rowck),
+              ptr(bias) if bias is not None else None, int(n_out), ctypes.c_int64(int(m)), ptr(lhs), stream_handle())
+

@@ -21,14 +21,15 @@ from . import device as D
 from . import kernels
 from .cost import MeasuredTimings, select
 from .profiler import graph_time_us
-from .protected_network import GLOBAL_DOT, SELECTABLE, GraphedNetwork, ProtectedNetwork
+from .protected_network import GLOBAL_DOT, GLOBAL_FUSED, SELECTABLE, GraphedNetwork, ProtectedNetwork
 from .schemes import Scheme
 from .shapes import DeviceProfile
 
 
 # plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output
-# stores; the chunk-split epilogue for narrow tiles
-PLAN_FLAGS = (0, 1, 4, 5, 8, 16)
+# stores; the chunk-split epilogue for narrow tiles; the split accumulator tail of 256-wide global
+# tiles; 64-byte-row output stores
+PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 32, 512)
 
 
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,
@@ -38,26 +39,47 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
     t_ver = graph_time_us(lambda: kernels.verify_partials(net.partials, net.ks, len(net.layers), net.numeric,
                                                           out=net.verdict_buf, detected_count=net.counters[1:2]),
                           iters)
+    # what a producer's epilogue pays for accumulating its consumers' window sums (charged to the
+    # consumer's fused global variant; measured on the producer's unprotected launch)
+    ws_cost = {}
+    if global_variants:
+        for P in net.layers:
+            if not P.ws_mode:
+                continue
+            it = iters if P.flops() < 2e11 else max(3, iters // 3)
+            t_off = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
+            P.ws_active = True
+            P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
+            t_on = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
+            P.ws_active = False
+            P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
+            ws_cost[P.index] = max(0.0, t_on - t_off)
     for L in net.layers:
         it = iters if L.flops() < 2e11 else max(3, iters // 3)
         times = {s: graph_time_us(lambda s=s: net.launch(L, s), it) for s in SELECTABLE}
         if global_variants:
             # the global scheme's lhs source: checksum MMA slice vs checksum-warp dot, the faster
             t_dot = graph_time_us(lambda: net.launch(L, GLOBAL_DOT), it)
+            best_var = "slice"
             if t_dot < times[S.GLOBAL_ABFT]:
-                times[S.GLOBAL_ABFT] = t_dot
-                net.set_global_variant(L, "dot")
-            else:
-                net.set_global_variant(L, "slice")
+                times[S.GLOBAL_ABFT], best_var = t_dot, "dot"
+            # and the producer-fused activation checksum (this kernel + the window-lhs launch + the
+            # producer epilogue's window sums)
+            if L.producer is not None:
+                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED), it) + ws_cost.get(L.producer.index, 0.0)
+                if t_fused < times[S.GLOBAL_ABFT]:
+                    times[S.GLOBAL_ABFT], best_var = t_fused, "fused"
+            net.set_global_variant(L, best_var)
             # and its plan hints (no k-block pairs / double output staging), the fastest
-            gkey = GLOBAL_DOT if L.gvar == "dot" else S.GLOBAL_ABFT
+            gkey = {"dot": GLOBAL_DOT, "fused": GLOBAL_FUSED}.get(L.gvar, S.GLOBAL_ABFT)
             best_fl = 0
             for fl in PLAN_FLAGS[1:]:
                 try:
                     net.set_tile(L, gkey, 0, fl)
                 except Exception:      # noqa: BLE001
                     continue
-                t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT), it)
+                t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT), it) + \
+                    (ws_cost.get(L.producer.index, 0.0) if L.gvar == "fused" else 0.0)
                 if t_fl < times[S.GLOBAL_ABFT]:
                     times[S.GLOBAL_ABFT], best_fl = t_fl, fl
             net.set_tile(L, gkey, 0, best_fl)
@@ -125,6 +147,7 @@ def refine_in_network(net: ProtectedNetwork, measured: MeasuredTimings, window: 
         keep = L.scheme
         alt = S.GLOBAL_ABFT if keep is S.THREAD_ONE_SIDED else S.THREAD_ONE_SIDED
         L.scheme = alt
+        net._refresh_window_sums()      # a fused global consumer needs its producer's window sums
         g_alt = GraphedNetwork(net, warmup=1)
         t_cur, t_alt = _forward_ms([cur.graph, g_alt.graph], reps)
         # thread-level only when it is faster alone AND in the network; global on ties
@@ -135,6 +158,7 @@ def refine_in_network(net: ProtectedNetwork, measured: MeasuredTimings, window: 
             switched.append((L.index, keep.value, alt.value, round(t_cur, 4), round(t_alt, 4)))
         else:
             L.scheme = keep
+            net._refresh_window_sums()
     return switched
 
 

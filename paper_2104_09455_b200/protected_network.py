@@ -45,7 +45,11 @@ from .shapes import BINARY16, DType, GemmShape
 
 SELECTABLE = (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED)
 GLOBAL_DOT = "global-dot"      # argument-set key of the global scheme with the checksum-warp lhs
-ARG_KEYS = SELECTABLE + (GLOBAL_DOT,)
+# ... and with the lhs from the producer's fused window sums (abft_window_lhs): the kernel runs the
+# output summation only (plan_flags bit 10)
+GLOBAL_FUSED = "global-fused"
+ARG_KEYS = SELECTABLE + (GLOBAL_DOT, GLOBAL_FUSED)
+EXT_LHS = 1024
 _VERDICT_DTYPE = np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"), ("det", "<i4"), ("k", "<i4")])
 
 
@@ -118,7 +122,11 @@ class LinearLayer:
     fault_args: Dict = field(default_factory=dict)
     tile_n: Dict = field(default_factory=dict)     # per-scheme CTA tile override (0 / absent: planner's)
     flags: Dict = field(default_factory=dict)      # per-scheme plan hints (abft_gemm_args_t.plan_flags)
-    gvar: str = "slice"       # global-ABFT lhs: "slice" (checksum MMA N-slice) or "dot" (checksum warps)
+    gvar: str = "slice"       # global-ABFT lhs: "slice" (checksum MMA N-slice), "dot" (checksum warps) or
+                              # "fused" (the producer's window sums, when `producer` is set)
+    producer: Optional["LinearLayer"] = None   # the layer whose stored output is exactly this layer's input
+    ws_mode: int = 0          # as a producer: 0 none, 1 column sums, 2 3x3 window buckets (for fused consumers)
+    ws_active: bool = False   # as a producer: a consumer currently takes its global lhs from our window sums
 
     @property
     def oc(self) -> int:
@@ -178,12 +186,20 @@ class ProtectedNetwork:
         with t.no_grad():
             self.output = _build(self, model)
         nl = len(self.layers)
+        self._find_fused_edges()
         # per-forward accumulators, ONE block cleared by one memset: per-CTA (lhs, rhs) slots of every
-        # layer [nl][cap][2] fp64, then the counters [fired thread tiles, flagged layers] int32
+        # layer [nl][cap][2] fp64, the counters [fired thread tiles, flagged layers] int32, then the
+        # producers' window-sum buckets [9][cp] fp32
         self.cap = max(1, D.sm_count())
-        self._block = t.zeros(16 * self.cap * nl + 16, dtype=t.uint8, device="cuda")
+        ws_floats = [9 * L.out.cp if L.ws_mode else 0 for L in self.layers]
+        base = 16 * self.cap * nl + 16
+        self._block = t.zeros(base + 4 * sum(ws_floats), dtype=t.uint8, device="cuda")
         self.partials = self._block[:16 * self.cap * nl].view(t.float64).view(nl, self.cap, 2)
         self.counters = self._block[16 * self.cap * nl:16 * self.cap * nl + 8].view(t.int32)
+        off = base
+        for L, nf in zip(self.layers, ws_floats):
+            L._wsum = self._block[off:off + 4 * nf].view(t.float32) if nf else None
+            off += 4 * nf
         self.sums = t.zeros((nl, 2), dtype=t.float64, device="cuda")
         self.verdict_buf = t.zeros(nl * _VERDICT_DTYPE.itemsize, dtype=t.uint8, device="cuda")
         # the reduction vector of the sharded verification: [sums (2 nl) | fired | flagged]
@@ -192,6 +208,42 @@ class ProtectedNetwork:
             self._build_layer(L)
         self.ks = t.tensor([L.k_ref for L in self.layers], dtype=t.int32, device="cuda")
         self.set_schemes(schemes)
+
+    def _find_fused_edges(self) -> None:
+        """Consumers whose input is exactly a producer layer's stored output (no glue in between, a
+        dense NHWC buffer) and whose im2col column sums the producer's epilogue can accumulate:
+        pointwise stride-1 layers (column sums) and 3x3 / stride 1 / pad 1 convs (window buckets)."""
+        by_out = {id(L.out): L for L in self.layers}
+        for L in self.layers:
+            P = by_out.get(id(L.x))
+            if P is None or P.out.phys is not None or P.out.cp != int(P.out.buf.shape[3]) or L.kind != "conv":
+                continue
+            pointwise = (L.r, L.s, L.stride, L.pad) == (1, 1, 1, 0)
+            window = (L.r, L.s, L.stride, L.pad) == (3, 3, 1, 1)
+            if not (pointwise or window) or P.out.cp > (512 if window else 4096):
+                continue
+            L.producer = P
+            P.ws_mode = max(P.ws_mode, 2 if window else 1)
+        for L in self.layers:
+            if L.ws_mode == 1 and L.out.cp > 4096:
+                L.ws_mode = 0
+
+    def fused_consumers(self, P: LinearLayer):
+        return [L for L in self.layers if L.producer is P]
+
+    def _refresh_window_sums(self) -> None:
+        """Producers accumulate window sums exactly while a consumer runs the fused global lhs."""
+        for P in self.layers:
+            if not P.ws_mode:
+                continue
+            active = any(C.scheme is Scheme.GLOBAL_ABFT and C.gvar == "fused" for C in self.fused_consumers(P))
+            if active != P.ws_active:
+                P.ws_active = active
+                for key in ARG_KEYS:
+                    if key in P.args:
+                        P.args[key] = self._make_args(P, key)
+                for key in list(P.fault_args):
+                    P.fault_args[key] = self._make_args(P, key, faults=P._fault_keep)
 
     # ---------------------------------------------------------------- building blocks
     def new_act(self, n: int, h: int, w: int, c: int, cp: Optional[int] = None) -> Act:
@@ -304,15 +356,23 @@ class ProtectedNetwork:
         L._res = L.residual.matrix() if L.residual is not None else None
         # rowck(B) in the packed K layout, zero-padded to whole 64-column k-blocks: the "dot" lhs
         L._rowck = kernels.weight_rowck(L._bt, oc8, L._k, self.dtype)
-        for key in ARG_KEYS:
+        for key in self.keys_of(L):
             L.args[key] = self._make_args(L, key)
 
+    @staticmethod
+    def keys_of(L: LinearLayer):
+        """The argument sets a layer has: every selectable scheme, the dot lhs, and the fused lhs when
+        a producer's epilogue can supply its activation checksum."""
+        return ARG_KEYS if L.producer is not None else tuple(k for k in ARG_KEYS if k != GLOBAL_FUSED)
+
     def _kw(self, L: LinearLayer, key, faults=None) -> dict:
-        scheme = Scheme.GLOBAL_ABFT if key == GLOBAL_DOT else key
+        scheme = Scheme.GLOBAL_ABFT if key in (GLOBAL_DOT, GLOBAL_FUSED) else key
         tl = self.tiling
         kw = dict(out=L._c, ldc=L.out.ld, out_kind="bf16" if self.sd == self.t.bfloat16 else "f16", relu=L.relu,
                   bias=L._bias_dev, residual=L._res, ld_res=L.residual.ld if L.residual is not None else 0,
-                  tile_n=L.tile_n.get(key, 0), plan_flags=L.flags.get(key, 0))
+                  tile_n=L.tile_n.get(key, 0), plan_flags=L.flags.get(key, 0) | (EXT_LHS if key == GLOBAL_FUSED else 0))
+        if L.ws_active:
+            kw.update(wsum=L._wsum, ws_ld=L.out.cp, ws_mode=L.ws_mode, ws_P=L.out.h, ws_Q=L.out.w)
         if faults is not None:
             kw["faults"], kw["nfaults"] = faults
         if scheme is Scheme.GLOBAL_ABFT:
@@ -343,7 +403,7 @@ class ProtectedNetwork:
 
     def _make_args(self, L: LinearLayer, key, faults=None):
         kw = self._kw(L, key, faults)
-        scheme = Scheme.GLOBAL_ABFT if key == GLOBAL_DOT else key
+        scheme = Scheme.GLOBAL_ABFT if key in (GLOBAL_DOT, GLOBAL_FUSED) else key
         oc8 = _r8(L.oc)
         if key is Scheme.GLOBAL_ABFT:
             if not hasattr(L, "_gck"):
@@ -379,24 +439,42 @@ class ProtectedNetwork:
 
     def set_global_variant(self, L: LinearLayer, variant: str) -> None:
         """The global-ABFT lhs source of one layer: "slice" (an extra MMA N-slice against the weight
-        tile's row sums) or "dot" (the checksum warps dot each staged A tile with rowck(B) on CUDA
-        cores; the CTA tile stays as wide as the unprotected one)."""
-        if variant not in ("slice", "dot"):
-            raise ValueError("global variant is 'slice' or 'dot'")
+        tile's row sums), "dot" (the checksum warps dot each staged A tile with rowck(B) on CUDA
+        cores; the CTA tile stays as wide as the unprotected one) or "fused" (the producer layer's
+        epilogue accumulates this layer's activation checksum — window sums of its stored output —
+        and abft_window_lhs dots it with rowck(B) after the layer: no checksum work in this kernel)."""
+        if variant not in ("slice", "dot", "fused"):
+            raise ValueError("global variant is 'slice', 'dot' or 'fused'")
+        if variant == "fused" and L.producer is None:
+            raise ValueError(f"{L.name}: no producer layer supplies its window sums")
         L.gvar = variant
+        self._refresh_window_sums()
 
     @staticmethod
     def _key(L: LinearLayer, scheme: Scheme):
-        return GLOBAL_DOT if scheme is Scheme.GLOBAL_ABFT and L.gvar == "dot" else scheme
+        if scheme is Scheme.GLOBAL_ABFT and L.gvar == "dot":
+            return GLOBAL_DOT
+        if scheme is Scheme.GLOBAL_ABFT and L.gvar == "fused":
+            return GLOBAL_FUSED
+        return scheme
 
     def launch(self, L: LinearLayer, scheme=None) -> None:
-        """One layer's kernel under `scheme` (default: the layer's), or under GLOBAL_DOT explicitly."""
-        key = self._key(L, L.scheme if scheme is None else scheme) if scheme != GLOBAL_DOT else GLOBAL_DOT
+        """One layer's kernel under `scheme` (default: the layer's; GLOBAL_DOT / GLOBAL_FUSED pick a
+        global variant explicitly).  The fused variant is the kernel (output summation only) plus
+        the window-lhs launch adding colck(A) . rowck(B) + M * sum(bias) to the layer's lhs slot."""
+        if scheme in (GLOBAL_DOT, GLOBAL_FUSED):
+            key = scheme
+        else:
+            key = self._key(L, L.scheme if scheme is None else scheme)
         kind, args = L.fault_args.get(key) or L.args[key]
         if kind == "gemm":
             kernels._lib.check(kernels._lib.load().abft_gemm(kernels.ctypes.byref(args), D.stream_handle()))
         else:
             kernels.conv2d(args)
+        if key == GLOBAL_FUSED:
+            P = L.producer
+            kernels.window_lhs(P._wsum, P.out.cp, L.x.cp, L.r, L.s, L._k // (L.r * L.s), L._rowck, L._bias_dev,
+                               _r8(L.oc), L.m, self.partials[L.index, 0, 0:1])
 
     # ---------------------------------------------------------------- schemes / faults
     def set_schemes(self, schemes) -> None:
@@ -410,6 +488,7 @@ class ProtectedNetwork:
             if s not in SELECTABLE:
                 raise ValueError(f"network layers take {[x.value for x in SELECTABLE]}, got {s}")
             L.scheme = s
+        self._refresh_window_sums()
 
     def schemes(self) -> List[Scheme]:
         return [L.scheme for L in self.layers]
@@ -426,7 +505,7 @@ class ProtectedNetwork:
                 continue
             ft = D.faults_tensor(list(cells))
             L._fault_keep = ft
-            for key in ARG_KEYS:
+            for key in self.keys_of(L):
                 L.fault_args[key] = self._make_args(L, key, faults=ft)
 
     # ---------------------------------------------------------------- forward

@@ -218,3 +218,42 @@ def test_benchmarked_layers_at_batch_256(PN, name, layers):
     net.inject({L0.index: [(L0.m - 3, 5, 8.0 * tau + 64.0)]})
     net.forward(x)
     assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [L0.index]
+
+
+@pytest.mark.parametrize("name", ["vgg16", "resnet50"])
+def test_fused_window_checksums(PN, name):
+    """Global ABFT with the producer-fused activation checksum: a producer's epilogue
+    accumulates window sums of its stored output, the consumer runs only the output summation and
+    abft_window_lhs rebuilds colck(im2col(x)) . rowck(B) (+ M * sum(bias)).  Clean runs agree far
+    inside tau on every fused layer; a fault in a fused consumer is flagged there and only there,
+    and a fault in its producer is flagged at the producer only (the consumer's checksum comes from
+    the faulty activation it really reads, as in run_protected_pipeline, checksum.py:207-237)."""
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model(name), 2, schemes=S.GLOBAL_ABFT)
+    fused = [L for L in net.layers if L.producer is not None]
+    assert len(fused) >= (8 if name == "vgg16" else 20), [L.name for L in fused]
+    for L in fused:
+        net.set_global_variant(L, "fused")
+    assert all(L.producer.ws_active for L in fused)
+    x = _input(2, seed=5)
+    net.forward(x)
+    torch.cuda.synchronize()
+    assert net.flags() == (0, 0)
+    vs = net.verdicts()
+    for L in net.layers:
+        check_layer(L)
+        v = vs[L.index]
+        assert not v.detected and abs(v.lhs - v.rhs) < 0.05 * v.tolerance_used, (L.name, v)
+    C = next(L for L in fused if L.k_ref <= 600)
+    P = C.producer
+    for target in (C, P):
+        tau = vs[target.index].tolerance_used
+        net.inject({target.index: [(target.m // 2, 3, 8.0 * tau + 64.0)]})
+        net.forward(x)
+        got = [i for i, v in enumerate(net.verdicts()) if v.detected]
+        assert got == [target.index], (target.name, got)
+    net.inject({})
+    # switching the consumer away from the fused lhs stops the producer's window sums
+    net.set_global_variant(C, "slice")
+    assert not P.ws_active or any(L.gvar == "fused" for L in net.fused_consumers(P))
