@@ -142,10 +142,10 @@ typedef struct {
    * when one would buy a pipeline stage; bit 3 = direct 16-byte stores of the output from the
    * epilogue registers instead of shared-memory staging + bulk tensor stores.  The profilers time
    * the alternatives and keep the fastest (T_o = min over plans); bit 4 = the chunk-split epilogue
-   * (both warp sets on every tile) for narrow tiles, which otherwise alternate whole tiles; bit 5 =
-   * global ABFT on a 256-wide tile splits the accumulator (columns 240..255 and the checksum slice
-   * in a shared TMEM tail, the rest double-buffered); bits 6-8 = k-blocks of gathered-stem copies
-   * in flight (3..7, 0 = 3). */
+   * (both warp sets on every tile) for narrow tiles, which otherwise alternate whole tiles; bits 6-8
+   * = k-blocks of gathered-stem copies in flight (3..7, 0 = 3); bit 9 = 64-byte-row output stores
+   * (32-column boxes) instead of 128-byte rows; bit 10 = the global lhs comes from outside the
+   * kernel (see wsum below). */
   int32_t plan_flags;
   /* optional window column sums of THIS layer's stored output (after bias / residual / ReLU /
    * rounding) for the next layer's global lhs (the fused activation checksum):
@@ -167,6 +167,11 @@ int abft_gemm(const abft_gemm_args_t* args, void* stream);
  * consumer's (R x S, stride 1, "same" padding) input rebuilt from the nine buckets (R = S = 3) or
  * the plain column sums (R = S = 1) — the reference's checksum_dot(colck(A), rowck(B))
  * (checksum.py:108-117) on the lowered GEMM.  fp64 dot, one atomic add into *lhs. */
+/* Buckets 1..8 of the window sums (rows on the first / last row and column of each image and the
+ * four corners) of an NHWC activation [n][h][w][c] (ldx elements per pixel), from its border
+ * pixels; bucket 0 comes from the producer (abft_gemm_args_t.wsum, ws_mode 1). Accumulates. */
+int abft_nhwc_border_sums(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t dtype,
+                          float* wsum, int32_t ws_ld, void* stream);
 int abft_window_lhs(const float* wsum, int32_t ws_ld, int32_t C, int32_t R, int32_t S, int32_t ck,
                     const float* rowck, const float* bias, int32_t n_out, int64_t M, double* lhs, void* stream);
 
@@ -303,6 +308,11 @@ int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w, int32_t c, i
 int abft_nhwc_maxpool(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t k,
                       int32_t stride, int32_t pad, int32_t ceil_mode, int32_t dtype, void* out, int64_t ldo,
                       void* stream);
+/* the same max pooling, also accumulating the window column sums of its output for the next
+ * layer's fused global lhs (layout and ws_mode as abft_gemm_args_t.wsum; the caller zeroes wsum) */
+int abft_nhwc_maxpool_ws(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t k,
+                         int32_t stride, int32_t pad, int32_t ceil_mode, int32_t dtype, void* out, int64_t ldo,
+                         float* wsum, int32_t ws_ld, int32_t ws_mode, void* stream);
 /* global average pooling: out[n][c] = mean over the hw pixels of image n (fp32 sum) */
 int abft_nhwc_avgpool(const void* x, int32_t n, int32_t hw, int32_t c, int64_t ldx, int32_t dtype, void* out,
                       int64_t ldo, void* stream);

@@ -47,7 +47,9 @@ EXPORTED_SYMBOLS = (
     "abft_version",
     "abft_device_sms",
     "abft_window_lhs",
+    "abft_nhwc_border_sums",
     "abft_nhwc_maxpool",
+    "abft_nhwc_maxpool_ws",
     "abft_nhwc_avgpool",
     "abft_nhwc_interleave2",
     "abft_sum_partials",

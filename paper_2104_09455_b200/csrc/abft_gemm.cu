@@ -88,11 +88,6 @@ struct GemmParams {
   uint32_t off_ones;     // smem [64 x 128 B] tile of ones (mode 1)
   uint32_t idesc_ones;
   int epi_split;         // 1: both epilogue warps of a lane quadrant take chunks (round-robin)
-  int tail_split;        // 1 (global ABFT, tile_n 256, lean epilogue): the MMA writes output columns [0, 240) into a
-                         //    double-buffered stage and columns [240, 256) + the 16-column checksum slice into a
-                         //    shared 32-column tail (TMEM columns tail_col..+31) that the epilogue drains first,
-                         //    so the 272-column tile no longer forces a single accumulator stage
-  int tail_col;
   int gdepth;            // gathered stems: k-blocks of cp.async copies in flight per gather thread (3..7)
   int epi_tiles;         // 1 (lean epilogues, narrow tiles): warps 2-5 take the even tiles of the CTA, warps 6-9
                          //    the odd ones, each warp all chunks of its quadrant — two tiles' epilogues in
@@ -229,8 +224,8 @@ __device__ __forceinline__ float warp_column_sums(float (&v)[32], int lane) {
 // column q == 0 / Q-1 and the four corners (rows are output pixels (n*P + p)*Q + q).  Border
 // buckets only reduce when the warp holds such a row (ballot), so interior chunks pay one
 // transpose-reduce (31 shuffles).
-__device__ __forceinline__ void wsum_chunk(const GemmParams& p, float* ws_s, const float (&vr)[32], int gm, bool row_ok,
-                                           int gc0, int ncols, int lane) {
+__device__ __forceinline__ void wsum_chunk(const GemmParams& p, float* ws_s, const float* vr, int gm, bool row_ok, int gc0,
+                                        int ncols, int lane) {
   float t[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) t[j] = (row_ok && j < ncols) ? vr[j] : 0.f;
@@ -495,7 +490,9 @@ __device__ __forceinline__ void lean_store_row(const float (&v)[32], void* C, in
 
 // AM: the A-load family of the instance — 0 TMA tiles / im2col boxes (a_mode 0-2), 1 halo
 // windows (a_mode 4), 2 gathered stems (a_mode 5)
-template <typename T, int CLASS, int NT, int AM>
+// WS: the instance accumulates window sums of its output (a producer of fused consumers); kept out
+// of the other instances, whose epilogue loops would otherwise spill
+template <typename T, int CLASS, int NT, int AM, bool WS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     abft_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmCK, const __grid_constant__ CUtensorMap tmC,
@@ -524,7 +521,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* dfull = tempty + 4;     // column-sum TMEM buffers (acolck_mode 1), DCK_BUFS deep
   uint64_t* dempty = dfull + DCK_BUFS;
   uint64_t* bres = dempty + DCK_BUFS;    // resident-B loaded (b_resident)
-  uint64_t* tailempty = bres + 1;        // the shared accumulator tail drained (tail_split)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bres + 2);
   double* red_d = reinterpret_cast<double*>(tmem_holder + 4);
 
@@ -562,7 +558,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&empty[s], (!gather && (p.acolck_mode == 2 || p.lhs_w != nullptr)) ? 5 : 1);
     }
     ptx::mbar_init(bres, 1);
-    ptx::mbar_init(tailempty, 4);      // the four warps that own the tile's last chunk
     for (int a = 0; a < DCK_BUFS; ++a) {
       ptx::mbar_init(&dfull[a], 1);
       ptx::mbar_init(&dempty[a], 4);    // one arrival per checksum warp
@@ -586,7 +581,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 256) colck_s[i] = 0.f;
   }
-  if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.wsum != nullptr) {
+  if (WS && warp >= EPI_WARP0 && warp < CK_WARP0) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.ws_nb * p.N; i += 256) ws_s[i] = 0.f;
   }
   if (warp >= CK_WARP0 && p.acolck_in_smem) {
@@ -813,7 +808,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int acc = t_local % L_acc_stages;
         const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
-        if (p.tail_split) ptx::mbar_wait(tailempty, ((uint32_t)t_local & 1u) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * L_cols_per_acc);
         if (p.kpair) {
@@ -840,8 +834,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (fast) {
           // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
-          const bool tail = p.tail_split != 0;
-          const uint32_t tail_d = tmem_base + (uint32_t)p.tail_col;
 #pragma unroll 1
           for (int kb = 0; kb < L_nkb; ++kb) {
             ptx::mbar_wait(&full[s], ph);
@@ -853,13 +845,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t accum = (kb | k) != 0;
               ptx::mma_f16_ss_w(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
-              if (tail) {
-                // weight rows 240..255 (30 SW128 atoms on) and the checksum rows into the tail
-                ptx::mma_f16_ss_w(tail_d, ad + (uint64_t)k * a_kstep, bd + 1920ull + 2ull * k, L_idesc_ck, accum);
-                ptx::mma_f16_ss_w(tail_d + 16, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
-              } else if (ck_loaded) {
-                ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
-              }
+              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
             }
             ptx::mma_commit_w(&empty[s]);
             if (++s == L_stages) { s = 0; ph ^= 1; }
@@ -1466,38 +1452,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
         const uint32_t tacc = tmem_base + lane_addr + (uint32_t)(acc * cols_per_acc);
-        const bool tail = p.tail_split != 0;
-        const bool gck_ld = p.gck && !tail && (h == 0 || epi_tiles);
+        const bool gck_ld = p.gck && (h == 0 || epi_tiles);
         float ck_hi = 0.f, ck_lo = 0.f;
         float tsum = 0.f;
-        float tv[16];
-        if (tail && h == 1) {
-          // the shared tail first (output columns 240..255 and the checksum pair), then release it
-          // so the next tile's MMAs can start while this tile's stage drains
-          const uint32_t ta = tmem_base + lane_addr + (uint32_t)p.tail_col;
-          ptx::tmem_ldn<16>(ta, tv);
-          ptx::tmem_ld2(ta + 16, ck_hi, ck_lo);
-          ptx::tmem_ld_wait();
-          if (row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tailempty);
-        }
         bool unit_wide = false;
 #pragma unroll 1
         for (int c0 = c_first; c0 < bn_eff; c0 = c_next(c0)) {
           float v[32];
           __syncwarp();
-          if (tail && c0 == 224) {
-            // columns 224..239 from the stage, 240..255 from the tail (read above)
-            float v16[16];
-            ptx::tmem_ldn<16>(tacc + c0, v16);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) { v[j] = v16[j]; v[16 + j] = tv[j]; }
-          } else {
-            ptx::tmem_ld32(tacc + c0, v);
-          }
+          ptx::tmem_ld32(tacc + c0, v);
           if (gck_ld && c0 == c_first) ptx::tmem_ld2(tacc + bn, ck_hi, ck_lo);
           ptx::tmem_ld_wait();
           if (gck_ld && c0 == c_first && row_in_tile) lhs_acc += (double)ck_hi + (double)ck_lo;
@@ -1525,7 +1488,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int cn = c_next(c0);
             have_rb = cn < bn_eff && residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
           }
-          if (p.wsum != nullptr) {
+          if constexpr (WS) {
             float vr[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
@@ -1608,7 +1571,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               have_rb = cn < bn_eff &&
                         residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
             }
-            if (p.wsum != nullptr) {
+            if constexpr (WS) {
               float vr[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
@@ -1817,19 +1780,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             if (j < ncols) v[j] += TR::unpack2((uint32_t)__ldg(r16 + j)).x;
         }
-        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr || p.wsum != nullptr)) {
+        if ((p.out_dtype != ABFT_OUT_NONE || p.next_colck != nullptr || WS)) {
           // ReLU (checksum.py:235 storage_array(activation(c))): folded into the 16-bit pack of
           // the TMA-store path; applied here for fp32 outputs, direct stores and the fused colck
           // whole 32-column chunks go out by bulk tensor stores; a tile's 16-column tail (bn_eff = 240
           // etc.) by direct stores
           const bool chunk_tma = p.tma_store && cmax >= 32 && q_full;
           const bool relu_in_pack = p.relu && chunk_tma && p.out_dtype != ABFT_OUT_F32 && p.next_colck == nullptr &&
-                                    p.wsum == nullptr;
+                                    !WS;
           if (p.relu && !relu_in_pack) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
           }
-          if ((p.next_colck != nullptr || p.wsum != nullptr) && p.out_dtype != ABFT_OUT_F32) {
+          if ((p.next_colck != nullptr || WS) && p.out_dtype != ABFT_OUT_F32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = round_out(v[j], p.out_dtype);
           }
@@ -1913,7 +1876,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
-          if (p.wsum != nullptr) wsum_chunk(p, ws_s, v, gm, row_store, gc0, min(cmax, p.N - gc0), lane);
+          if constexpr (WS) wsum_chunk(p, ws_s, v, gm, row_store, gc0, min(cmax, p.N - gc0), lane);
           if (p.next_colck != nullptr) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (row_store && j < cmax && gc0 + j < p.N) ? v[j] : 0.f;
@@ -1973,7 +1936,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (x != 0.f) atomicAdd(&p.next_colck[i], x);
       }
     }
-    if (p.wsum != nullptr) {
+    if (WS) {
       ptx::named_bar_sync(3, 256);
       for (int i = et; i < p.ws_nb * p.N; i += 256) {
         const float x = ws_s[i];
@@ -2104,13 +2067,13 @@ int cached_map(CUtensorMap* out, const void* base, int dtype, int64_t k, int64_t
   return ABFT_OK;
 }
 
-template <typename T, int CLASS, int NT, int AM>
+template <typename T, int CLASS, int NT, int AM, bool WS>
 int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mo, const CUtensorMap& mo2,
                 const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(abft_gemm_kernel<T, CLASS, NT, AM, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
@@ -2125,27 +2088,39 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM>, ma, mb, mc, mo, mo2, p),
+    return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM, WS>, ma, mb, mc, mo, mo2, p),
                       "abft_gemm_kernel launch (PDL)");
   }
-  abft_gemm_kernel<T, CLASS, NT, AM><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo2, p);
+  abft_gemm_kernel<T, CLASS, NT, AM, WS><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo2, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
 }
 
 template <typename T, int AM>
 int launch_cls(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                const CUtensorMap& mo, const CUtensorMap& mo2, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
-  if (cls == CLASS_PLAIN) return launch_inst<T, CLASS_PLAIN, 0, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+  const bool ws = p.wsum != nullptr;
+  if (cls == CLASS_PLAIN) {
+    if (ws) return launch_inst<T, CLASS_PLAIN, 0, AM, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    return launch_inst<T, CLASS_PLAIN, 0, AM, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+  }
   if (cls == CLASS_CHECKSUM) {
-    if (ntc == 8) return launch_inst<T, CLASS_CHECKSUM, 8, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_CHECKSUM, 16, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
-    if constexpr (AM != 2) return launch_inst<T, CLASS_CHECKSUM, 0, AM>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if (ntc == 8) {
+      if (ws) return launch_inst<T, CLASS_CHECKSUM, 8, AM, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+      return launch_inst<T, CLASS_CHECKSUM, 8, AM, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    }
+    if (ntc == 16) {
+      if (ws) return launch_inst<T, CLASS_CHECKSUM, 16, AM, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+      return launch_inst<T, CLASS_CHECKSUM, 16, AM, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    }
+    if (ws) return fail(ABFT_E_UNSUPPORTED, "window sums with a thread-level check need thread_n 8 or 16");
+    if constexpr (AM != 2) return launch_inst<T, CLASS_CHECKSUM, 0, AM, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
     return fail(ABFT_E_UNSUPPORTED, "gathered stems take thread_n 8 or 16");
   }
+  if (ws) return fail(ABFT_E_UNSUPPORTED, "window sums are not produced by the replication schemes");
   if constexpr (AM == 0) {
-    if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
-    if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
-    return launch_inst<T, CLASS_REPLICA, 0, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if (ntc == 8) return launch_inst<T, CLASS_REPLICA, 8, 0, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    if (ntc == 16) return launch_inst<T, CLASS_REPLICA, 16, 0, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    return launch_inst<T, CLASS_REPLICA, 0, 0, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
   }
   return fail(ABFT_E_UNSUPPORTED, "replication schemes have no halo / gathered conv path");
 }
@@ -2281,16 +2256,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // Thread-level schemes keep <= 32 checksum groups per tile; ties go to the wider tile.
     int best = 0;
     long long best_cost = 0;
-    // (the lean-epilogue conditions under which a 256-wide global tile splits its accumulator tail)
-    const bool tail_est = (a->out_dtype == ABFT_OUT_F16 || a->out_dtype == ABFT_OUT_BF16) && a->next_colck == nullptr &&
-                          (a->faults == nullptr || a->nfaults == 0) && a->a_colck == nullptr && !(a->plan_flags & 32);
     for (int cand : {256, 240, 224, 192, 128, 64, 32}) {
       if (cand < nt || (thread_level && cand / nt > 32)) continue;
       if (gather && (cand / nt) * nt < n_ext) continue;    // gathered stems: one N block (resident B)
       if (cand == 240 && (thread_level || !(gck && a->ck_layout == 1))) continue;   // 240 + 16 checksum rows
       const int cols = tile_cols(cand, nt, has_ck, has_shadow, split) + (gck ? 16 : 0);
       if (cols + extra_cols > 512) continue;
-      const bool dbuf = 2 * cols + extra_cols <= 512 || (cand == 256 && gck && tail_est && (a->plan_flags & 32));
+      const bool dbuf = 2 * cols + extra_cols <= 512;
       const int eff = (cand / nt) * nt;
       const long long tiles = (long long)m_blocks * ceil_div(n_ext, eff);
       // whole waves while a CTA runs few tiles; fractional beyond 4 waves, where the CTAs with one
@@ -2474,21 +2446,6 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
       if (p.acc_stages < 2) p.epi_tiles = 0, p.acc_stages = 1;
       p.dck_col = p.acc_stages * p.cols_per_acc;
       p.tmem_cols = (int)pow2_at_least((uint32_t)(p.acc_stages * p.cols_per_acc));
-    }
-    // global ABFT on a 256-wide tile: columns [0, 240) double-buffered, the last 16 output columns
-    // and the checksum slice in a shared 32-column tail
-    // (opt-in, plan_flags bit 5: measured slower than the single 272-column stage on the VGG-16
-    // layers — the two N = 16 MMAs per k-step cost more than the serialised epilogue)
-    p.tail_split = (lean_ok && out.cls == CLASS_PLAIN && p.gck && p.ck_mode == 4 && bn == 256 && p.bn_eff == 256 &&
-                    (a->plan_flags & 32)) ? 1 : 0;
-    if (p.tail_split) {
-      p.cols_per_acc = 240;
-      p.acc_stages = 2;
-      p.tail_col = 480;
-      p.dck_col = 512;
-      p.tmem_cols = 512;
-      p.idesc_main = ptx::idesc_f16(a->dtype == ABFT_BF16 ? 1u : 0u, BM, 240);
-      p.idesc_aug = p.idesc_main;
     }
     // 128-byte-row bulk stores (plan_flags bit 9 keeps 64-byte rows)
     p.out_wide = (lean_ok && p.tma_store && p.bn_eff >= 64 && !(a->plan_flags & 512)) ? 1 : 0;

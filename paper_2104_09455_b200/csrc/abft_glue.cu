@@ -35,6 +35,19 @@ struct Max2<__nv_bfloat16> {
   static constexpr uint32_t lowest = 0xFF80FF80u;
 };
 
+template <typename T>
+struct Unpack2;
+template <>
+struct Unpack2<__half> {
+  static __device__ __forceinline__ float2 f(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
+};
+template <>
+struct Unpack2<__nv_bfloat16> {
+  static __device__ __forceinline__ float2 f(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
+  }
+};
+
 // out[n][p][q][c] = max over the window (padding never wins), one 8-channel vector per thread
 template <typename T>
 __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
@@ -66,6 +79,83 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const T* __restrict__
     }
     *reinterpret_cast<uint4*>(out + ((n * P + p) * Q + q) * ldo + c8 * 8) = m;
   }
+}
+
+// The same pooling, and the window column sums of its output for the next layer's fused global
+// lhs (buckets as in abft_gemm_args_t.wsum): a thread keeps one 8-channel vector and strides over
+// output pixels, summing the stored (rounded) maxima per bucket in registers; one smem reduction
+// and one global atomic per (bucket, channel) and CTA
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_ws_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
+                                                         int P, int Q, int k, int s, int pad, T* __restrict__ out,
+                                                         long long ldo, long long npix, float* __restrict__ wsum,
+                                                         int ws_ld, int ws_mode) {
+  extern __shared__ float wsm[];          // [nb][C]
+  const int cv = C / 8;
+  const int lanes_p = blockDim.x / cv;    // pixels in flight per CTA
+  const int nb = ws_mode == 2 ? 9 : 1;
+  for (int i = threadIdx.x; i < nb * C; i += blockDim.x) wsm[i] = 0.f;
+  __syncthreads();
+  const int c8 = threadIdx.x % cv, lp = threadIdx.x / cv;
+  float acc[9][8];
+#pragma unroll
+  for (int b = 0; b < 9; ++b)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
+  if (lp < lanes_p) {
+    for (long long pix = (long long)blockIdx.x * lanes_p + lp; pix < npix; pix += (long long)gridDim.x * lanes_p) {
+      const int q = (int)(pix % Q);
+      const long long pq = pix / Q;
+      const int p = (int)(pq % P);
+      const long long n = pq / P;
+      uint4 m = make_uint4(Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest);
+      const int h0 = p * s - pad, w0 = q * s - pad;
+      for (int dh = 0; dh < k; ++dh) {
+        const int hh = h0 + dh;
+        if (hh < 0 || hh >= H) continue;
+        for (int dw = 0; dw < k; ++dw) {
+          const int ww = w0 + dw;
+          if (ww < 0 || ww >= W) continue;
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + ((n * H + hh) * W + ww) * ldx + c8 * 8));
+          m.x = Max2<T>::op(m.x, u.x);
+          m.y = Max2<T>::op(m.y, u.y);
+          m.z = Max2<T>::op(m.z, u.z);
+          m.w = Max2<T>::op(m.w, u.w);
+        }
+      }
+      *reinterpret_cast<uint4*>(out + ((n * P + p) * Q + q) * ldo + c8 * 8) = m;
+      float v[8];
+      const uint32_t w4[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = Unpack2<T>::f(w4[e]);
+        v[2 * e] = f.x;
+        v[2 * e + 1] = f.y;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[0][e] += v[e];
+      if (ws_mode == 2) {
+        const bool p0 = p == 0, pl = p == P - 1, q0 = q == 0, ql = q == Q - 1;
+        if (p0 | pl | q0 | ql) {
+          const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (in[b])
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[b + 1][e] += v[e];
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < 9; ++b)
+      if (b < nb)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (acc[b][e] != 0.f) atomicAdd(&wsm[b * C + c8 * 8 + e], acc[b][e]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb * C; i += blockDim.x)
+    if (wsm[i] != 0.f) atomicAdd(&wsum[(long long)(i / C) * ws_ld + (i % C)], wsm[i]);
 }
 
 // out[n][c] = mean over the H*W pixels of image n (fp32 sum, rounded once); CTA = (image, 256-vector slab)
@@ -174,6 +264,43 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_maxpool(const vo
   return cuda_check(cudaGetLastError(), "maxpool launch");
 }
 
+extern "C" __attribute__((visibility("default"))) int abft_nhwc_maxpool_ws(const void* x, int32_t n, int32_t h,
+                                                                          int32_t w, int32_t c, int64_t ldx, int32_t k,
+                                                                          int32_t stride, int32_t pad, int32_t ceil_mode,
+                                                                          int32_t dtype, void* out, int64_t ldo,
+                                                                          float* wsum, int32_t ws_ld, int32_t ws_mode,
+                                                                          void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || c > 2048 || k < 1 || stride < 1 || pad < 0 || 2 * pad > k)
+    return fail(ABFT_E_SHAPE, "maxpool_ws: bad extents (channels a multiple of 8 up to 2048, pad <= k/2)");
+  if (ldx < c || ldx % 8 || ldo < c || ldo % 8) return fail(ABFT_E_SHAPE, "maxpool_ws: ldx/ldo must be >= c and a multiple of 8");
+  if (wsum == nullptr || ws_ld < c || (ws_mode != 1 && ws_mode != 2))
+    return fail(ABFT_E_VALUE, "maxpool_ws: window sums [1 or 9][ws_ld >= c], ws_mode 1 or 2");
+  auto osz = [&](int len) {
+    const int num = len + 2 * pad - k;
+    int o = (ceil_mode ? (num + stride - 1) / stride : num / stride) + 1;
+    if (ceil_mode && (o - 1) * stride >= len + pad) --o;
+    return o;
+  };
+  const int P = osz(h), Q = osz(w);
+  if (P < 1 || Q < 1) return fail(ABFT_E_SHAPE, "maxpool_ws: empty output");
+  const int cv = c / 8;
+  const int threads = cv >= 256 ? cv : (256 / cv) * cv;
+  if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "maxpool_ws: more than 256 channel vectors");
+  const size_t smem = (size_t)(ws_mode == 2 ? 9 : 1) * c * sizeof(float);
+  if (smem > 48 * 1024) return fail(ABFT_E_UNSUPPORTED, "maxpool_ws: 9 buckets x channels beyond 48 KB of smem");
+  const long long npix = (long long)n * P * Q;
+  const int grid = std::max(1, std::min<int>(2 * num_sms(), (int)((npix + 63) / 64)));
+  cudaStream_t st = as_stream(stream);
+  if (dtype == ABFT_BF16)
+    maxpool_ws_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k, stride,
+                                                                   pad, (__nv_bfloat16*)out, ldo, npix, wsum, ws_ld,
+                                                                   ws_mode);
+  else
+    maxpool_ws_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, h, w, c, ldx, P, Q, k, stride, pad,
+                                                            (__half*)out, ldo, npix, wsum, ws_ld, ws_mode);
+  return cuda_check(cudaGetLastError(), "maxpool_ws launch");
+}
+
 extern "C" __attribute__((visibility("default"))) int abft_nhwc_avgpool(const void* x, int32_t n, int32_t hw, int32_t c,
                                                                        int64_t ldx, int32_t dtype, void* out, int64_t ldo,
                                                                        void* stream) {
@@ -202,6 +329,85 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
   interleave2_kernel<__half><<<grid_for(total), 256, 0, st>>>((const __half*)x1, ld1, (const __half*)b, ld2, half,
                                                                (__half*)out, ldo, half_pad, total);
   return cuda_check(cudaGetLastError(), "interleave2 launch");
+}
+
+// The border buckets (1..8) of a 3x3 consumer's window sums, from the activation's border pixels
+// only (first / last row and column of every image): CTA = one image; a thread keeps one
+// 8-channel vector and a slice of the border, sums in registers, one smem reduction and one
+// atomic per (bucket, channel) per image.  Bucket 0 (all pixels) comes from the producer's epilogue.
+template <typename T>
+__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
+                                                          float* __restrict__ ws, int ws_ld) {
+  extern __shared__ float bsm[];           // [8][C]
+  const int cv = C / 8;
+  const int parts = blockDim.x / cv;
+  for (int i = threadIdx.x; i < 8 * C; i += blockDim.x) bsm[i] = 0.f;
+  __syncthreads();
+  const int c8 = threadIdx.x % cv, part = threadIdx.x / cv;
+  const long long img = blockIdx.x;
+  // border pixel list: rows 0 and H-1 (all W columns), then columns 0 and W-1 of rows 1..H-2
+  const int nrow = (H > 1 ? 2 : 1) * W;
+  const int ncol = H > 2 ? (W > 1 ? 2 : 1) * (H - 2) : 0;
+  float acc[8][8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
+  if (part < parts) {
+    for (int i = part; i < nrow + ncol; i += parts) {
+      int hh, ww;
+      if (i < nrow) {
+        hh = (i < W) ? 0 : H - 1;
+        ww = i % W;
+      } else {
+        const int j = i - nrow;
+        hh = 1 + j % (H - 2);
+        ww = (W > 1 && j >= H - 2) ? W - 1 : 0;
+      }
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + ((img * H + hh) * W + ww) * ldx + c8 * 8));
+      float v[8];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = Unpack2<T>::f(w4[e]);
+        v[2 * e] = f.x;
+        v[2 * e + 1] = f.y;
+      }
+      const bool p0 = hh == 0, pl = hh == H - 1, q0 = ww == 0, ql = ww == W - 1;
+      const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (in[b])
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[b][e] += v[e];
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (acc[b][e] != 0.f) atomicAdd(&bsm[b * C + c8 * 8 + e], acc[b][e]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * C; i += blockDim.x)
+    if (bsm[i] != 0.f) atomicAdd(&ws[(long long)(1 + i / C) * ws_ld + (i % C)], bsm[i]);
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(const void* x, int32_t n, int32_t h,
+                                                                           int32_t w, int32_t c, int64_t ldx,
+                                                                           int32_t dtype, float* wsum, int32_t ws_ld,
+                                                                           void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || c > 1024 || ldx < c || ldx % 8 || wsum == nullptr || ws_ld < c)
+    return fail(ABFT_E_SHAPE, "border_sums: bad extents (channels a multiple of 8 up to 1024, ldx >= c)");
+  const int cv = c / 8;
+  const int threads = cv >= 256 ? cv : (256 / cv) * cv;
+  if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "border_sums: more than 256 channel vectors");
+  const size_t smem = (size_t)8 * c * sizeof(float);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == ABFT_BF16)
+    border_sums_kernel<__nv_bfloat16><<<n, threads, smem, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, wsum, ws_ld);
+  else
+    border_sums_kernel<__half><<<n, threads, smem, st>>>((const __half*)x, h, w, c, ldx, wsum, ws_ld);
+  return cuda_check(cudaGetLastError(), "border_sums launch");
 }
 
 // The consumer's global lhs from the producer's window sums (abft_window_lhs): one CTA, fp64.

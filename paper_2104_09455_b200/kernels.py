@@ -256,6 +256,15 @@ def maxpool_nhwc(x, n: int, h: int, w: int, c: int, ldx: int, k: int, stride: in
               storage_code(dtype), ptr(out), ctypes.c_int64(ldo), stream_handle())
 
 
+def maxpool_nhwc_ws(x, n: int, h: int, w: int, c: int, ldx: int, k: int, stride: int, pad: int, ceil_mode: bool,
+                    dtype: DType, out, ldo: int, wsum, ws_ld: int, ws_mode: int) -> None:
+    """Max pooling that also accumulates the window column sums of its output (the next layer's
+    fused global lhs)."""
+    _lib.call("abft_nhwc_maxpool_ws", ptr(x), n, h, w, c, ctypes.c_int64(ldx), k, stride, pad, int(ceil_mode),
+              storage_code(dtype), ptr(out), ctypes.c_int64(ldo), ptr(wsum), int(ws_ld), int(ws_mode),
+              stream_handle())
+
+
 def avgpool_nhwc(x, n: int, hw: int, c: int, ldx: int, dtype: DType, out, ldo: int) -> None:
     _lib.call("abft_nhwc_avgpool", ptr(x), n, hw, c, ctypes.c_int64(ldx), storage_code(dtype), ptr(out),
               ctypes.c_int64(ldo), stream_handle())
@@ -271,6 +280,12 @@ def interleave2(x1, ld1: int, b, ld2: int, pixels: int, half: int, out, ldo: int
 def sum_partials(partials, ntasks: int, sums) -> None:
     """[n, cap, 2] per-CTA (lhs, rhs) slots -> sums [n, 2] fp64 (one launch)."""
     _lib.call("abft_sum_partials", ptr(partials), partials.shape[1], ntasks, ptr(sums), stream_handle())
+
+
+def border_sums(x, n: int, h: int, w: int, c: int, ldx: int, dtype: DType, wsum, ws_ld: int) -> None:
+    """abft_nhwc_border_sums: buckets 1..8 of a 3x3 consumer's window sums from the border pixels."""
+    _lib.call("abft_nhwc_border_sums", ptr(x), n, h, w, c, ctypes.c_int64(ldx), storage_code(dtype), ptr(wsum),
+              int(ws_ld), stream_handle())
 
 
 def window_lhs(wsum, ws_ld: int, c: int, r: int, s: int, ck: int, rowck, bias, n_out: int, m: int, lhs) -> None:

@@ -21,15 +21,14 @@ from . import device as D
 from . import kernels
 from .cost import MeasuredTimings, select
 from .profiler import graph_time_us
-from .protected_network import GLOBAL_DOT, GLOBAL_FUSED, SELECTABLE, GraphedNetwork, ProtectedNetwork
+from .protected_network import GLOBAL_DOT, GLOBAL_FUSED, SELECTABLE, GraphedNetwork, PoolProducer, ProtectedNetwork
 from .schemes import Scheme
 from .shapes import DeviceProfile
 
 
 # plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output
-# stores; the chunk-split epilogue for narrow tiles; the split accumulator tail of 256-wide global
-# tiles; 64-byte-row output stores
-PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 32, 512)
+# stores; the chunk-split epilogue for narrow tiles; 64-byte-row output stores
+PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 512)
 
 
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,
@@ -43,17 +42,21 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
     # consumer's fused global variant; measured on the producer's unprotected launch)
     ws_cost = {}
     if global_variants:
-        for P in net.layers:
-            if not P.ws_mode:
-                continue
-            it = iters if P.flops() < 2e11 else max(3, iters // 3)
-            t_off = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
-            P.ws_active = True
-            P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
-            t_on = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
-            P.ws_active = False
-            P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
-            ws_cost[P.index] = max(0.0, t_on - t_off)
+        for P in net.producers():
+            if isinstance(P, PoolProducer):
+                t_off = graph_time_us(P.run, iters)
+                P.ws_active = True
+                t_on = graph_time_us(P.run, iters)
+                P.ws_active = False
+            else:
+                it = iters if P.flops() < 2e11 else max(3, iters // 3)
+                t_off = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
+                P.ws_active = True
+                P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
+                t_on = graph_time_us(lambda: net.launch(P, S.UNPROTECTED), it)
+                P.ws_active = False
+                P.args[S.UNPROTECTED] = net._make_args(P, S.UNPROTECTED)
+            ws_cost[id(P)] = max(0.0, t_on - t_off)
     for L in net.layers:
         it = iters if L.flops() < 2e11 else max(3, iters // 3)
         times = {s: graph_time_us(lambda s=s: net.launch(L, s), it) for s in SELECTABLE}
@@ -66,7 +69,7 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
             # and the producer-fused activation checksum (this kernel + the window-lhs launch + the
             # producer epilogue's window sums)
             if L.producer is not None:
-                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED), it) + ws_cost.get(L.producer.index, 0.0)
+                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED), it) + ws_cost.get(id(L.producer), 0.0)
                 if t_fused < times[S.GLOBAL_ABFT]:
                     times[S.GLOBAL_ABFT], best_var = t_fused, "fused"
             net.set_global_variant(L, best_var)
@@ -79,7 +82,7 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
                 except Exception:      # noqa: BLE001
                     continue
                 t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT), it) + \
-                    (ws_cost.get(L.producer.index, 0.0) if L.gvar == "fused" else 0.0)
+                    (ws_cost.get(id(L.producer), 0.0) if L.gvar == "fused" else 0.0)
                 if t_fl < times[S.GLOBAL_ABFT]:
                     times[S.GLOBAL_ABFT], best_fl = t_fl, fl
             net.set_tile(L, gkey, 0, best_fl)

@@ -154,6 +154,19 @@ class LinearLayer:
 
 
 @dataclass
+class PoolProducer:
+    """A max-pooling glue op as the producer of a fused consumer's window sums (the pooled output
+    feeds a 1x1 or 3x3 / stride 1 / pad 1 conv directly)."""
+
+    name: str
+    out: Act
+    ws_mode: int = 0
+    ws_active: bool = False
+    index: int = -1
+    _wsum: object = None
+
+
+@dataclass
 class GlueOp:
     name: str
     fn: Callable[[], None]
@@ -180,6 +193,7 @@ class ProtectedNetwork:
         self.batch, self.h, self.w = batch, h, w
         self.ops: List[object] = []          # LinearLayer | GlueOp in execution order
         self.layers: List[LinearLayer] = []
+        self.pools: List[PoolProducer] = []   # max-pooling glue ops (window-sum producers)
         self.input = Act(t.zeros((batch, h, w, 8), dtype=self.sd, device="cuda"), 3)
         self.name = type(model).__name__.lower()
         model = model.eval()
@@ -191,14 +205,15 @@ class ProtectedNetwork:
         # layer [nl][cap][2] fp64, the counters [fired thread tiles, flagged layers] int32, then the
         # producers' window-sum buckets [9][cp] fp32
         self.cap = max(1, D.sm_count())
-        ws_floats = [9 * L.out.cp if L.ws_mode else 0 for L in self.layers]
+        prods = list(self.layers) + self.pools
+        ws_floats = [9 * P.out.cp if P.ws_mode else 0 for P in prods]
         base = 16 * self.cap * nl + 16
         self._block = t.zeros(base + 4 * sum(ws_floats), dtype=t.uint8, device="cuda")
         self.partials = self._block[:16 * self.cap * nl].view(t.float64).view(nl, self.cap, 2)
         self.counters = self._block[16 * self.cap * nl:16 * self.cap * nl + 8].view(t.int32)
         off = base
-        for L, nf in zip(self.layers, ws_floats):
-            L._wsum = self._block[off:off + 4 * nf].view(t.float32) if nf else None
+        for P, nf in zip(prods, ws_floats):
+            P._wsum = self._block[off:off + 4 * nf].view(t.float32) if nf else None
             off += 4 * nf
         self.sums = t.zeros((nl, 2), dtype=t.float64, device="cuda")
         self.verdict_buf = t.zeros(nl * _VERDICT_DTYPE.itemsize, dtype=t.uint8, device="cuda")
@@ -214,31 +229,33 @@ class ProtectedNetwork:
         dense NHWC buffer) and whose im2col column sums the producer's epilogue can accumulate:
         pointwise stride-1 layers (column sums) and 3x3 / stride 1 / pad 1 convs (window buckets)."""
         by_out = {id(L.out): L for L in self.layers}
+        by_out.update({id(P.out): P for P in self.pools})
         for L in self.layers:
             P = by_out.get(id(L.x))
             if P is None or P.out.phys is not None or P.out.cp != int(P.out.buf.shape[3]) or L.kind != "conv":
                 continue
             pointwise = (L.r, L.s, L.stride, L.pad) == (1, 1, 1, 0)
             window = (L.r, L.s, L.stride, L.pad) == (3, 3, 1, 1)
-            if not (pointwise or window) or P.out.cp > (512 if window else 4096):
+            # (smem buckets: the producer kernel's [9][N] / [N] fp32, the pool kernel's [9][C])
+            if not (pointwise or window) or P.out.cp > (512 if window else 2048):
                 continue
             L.producer = P
             P.ws_mode = max(P.ws_mode, 2 if window else 1)
-        for L in self.layers:
-            if L.ws_mode == 1 and L.out.cp > 4096:
-                L.ws_mode = 0
+
+    def producers(self):
+        return [P for P in list(self.layers) + self.pools if P.ws_mode]
 
     def fused_consumers(self, P: LinearLayer):
         return [L for L in self.layers if L.producer is P]
 
     def _refresh_window_sums(self) -> None:
         """Producers accumulate window sums exactly while a consumer runs the fused global lhs."""
-        for P in self.layers:
-            if not P.ws_mode:
-                continue
+        for P in self.producers():
             active = any(C.scheme is Scheme.GLOBAL_ABFT and C.gvar == "fused" for C in self.fused_consumers(P))
             if active != P.ws_active:
                 P.ws_active = active
+                if isinstance(P, PoolProducer):
+                    continue          # the pool's launch reads ws_active itself
                 for key in ARG_KEYS:
                     if key in P.args:
                         P.args[key] = self._make_args(P, key)
@@ -283,8 +300,18 @@ class ProtectedNetwork:
                 o -= 1
             return o
         out = Act(self.t.zeros((x.n, osz(x.h), osz(x.w), x.cp), dtype=self.sd, device="cuda"), x.c, x.phys)
-        self.add_glue("maxpool", lambda: kernels.maxpool_nhwc(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad,
-                                                              ceil_mode, self.dtype, out.buf, out.ld))
+        prod = PoolProducer("maxpool", out)
+        self.pools.append(prod)
+
+        def run():
+            if prod.ws_active:
+                kernels.maxpool_nhwc_ws(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad, ceil_mode, self.dtype, out.buf,
+                                        out.ld, prod._wsum, out.cp, prod.ws_mode)
+            else:
+                kernels.maxpool_nhwc(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad, ceil_mode, self.dtype, out.buf,
+                                     out.ld)
+        self.add_glue("maxpool", run)
+        prod.run = run
         return out
 
     def avgpool(self, x: Act) -> Act:
@@ -372,7 +399,9 @@ class ProtectedNetwork:
                   bias=L._bias_dev, residual=L._res, ld_res=L.residual.ld if L.residual is not None else 0,
                   tile_n=L.tile_n.get(key, 0), plan_flags=L.flags.get(key, 0) | (EXT_LHS if key == GLOBAL_FUSED else 0))
         if L.ws_active:
-            kw.update(wsum=L._wsum, ws_ld=L.out.cp, ws_mode=L.ws_mode, ws_P=L.out.h, ws_Q=L.out.w)
+            # the epilogue sums all rows only (bucket 0); a 3x3 consumer's border buckets come from
+            # abft_nhwc_border_sums over the border pixels (cheaper than per-chunk border reductions)
+            kw.update(wsum=L._wsum, ws_ld=L.out.cp, ws_mode=1, ws_P=L.out.h, ws_Q=L.out.w)
         if faults is not None:
             kw["faults"], kw["nfaults"] = faults
         if scheme is Scheme.GLOBAL_ABFT:
@@ -473,6 +502,12 @@ class ProtectedNetwork:
             kernels.conv2d(args)
         if key == GLOBAL_FUSED:
             P = L.producer
+            # (once per forward and producer: by its first 3x3 consumer running the fused lhs)
+            fc = [C for C in self.fused_consumers(P)
+                  if C.r == 3 and C.scheme is Scheme.GLOBAL_ABFT and C.gvar == "fused"]
+            if L.r == 3 and isinstance(P, LinearLayer) and (not fc or fc[0] is L):
+                x = L.x
+                kernels.border_sums(x.buf, x.n, x.h, x.w, x.cp, x.ld, self.dtype, P._wsum, P.out.cp)
             kernels.window_lhs(P._wsum, P.out.cp, L.x.cp, L.r, L.s, L._k // (L.r * L.s), L._rowck, L._bias_dev,
                                _r8(L.oc), L.m, self.partials[L.index, 0, 0:1])
 

@@ -196,12 +196,12 @@ def test_conv_full_width_tile_checksum_slice(P, case, scheme, faulted):
             [(v.thread_row, v.thread_col) for v in verdicts if v.detected]
 
 
-@pytest.mark.parametrize("flags", [0, 32])
-def test_gemm_full_width_global_tail_split_exact(P, flags):
-    """Global ABFT on a 256-wide tile with 16-bit outputs (the lean epilogue): the default single
-    272-column accumulator stage and the opt-in split tail (plan_flags bit 5: output columns
-    240..255 and the checksum slice in a shared TMEM tail) give the exact outputs and the exact
-    global lhs / rhs of the reference (checksum.py:108-127)."""
+@pytest.mark.parametrize("flags", [0, 512])
+def test_gemm_full_width_global_lean_exact(P, flags):
+    """Global ABFT on a 256-wide tile with 16-bit outputs (the lean epilogue, the 272-column
+    accumulator with its own checksum N-slice), with 128-byte-row and (plan_flags bit 9) 64-byte-row
+    bulk stores: the exact outputs and the exact global lhs / rhs of the reference
+    (checksum.py:108-127)."""
     import torch
     from paper_2104_09455_b200 import _lib, kernels
     from paper_2104_09455_b200 import device as D

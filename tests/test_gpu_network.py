@@ -232,7 +232,7 @@ def test_fused_window_checksums(PN, name):
     S = PN.Scheme
     net = PN.ProtectedNetwork(PN.build_model(name), 2, schemes=S.GLOBAL_ABFT)
     fused = [L for L in net.layers if L.producer is not None]
-    assert len(fused) >= (8 if name == "vgg16" else 20), [L.name for L in fused]
+    assert len(fused) >= (12 if name == "vgg16" else 20), [L.name for L in fused]
     for L in fused:
         net.set_global_variant(L, "fused")
     assert all(L.producer.ws_active for L in fused)
@@ -245,7 +245,7 @@ def test_fused_window_checksums(PN, name):
         check_layer(L)
         v = vs[L.index]
         assert not v.detected and abs(v.lhs - v.rhs) < 0.05 * v.tolerance_used, (L.name, v)
-    C = next(L for L in fused if L.k_ref <= 600)
+    C = next(L for L in fused if L.k_ref <= 600 and isinstance(L.producer, PN.LinearLayer))
     P = C.producer
     for target in (C, P):
         tau = vs[target.index].tolerance_used
@@ -253,6 +253,15 @@ def test_fused_window_checksums(PN, name):
         net.forward(x)
         got = [i for i, v in enumerate(net.verdicts()) if v.detected]
         assert got == [target.index], (target.name, got)
+    net.inject({})
+    # a consumer fed by a max-pooling glue op (its window sums come from the pool kernel)
+    pooled = [L for L in fused if isinstance(L.producer, PN.PoolProducer)]
+    assert pooled, "no pool-fed fused consumer"
+    Lp = pooled[0]
+    tau = vs[Lp.index].tolerance_used
+    net.inject({Lp.index: [(Lp.m // 3, 1, 8.0 * tau + 64.0)]})
+    net.forward(x)
+    assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [Lp.index]
     net.inject({})
     # switching the consumer away from the fused lhs stops the producer's window sums
     net.set_global_variant(C, "slice")
