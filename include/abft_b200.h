@@ -308,8 +308,9 @@ int abft_conv_colck(const void* X, int32_t n, int32_t h, int32_t w, int32_t c, i
 int abft_nhwc_maxpool(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t k,
                       int32_t stride, int32_t pad, int32_t ceil_mode, int32_t dtype, void* out, int64_t ldo,
                       void* stream);
-/* the same max pooling, also accumulating the window column sums of its output for the next
- * layer's fused global lhs (layout and ws_mode as abft_gemm_args_t.wsum; the caller zeroes wsum) */
+/* the same max pooling, also accumulating the column sums of its output (bucket 0 of the window
+ * sums, abft_gemm_args_t.wsum) for the next layer's fused global lhs; a 3x3 consumer's border
+ * buckets come from abft_nhwc_border_sums.  ws_mode: 1 or 2 (the consumer's), the caller zeroes wsum. */
 int abft_nhwc_maxpool_ws(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int64_t ldx, int32_t k,
                          int32_t stride, int32_t pad, int32_t ceil_mode, int32_t dtype, void* out, int64_t ldo,
                          float* wsum, int32_t ws_ld, int32_t ws_mode, void* stream);

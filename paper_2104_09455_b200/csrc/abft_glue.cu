@@ -81,34 +81,32 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const T* __restrict__
   }
 }
 
-// The same pooling, and the window column sums of its output for the next layer's fused global
-// lhs (buckets as in abft_gemm_args_t.wsum): a thread keeps one 8-channel vector and strides over
-// output pixels, summing the stored (rounded) maxima per bucket in registers; one smem reduction
-// and one global atomic per (bucket, channel) and CTA
+// The same pooling, and the column sums of its output (bucket 0 of the window sums; a 3x3
+// consumer's border buckets come from border_sums): a thread keeps one 8-channel vector and
+// strides over output pixels, summing the stored (rounded) maxima in registers; one smem
+// reduction and one global atomic per channel and CTA
 template <typename T>
 __global__ void __launch_bounds__(256) maxpool_ws_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
                                                          int P, int Q, int k, int s, int pad, T* __restrict__ out,
-                                                         long long ldo, long long npix, float* __restrict__ wsum,
-                                                         int ws_ld, int ws_mode) {
-  extern __shared__ float wsm[];          // [nb][C]
+                                                         long long ldo, int npix, float* __restrict__ wsum) {
+  extern __shared__ float wsm[];          // [C]
   const int cv = C / 8;
   const int lanes_p = blockDim.x / cv;    // pixels in flight per CTA
-  const int nb = ws_mode == 2 ? 9 : 1;
-  for (int i = threadIdx.x; i < nb * C; i += blockDim.x) wsm[i] = 0.f;
+  for (int i = threadIdx.x; i < C; i += blockDim.x) wsm[i] = 0.f;
   __syncthreads();
   const int c8 = threadIdx.x % cv, lp = threadIdx.x / cv;
-  float acc[9][8];
+  float acc[8];
 #pragma unroll
-  for (int b = 0; b < 9; ++b)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   if (lp < lanes_p) {
-    for (long long pix = (long long)blockIdx.x * lanes_p + lp; pix < npix; pix += (long long)gridDim.x * lanes_p) {
-      const int q = (int)(pix % Q);
-      const long long pq = pix / Q;
-      const int p = (int)(pq % P);
+    // two output pixels per iteration: twice the loads in flight (the loop is latency-bound)
+    const int step = gridDim.x * lanes_p;
+    auto pool = [&](int pix, uint4& m) {
+      const int q = pix % Q;
+      const int pq = pix / Q;
+      const int p = pq % P;
       const long long n = pq / P;
-      uint4 m = make_uint4(Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest);
+      m = make_uint4(Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest);
       const int h0 = p * s - pad, w0 = q * s - pad;
       for (int dh = 0; dh < k; ++dh) {
         const int hh = h0 + dh;
@@ -123,39 +121,37 @@ __global__ void __launch_bounds__(256) maxpool_ws_kernel(const T* __restrict__ x
           m.w = Max2<T>::op(m.w, u.w);
         }
       }
-      *reinterpret_cast<uint4*>(out + ((n * P + p) * Q + q) * ldo + c8 * 8) = m;
-      float v[8];
+      *reinterpret_cast<uint4*>(out + (long long)pix * ldo + c8 * 8) = m;
+    };
+    auto add = [&](const uint4& m) {
       const uint32_t w4[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = Unpack2<T>::f(w4[e]);
-        v[2 * e] = f.x;
-        v[2 * e + 1] = f.y;
+        acc[2 * e] += f.x;
+        acc[2 * e + 1] += f.y;
       }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[0][e] += v[e];
-      if (ws_mode == 2) {
-        const bool p0 = p == 0, pl = p == P - 1, q0 = q == 0, ql = q == Q - 1;
-        if (p0 | pl | q0 | ql) {
-          const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (in[b])
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc[b + 1][e] += v[e];
-        }
-      }
+    };
+    int pix = blockIdx.x * lanes_p + lp;
+    for (; pix + step < npix; pix += 2 * step) {
+      uint4 m0, m1;
+      pool(pix, m0);
+      pool(pix + step, m1);
+      add(m0);
+      add(m1);
+    }
+    if (pix < npix) {
+      uint4 m0;
+      pool(pix, m0);
+      add(m0);
     }
 #pragma unroll
-    for (int b = 0; b < 9; ++b)
-      if (b < nb)
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (acc[b][e] != 0.f) atomicAdd(&wsm[b * C + c8 * 8 + e], acc[b][e]);
+    for (int e = 0; e < 8; ++e)
+      if (acc[e] != 0.f) atomicAdd(&wsm[c8 * 8 + e], acc[e]);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nb * C; i += blockDim.x)
-    if (wsm[i] != 0.f) atomicAdd(&wsum[(long long)(i / C) * ws_ld + (i % C)], wsm[i]);
+  for (int i = threadIdx.x; i < C; i += blockDim.x)
+    if (wsm[i] != 0.f) atomicAdd(&wsum[i], wsm[i]);
 }
 
 // out[n][c] = mean over the H*W pixels of image n (fp32 sum, rounded once); CTA = (image, 256-vector slab)
@@ -286,18 +282,18 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_maxpool_ws(const
   const int cv = c / 8;
   const int threads = cv >= 256 ? cv : (256 / cv) * cv;
   if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "maxpool_ws: more than 256 channel vectors");
-  const size_t smem = (size_t)(ws_mode == 2 ? 9 : 1) * c * sizeof(float);
-  if (smem > 48 * 1024) return fail(ABFT_E_UNSUPPORTED, "maxpool_ws: 9 buckets x channels beyond 48 KB of smem");
+  const size_t smem = (size_t)c * sizeof(float);
+  (void)ws_ld;
   const long long npix = (long long)n * P * Q;
-  const int grid = std::max(1, std::min<int>(2 * num_sms(), (int)((npix + 63) / 64)));
+  if (npix >= (1LL << 30)) return fail(ABFT_E_UNSUPPORTED, "maxpool_ws: more than 2^30 output pixels");
+  const int grid = std::max(1, std::min<int>(8 * num_sms(), (int)((npix + 63) / 64)));
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
     maxpool_ws_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k, stride,
-                                                                   pad, (__nv_bfloat16*)out, ldo, npix, wsum, ws_ld,
-                                                                   ws_mode);
+                                                                   pad, (__nv_bfloat16*)out, ldo, (int)npix, wsum);
   else
     maxpool_ws_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, h, w, c, ldx, P, Q, k, stride, pad,
-                                                            (__half*)out, ldo, npix, wsum, ws_ld, ws_mode);
+                                                            (__half*)out, ldo, (int)npix, wsum);
   return cuda_check(cudaGetLastError(), "maxpool_ws launch");
 }
 
@@ -336,15 +332,14 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
 // 8-channel vector and a slice of the border, sums in registers, one smem reduction and one
 // atomic per (bucket, channel) per image.  Bucket 0 (all pixels) comes from the producer's epilogue.
 template <typename T>
-__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
-                                                          float* __restrict__ ws, int ws_ld) {
+__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, long long nimg, int H, int W, int C,
+                                                          long long ldx, float* __restrict__ ws, int ws_ld) {
   extern __shared__ float bsm[];           // [8][C]
   const int cv = C / 8;
   const int parts = blockDim.x / cv;
   for (int i = threadIdx.x; i < 8 * C; i += blockDim.x) bsm[i] = 0.f;
   __syncthreads();
   const int c8 = threadIdx.x % cv, part = threadIdx.x / cv;
-  const long long img = blockIdx.x;
   // border pixel list: rows 0 and H-1 (all W columns), then columns 0 and W-1 of rows 1..H-2
   const int nrow = (H > 1 ? 2 : 1) * W;
   const int ncol = H > 2 ? (W > 1 ? 2 : 1) * (H - 2) : 0;
@@ -353,7 +348,8 @@ __global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ 
   for (int b = 0; b < 8; ++b)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
-  if (part < parts) {
+  // images strided over the CTAs (registers accumulate across images: one flush per CTA)
+  if (part < parts) for (long long img = blockIdx.x; img < nimg; img += gridDim.x) {
     for (int i = part; i < nrow + ncol; i += parts) {
       int hh, ww;
       if (i < nrow) {
@@ -381,6 +377,8 @@ __global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ 
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[b][e] += v[e];
     }
+  }
+  if (part < parts) {
 #pragma unroll
     for (int b = 0; b < 8; ++b)
 #pragma unroll
@@ -402,11 +400,12 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(cons
   const int threads = cv >= 256 ? cv : (256 / cv) * cv;
   if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "border_sums: more than 256 channel vectors");
   const size_t smem = (size_t)8 * c * sizeof(float);
+  const int grid = std::min(n, num_sms());
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
-    border_sums_kernel<__nv_bfloat16><<<n, threads, smem, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, wsum, ws_ld);
+    border_sums_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, n, h, w, c, ldx, wsum, ws_ld);
   else
-    border_sums_kernel<__half><<<n, threads, smem, st>>>((const __half*)x, h, w, c, ldx, wsum, ws_ld);
+    border_sums_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, n, h, w, c, ldx, wsum, ws_ld);
   return cuda_check(cudaGetLastError(), "border_sums launch");
 }
 

@@ -505,7 +505,7 @@ class ProtectedNetwork:
             # (once per forward and producer: by its first 3x3 consumer running the fused lhs)
             fc = [C for C in self.fused_consumers(P)
                   if C.r == 3 and C.scheme is Scheme.GLOBAL_ABFT and C.gvar == "fused"]
-            if L.r == 3 and isinstance(P, LinearLayer) and (not fc or fc[0] is L):
+            if L.r == 3 and (not fc or fc[0] is L):
                 x = L.x
                 kernels.border_sums(x.buf, x.n, x.h, x.w, x.cp, x.ld, self.dtype, P._wsum, P.out.cp)
             kernels.window_lhs(P._wsum, P.out.cp, L.x.cp, L.r, L.s, L._k // (L.r * L.s), L._rowck, L._bias_dev,

@@ -4,7 +4,7 @@ times each — an ncu target.  Also prints each layer's CUDA-graph time per sche
   python tools/ncu_netlayer.py NET BATCH SCHEME LAYER[,LAYER...] [reps] [plan_flags]
 
 LAYER is a layer name (e.g. features.2, conv1, layer1.0.conv3).  SCHEME: unprotected |
-global-abft | thread-one-sided | global-dot.
+global-abft | thread-one-sided | global-dot | global-fused.
 """
 import os
 import sys
@@ -25,7 +25,7 @@ x = (torch.rand((batch, 3, hw, hw), device="cuda") * 2 - 1).half()
 net.load_input(x)
 net.forward()
 torch.cuda.synchronize()
-sch = PN.GLOBAL_DOT if scheme == "global-dot" else PN.Scheme(scheme)
+sch = {"global-dot": PN.GLOBAL_DOT, "global-fused": PN.GLOBAL_FUSED}.get(scheme) or PN.Scheme(scheme)
 layers = {L.name: L for L in net.layers}
 if flags:
     for n in names:
@@ -33,7 +33,7 @@ if flags:
 for n in names:
     L = layers[n]
     us = profiler.graph_time_us(lambda: net.launch(L, sch), 10)
-    print(f"{n}: M={L.m} N={L.oc} K={L.k_ref} {scheme} {us:.1f} us  plan={net.plan_of(L, PN.Scheme.GLOBAL_ABFT if sch == PN.GLOBAL_DOT else sch)}",
+    print(f"{n}: M={L.m} N={L.oc} K={L.k_ref} {scheme} {us:.1f} us  plan={net.plan_of(L, PN.Scheme.GLOBAL_ABFT if isinstance(sch, str) else sch)}",
           flush=True)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
