@@ -404,7 +404,7 @@ def main():
                                             "ig": round(100 * (min(t1[S.GLOBAL_ABFT], t1[S.THREAD_ONE_SIDED])
                                                                / t1[S.UNPROTECTED] - 1), 2)}}
         from tools import dlrm_secondary
-        secondary["c2"] = dlrm_secondary.run(dev, steps=max(5, args.steps // 2), warmup=3)
+        secondary["c2"] = dlrm_secondary.run(dev, steps=max(30, args.steps), warmup=5)
     per_cfg = {}
     if "c1" in secondary:
         per_cfg["C1"] = secondary["c1"]["overhead_pct"]["ig"]

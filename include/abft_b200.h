@@ -161,6 +161,19 @@ typedef struct {
 
 int abft_gemm(const abft_gemm_args_t* args, void* stream);
 
+/* Grouped launch: many independent protected GEMMs (same dtype, scheme, thread tile, output type,
+ * ReLU and tile_n — one kernel configuration) as ONE persistent launch over all their tiles, e.g.
+ * one layer depth of a group of DLRM chains (the ~5 us launch latency, not the math, bounds such
+ * small GEMMs).  Per problem: A / B (or augmented weights) / C, M, N, K, out_partials (global) —
+ * no faults, bias, residual or fused verification.  prepare() writes the problem table (tensor
+ * maps, extents, outputs; count * abft_group_problem_bytes(), 64-byte aligned device memory) once,
+ * synchronously; launch() is stream-ordered and graph-capturable.  Outputs, (lhs, rhs) slots and
+ * fired-tile counts equal those of launching each problem alone (the slots are added atomically
+ * per problem and CTA: the caller zeroes them, as for abft_verify_partials). */
+int abft_gemm_group_prepare(const abft_gemm_args_t* args, int32_t count, void* table, int64_t table_bytes);
+int abft_gemm_group_launch(const abft_gemm_args_t* args, int32_t count, const void* table, void* stream);
+int abft_group_problem_bytes(void);
+
 /* The global lhs of a layer whose activation checksum came from the producer's window sums
  * (abft_gemm_args_t.wsum): lhs += sum_{r,s,c<C} colck_im2col(r,s,c) * rowck[(r*S + s)*ck + c]
  * + M * sum_{j<n_out} bias[j] (bias optional), where colck_im2col is the im2col column sum of the

@@ -47,6 +47,9 @@ EXPORTED_SYMBOLS = (
     "abft_version",
     "abft_device_sms",
     "abft_window_lhs",
+    "abft_gemm_group_prepare",
+    "abft_gemm_group_launch",
+    "abft_group_problem_bytes",
     "abft_nhwc_border_sums",
     "abft_nhwc_maxpool",
     "abft_nhwc_maxpool_ws",

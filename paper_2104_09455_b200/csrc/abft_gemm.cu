@@ -29,9 +29,11 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "abft_common.cuh"
 #include "sm100_ptx.cuh"
@@ -48,6 +50,18 @@ constexpr int DCK_BUFS = 4;        // column-sum MMA results in flight (8 TMEM c
 
 enum { CLASS_PLAIN = 0, CLASS_CHECKSUM = 1, CLASS_REPLICA = 2 };
 
+
+// Grouped launch (abft_gemm_group_*): one persistent grid over the tiles of many independent
+// GEMMs of the same kernel configuration (e.g. one layer depth of the DLRM chains).  The tiles
+// are numbered problem by problem; each role walks its CTA's tiles with a problem cursor.
+struct __align__(64) GroupProblem {
+  CUtensorMap ma, mb, mc, mc2;       // A, B (or augmented weights), C (32-column box), C (64-column box)
+  int M, N, nkb, num_n_blocks, num_tiles, tile_begin, n_trows, n_tcols;
+  void* C;
+  long long ldc;
+  double* partials;                  // global scheme: [grid][2] (lhs, rhs) slots of this problem
+  int pad[2];
+};
 
 struct GemmParams {
   int M, N, K, m_ext, n_ext, tol_k;
@@ -140,6 +154,8 @@ struct GemmParams {
   float* wsum;
   int ws_ld, ws_mode, ws_P, ws_Q, ws_nb;
   uint32_t off_ws;
+  const GroupProblem* group;         // grouped launch: the problem table (device memory), else null
+  int group_n;
 };
 
 template <typename T>
@@ -571,11 +587,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // programmatic dependent launch: let the next kernel on the stream start its prologue now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0 && lane == 0) {
-    if (!gather) ptx::tma_prefetch(&tmA);
-    ptx::tma_prefetch(&tmB);
-    if (ck_loaded) ptx::tma_prefetch(&tmCK);
-    if (p.tma_store) ptx::tma_prefetch(&tmC);
-    if (p.out_wide) ptx::tma_prefetch(&tmC2);
+    if (p.group == nullptr) {
+      if (!gather) ptx::tma_prefetch(&tmA);
+      ptx::tma_prefetch(&tmB);
+      if (ck_loaded) ptx::tma_prefetch(&tmCK);
+      if (p.tma_store) ptx::tma_prefetch(&tmC);
+      if (p.out_wide) ptx::tma_prefetch(&tmC2);
+    }
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
@@ -648,8 +666,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      if (p.group != nullptr) {
+        // grouped launch: plain GEMM A tiles, one k-block per stage, per-problem maps and K
+        const GroupProblem* pr = p.group;
+        int pend = pr->tile_begin + pr->num_tiles;
+        for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x) {
+          while (tile >= pend) { ++pr; pend = pr->tile_begin + pr->num_tiles; }
+          const int local = tile - pr->tile_begin;
+          const int nnb = pr->num_n_blocks;
+          const int nb = local % nnb;
+          const int m0 = (local / nnb) * L_bm_eff;
+          const int brow = ck_aug ? nb * L_b_rows_blk : nb * L_bn_eff;
+          const int nkb = pr->nkb;
+#pragma unroll 1
+          for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            ptx::mbar_arrive_expect_tx_w(&full[s], L_stage_a_bytes + L_tx_b);
+            ptx::tma_load_2d_w(sm_a + s * L_stage_a_bytes, &pr->ma, &full[s], kb * BK, m0);
+            ptx::tma_load_2d_w(sm_b + s * L_stage_b_bytes, &pr->mb, &full[s], kb * BK, brow);
+            if (++s == L_stages) { s = 0; ph ^= 1; }
+          }
+        }
+      }
       // gathered stems: the checksum warps fill the A stages; B is resident (loaded above)
-      for (int tile = gather ? L_num_tiles : (int)blockIdx.x; tile < L_num_tiles; tile += gridDim.x) {
+      for (int tile = (gather || p.group != nullptr) ? L_num_tiles : (int)blockIdx.x; tile < L_num_tiles;
+           tile += gridDim.x) {
         const int nb = tile % L_num_n_blocks;
         const int m0 = (tile / L_num_n_blocks) * L_bm_eff;
         const int n0 = nb * L_bn_eff;
@@ -803,8 +844,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t dph = 0;
       int t_local = 0;
       if (b_res && blockIdx.x < L_num_tiles) ptx::mbar_wait(bres, 0);
+      const GroupProblem* gpr = p.group;       // grouped launch: the tile's problem (its K)
+      int gpend = gpr != nullptr ? gpr->tile_begin + gpr->num_tiles : 0;
       for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x, ++t_local) {
         const bool count_tile = (tile % L_num_n_blocks) == 0;
+        int nkb_t = L_nkb;
+        if (gpr != nullptr) {
+          while (tile >= gpend) { ++gpr; gpend = gpr->tile_begin + gpr->num_tiles; }
+          nkb_t = gpr->nkb;
+        }
         const int acc = t_local % L_acc_stages;
         const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -835,7 +883,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (fast) {
           // lean loop: stage descriptors advance by constant steps (no per-MMA layout selects)
 #pragma unroll 1
-          for (int kb = 0; kb < L_nkb; ++kb) {
+          for (int kb = 0; kb < nkb_t; ++kb) {
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
@@ -1340,10 +1388,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Lean-path store of one 32-column sub-chunk: wide units (two sub-chunks staged as 128-byte
     // rows, one bulk tensor store), 32-column bulk stores (64-byte rows), or direct row stores
     // (16-column tails, partial halo quadrants)
+    // (mc / mc2 / Cp / ldc / N: the output of the tile's problem — the launch's, or a grouped one's)
     auto store_chunk = [&](const float (&v)[32], int c0, int cmax, int gc0, int m0, int gm, bool row_ok, bool relu,
-                           bool tma, bool& unit_wide) {
-      const long long ldc = p.ldc;
-      const int N = p.N;
+                           bool tma, bool& unit_wide, const CUtensorMap* mc, const CUtensorMap* mc2, void* Cp,
+                           long long ldc, int N) {
       const bool single = p.out_single != 0;
       const int sub = (c0 >> 5) & 1;
       if (wide && sub == 0) unit_wide = tma && cmax >= 64;
@@ -1376,7 +1424,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&tmC2, my_stage + sbuf * 4096, gc0 - 32, m0 + q * 32);
+            ptx::tma_store_2d(mc2, my_stage + sbuf * 4096, gc0 - 32, m0 + q * 32);
             ptx::bulk_commit();
           }
           sbuf ^= single ? 0 : 1;
@@ -1407,14 +1455,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_2d(&tmC, my_stage + sbuf * (wide ? 4096 : 2048), gc0, m0 + q * 32);
+          ptx::tma_store_2d(mc, my_stage + sbuf * (wide ? 4096 : 2048), gc0, m0 + q * 32);
           ptx::bulk_commit();
         }
         sbuf ^= single ? 0 : 1;
       } else {
         // direct stores: a tile's 16-column tail, or tiles without bulk-tensor stores (halo
         // conv tiles of Qt < 128 pixels)
-        if (row_ok) lean_store_row<T>(v, p.C, gm, ldc, gc0, cmax, N, relu);
+        if (row_ok) lean_store_row<T>(v, Cp, gm, ldc, gc0, cmax, N, relu);
       }
     };
     int t_local = 0;
@@ -1426,11 +1474,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       lean = (p.out_dtype == ABFT_OUT_F16 || p.out_dtype == ABFT_OUT_BF16) && p.next_colck == nullptr &&
              p.nfaults == 0 && split;
     }
+    // grouped launch: the tile's problem (cursor), and its (lhs, rhs) flushed into its own slot of
+    // this CTA whenever the warp moves on to another problem
+    const GroupProblem* gpr = p.group;
+    int gpend = gpr != nullptr ? gpr->tile_begin + gpr->num_tiles : 0;
+    auto group_flush = [&](const GroupProblem* pr) {
+      double x = rhs_acc, y = lhs_acc;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+      }
+      if (lane == 0 && pr->partials != nullptr) {
+        if (y != 0.0) atomicAdd(&pr->partials[2 * blockIdx.x], y);
+        if (x != 0.0) atomicAdd(&pr->partials[2 * blockIdx.x + 1], x);
+      }
+      rhs_acc = 0.0;
+      lhs_acc = 0.0;
+    };
     if (lean) {
-      const bool want_sum = p.out_sum != nullptr || p.out_partials != nullptr;
+      const bool want_sum = p.out_sum != nullptr || p.out_partials != nullptr || p.group != nullptr;
       const bool relu = p.relu != 0;
-      const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
-      const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M;
+      const int bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
+      const int cols_per_acc = p.cols_per_acc;
+      int nnb = p.num_n_blocks, N = p.N, M = p.M;
+      const CUtensorMap* mc = &tmC;
+      const CUtensorMap* mc2 = &tmC2;
+      void* Cp = p.C;
+      long long ldc = p.ldc;
       const bool tma = p.tma_store != 0 && q_full;
       const float* __restrict__ bias = p.bias;
       const bool bias_lhs = bias != nullptr && p.lhs_epi;
@@ -1440,9 +1511,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (epi_tiles && (t_local & 1) != h) continue;
         const int acc = t_local % acc_stages;
         const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
-        const int mb = tile / nnb;
+        int lt = tile;
+        if (gpr != nullptr) {
+          if (tile >= gpend) {
+            group_flush(gpr);
+            while (tile >= gpend) { ++gpr; gpend = gpr->tile_begin + gpr->num_tiles; }
+          }
+          nnb = gpr->num_n_blocks; N = gpr->N; M = gpr->M;
+          mc = &gpr->mc; mc2 = &gpr->mc2; Cp = gpr->C; ldc = gpr->ldc;
+          lt = tile - gpr->tile_begin;
+        }
+        const int mb = lt / nnb;
         const int m0 = mb * bm_eff;
-        const int n0 = (tile - mb * nnb) * bn_eff;
+        const int n0 = (lt - mb * nnb) * bn_eff;
         const int gm = m0 + row;
         const bool row_in_tile = row < bm_eff;
         const bool row_valid = row_in_tile && gm < M;
@@ -1494,13 +1575,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
             wsum_chunk(p, ws_s, vr, gm, row_valid, gc0, min(cmax, N - gc0), lane);
           }
-          store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide);
+          store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide, mc, mc2, Cp, ldc, N);
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         if (row_valid) rhs_acc += (double)tsum;
       }
+      if (gpr != nullptr) group_flush(gpr);
     }
     // Lean one-sided path (static group width, flags-only verdicts, 16-bit bulk-tensor stores,
     // no faults / fused colck / bring-up bits): the generic loop's checks, without its dispatch.
@@ -1515,8 +1597,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool exact_mode = p.r == 0.0;
         const float rk = p.rk;
         const bool ck_split = p.split != 0;
-        const int nnb = p.num_n_blocks, bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
-        const int cols_per_acc = p.cols_per_acc, N = p.N, M = p.M, mt = p.mt, groups = p.groups;
+        const int bm_eff = p.bm_eff, bn_eff = p.bn_eff, acc_stages = p.acc_stages;
+        const int cols_per_acc = p.cols_per_acc, mt = p.mt, groups = p.groups;
+        int nnb = p.num_n_blocks, N = p.N, M = p.M, n_trows = p.n_trows, n_tcols = p.n_tcols;
+        const CUtensorMap* mc = &tmC;
+        const CUtensorMap* mc2 = &tmC2;
+        void* Cp = p.C;
+        long long ldc = p.ldc;
         const bool tma = p.tma_store != 0 && q_full;
         const float* __restrict__ bias = p.bias;
         const void* resid = p.residual;
@@ -1525,13 +1612,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (epi_tiles && (t_local & 1) != h) continue;
           const int acc = t_local % acc_stages;
           const uint32_t aph = (uint32_t)(t_local / acc_stages) & 1u;
-          const int mb = tile / nnb;
+          int lt = tile;
+          if (gpr != nullptr) {
+            while (tile >= gpend) { ++gpr; gpend = gpr->tile_begin + gpr->num_tiles; }
+            nnb = gpr->num_n_blocks; N = gpr->N; M = gpr->M; n_trows = gpr->n_trows; n_tcols = gpr->n_tcols;
+            mc = &gpr->mc; mc2 = &gpr->mc2; Cp = gpr->C; ldc = gpr->ldc;
+            lt = tile - gpr->tile_begin;
+          }
+          const int mb = lt / nnb;
           const int m0 = mb * bm_eff;
-          const int n0 = (tile - mb * nnb) * bn_eff;
+          const int n0 = (lt - mb * nnb) * bn_eff;
           const int gm = m0 + row;
           const bool row_in_tile = row < bm_eff;
           const int t_row = gm / mt;
-          const bool row_verdict = row_in_tile && t_row < p.n_trows;
+          const bool row_verdict = row_in_tile && t_row < n_trows;
           uint4 rb[4];
           bool have_rb = resid != nullptr && row_in_tile && gm < M && c_first < bn_eff &&
                          residual_prefetch<T>(rb, resid, ld_res, gm, n0 + c_first,
@@ -1577,7 +1671,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
               wsum_chunk(p, ws_s, vr, gm, row_in_tile && gm < M, gc0, min(cmax, N - gc0), lane);
             }
-            store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide);
+            store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide, mc, mc2, Cp, ldc, N);
           }
           // fired groups of the thread tile's Mt rows -> verdicts (rare)
           uint32_t m = row_verdict ? fmask : 0u;
@@ -1587,7 +1681,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             while (m != 0u) {
               const int gbit = __ffs(m) - 1;
               m &= m - 1u;
-              if (t_col0 + gbit < p.n_tcols) emit_verdict(p, t_row, t_col0 + gbit, true, 0.0, 0.0);
+              if (t_col0 + gbit < n_tcols) emit_verdict(p, t_row, t_col0 + gbit, true, 0.0, 0.0);
             }
           }
           ptx::tc_fence_before();
@@ -1949,8 +2043,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
-  if ((p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) && warp == EPI_WARP0) {
+  if (p.group == nullptr && (p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) && warp == EPI_WARP0) {
     // one add per CTA of its (rhs, lhs) partials, by the thread that then counts the CTA done
+    // (grouped launches flushed theirs per problem)
     double tx = lane < 8 ? red_d[lane] : 0.0, ty = lane < 8 ? red_d[8 + lane] : 0.0;
     // the checksum warps' CUDA-core lhs (lhs_rowck) joins the per-CTA slot
     if (p.out_partials != nullptr && p.lhs_w != nullptr && lane >= 8 && lane < 12) ty = red_d[16 + lane - 8];
@@ -2837,6 +2932,121 @@ extern "C" __attribute__((visibility("default"))) int abft_gemm(const abft_gemm_
   rc = cached_map(&ma, a->A, a->dtype, a->K, a->M, a->lda, BM);
   if (rc != ABFT_OK) return rc;
   return launch_with_a(a, pl, ma, stream);
+}
+
+// ---------------------------------------------------------------- grouped launch
+namespace abft {
+namespace {
+// The common kernel configuration of a group (every problem must plan to it) and each problem's
+// tile count under it.  plan_flags bits 0 and 2 are forced: no k-block pairs and two output
+// staging buffers, whose choice would otherwise depend on each problem's K.
+int group_plans(const abft_gemm_args_t* args, int count, Plan& common, std::vector<Plan>& plans) {
+  if (args == nullptr || count < 1) return fail(ABFT_E_VALUE, "group: at least one problem");
+  plans.resize(count);
+  for (int i = 0; i < count; ++i) {
+    abft_gemm_args_t a = args[i];
+    a.plan_flags |= 1 | 4;
+    if (a.lda < a.K || (a.lda % 8)) return fail(ABFT_E_SHAPE, "group: lda must be >= K and a multiple of 8");
+    int rc = validate_common(&a);
+    if (rc != ABFT_OK) return rc;
+    if (a.faults != nullptr && a.nfaults > 0) return fail(ABFT_E_UNSUPPORTED, "group: no injected faults (launch singly)");
+    if (a.bias || a.residual || a.next_colck || a.wsum || a.a_colck || a.lhs_rowck || a.verdicts || a.vn || a.out_sum ||
+        a.out_lhs)
+      return fail(ABFT_E_UNSUPPORTED, "group: plain GEMM layers (partials / fired counts only)");
+    rc = make_plan(&a, plans[i]);
+    if (rc != ABFT_OK) return rc;
+    const GemmParams& p = plans[i].p;
+    const GemmParams& q = plans[0].p;
+    if (i > 0 && (plans[i].cls != plans[0].cls || plans[i].ntc != plans[0].ntc || p.bn != q.bn || p.bn_eff != q.bn_eff ||
+                  p.stages != q.stages || p.acc_stages != q.acc_stages || p.cols_per_acc != q.cols_per_acc ||
+                  p.ck_mode != q.ck_mode || p.b_rows_blk != q.b_rows_blk || p.scheme != q.scheme ||
+                  p.out_dtype != q.out_dtype || p.relu != q.relu || p.tma_store != q.tma_store ||
+                  p.out_wide != q.out_wide || p.epi_tiles != q.epi_tiles || p.out_single != q.out_single ||
+                  p.mt != q.mt || p.nt != q.nt || plans[i].smem != plans[0].smem))
+      return fail(ABFT_E_UNSUPPORTED, "group: problem " + std::to_string(i) + " plans a different kernel configuration");
+    if (!p.tma_store || p.kpair || p.ck_mode == 1 || p.ck_mode == 2 || p.ck_mode == 4 || p.acolck_mode)
+      return fail(ABFT_E_UNSUPPORTED, "group: needs bulk-tensor stores and no separate checksum boxes");
+  }
+  common = plans[0];
+  return ABFT_OK;
+}
+}  // namespace
+}  // namespace abft
+
+extern "C" __attribute__((visibility("default"))) int abft_gemm_group_prepare(const abft_gemm_args_t* args,
+                                                                             int32_t count, void* table,
+                                                                             int64_t table_bytes) {
+  using namespace abft;
+  Plan common;
+  std::vector<Plan> plans;
+  int rc = group_plans(args, count, common, plans);
+  if (rc != ABFT_OK) return rc;
+  if (table == nullptr || table_bytes < (int64_t)sizeof(GroupProblem) * count || (reinterpret_cast<uintptr_t>(table) & 63))
+    return fail(ABFT_E_VALUE, "group: table must be 64-byte aligned with count * abft_group_problem_bytes()");
+  std::vector<GroupProblem> host(count);
+  int tiles = 0;
+  for (int i = 0; i < count; ++i) {
+    const abft_gemm_args_t& a = args[i];
+    const GemmParams& p = plans[i].p;
+    GroupProblem& g = host[i];
+    memset(&g, 0, sizeof(g));
+    rc = cached_map(&g.ma, a.A, a.dtype, a.K, a.M, a.lda, BM);
+    if (rc == ABFT_OK) {
+      if (p.ck_mode == 3) {
+        if (a.ck_rows == nullptr || a.ck_rows_n != p.num_n_blocks * p.b_rows_blk)
+          return fail(ABFT_E_SHAPE, "group: augmented weights do not match the common plan");
+        rc = cached_map(&g.mb, a.ck_rows, a.dtype, a.K, a.ck_rows_n, a.ldck, p.b_rows_blk);
+      } else {
+        rc = cached_map(&g.mb, a.Bt, a.dtype, a.K, a.N, a.ldbt, p.bn);
+      }
+    }
+    if (rc == ABFT_OK) rc = make_out_map(&g.mc, &a);
+    if (rc == ABFT_OK && p.out_wide) rc = make_out_map(&g.mc2, &a, 32, 64);
+    if (rc != ABFT_OK) return rc;
+    g.M = a.M; g.N = a.N; g.nkb = p.nkb; g.num_n_blocks = p.num_n_blocks; g.num_tiles = p.num_tiles;
+    g.tile_begin = tiles; g.n_trows = p.n_trows; g.n_tcols = p.n_tcols;
+    g.C = a.C; g.ldc = a.ldc;
+    g.partials = (a.scheme == ABFT_GLOBAL) ? a.out_partials : nullptr;
+    if (a.scheme == ABFT_GLOBAL && (a.out_partials == nullptr || a.partials_cap < std::min(p.num_tiles, num_sms())))
+      return fail(ABFT_E_VALUE, "group: the global scheme needs out_partials with a slot per CTA");
+    tiles += p.num_tiles;
+  }
+  return cuda_check(cudaMemcpy(table, host.data(), sizeof(GroupProblem) * count, cudaMemcpyHostToDevice),
+                    "group table upload");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_gemm_group_launch(const abft_gemm_args_t* args,
+                                                                            int32_t count, const void* table,
+                                                                            void* stream) {
+  using namespace abft;
+  Plan common;
+  std::vector<Plan> plans;
+  int rc = group_plans(args, count, common, plans);
+  if (rc != ABFT_OK) return rc;
+  if (table == nullptr) return fail(ABFT_E_VALUE, "group: null table (abft_gemm_group_prepare)");
+  int tiles = 0;
+  for (const Plan& pl : plans) tiles += pl.p.num_tiles;
+  GemmParams& p = common.p;
+  p.group = reinterpret_cast<const GroupProblem*>(table);
+  p.group_n = count;
+  p.num_tiles = tiles;
+  p.out_partials = nullptr;      // per problem, in the table
+  p.out_sum = nullptr;
+  p.out_lhs = nullptr;
+  p.pdl = args[0].pdl;
+  const int sms = args[0].num_sms > 0 ? args[0].num_sms : num_sms();
+  common.grid = std::min(tiles, sms);
+  // the kernel reads every map from the table; these arguments are placeholders
+  CUtensorMap dummy{};
+  const CUtensorMap& d = dummy;
+  cudaStream_t st = as_stream(stream);
+  if (args[0].dtype == ABFT_BF16)
+    return launch_typed<__nv_bfloat16>(common.cls, common.ntc, d, d, d, d, d, p, common.smem, common.grid, st);
+  return launch_typed<__half>(common.cls, common.ntc, d, d, d, d, d, p, common.smem, common.grid, st);
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_group_problem_bytes() {
+  return (int)sizeof(abft::GroupProblem);
 }
 
 // conv -> GEMM view: M = n*P*Q output pixels, K = r*s*c in (r, s, c) order, A = the NHWC input

@@ -294,3 +294,21 @@ def window_lhs(wsum, ws_ld: int, c: int, r: int, s: int, ck: int, rowck, bias, n
     _lib.call("abft_window_lhs", ptr(wsum), int(ws_ld), int(c), int(r), int(s), int(ck), ptr(rowck),
               ptr(bias) if bias is not None else None, int(n_out), ctypes.c_int64(int(m)), ptr(lhs), stream_handle())
 
+
+def group_problem_bytes() -> int:
+    return int(_lib.load().abft_group_problem_bytes())
+
+
+def gemm_group_prepare(args_list, table) -> None:
+    """abft_gemm_group_prepare: write the problem table of a grouped launch (synchronous)."""
+    arr = (_lib.GemmArgs * len(args_list))(*args_list)
+    _lib.check(_lib.load().abft_gemm_group_prepare(arr, len(args_list), ctypes.c_void_p(table.data_ptr()),
+                                                   ctypes.c_int64(table.numel() * table.element_size())))
+
+
+def gemm_group_launch(args_arr, count: int, table) -> None:
+    """abft_gemm_group_launch over a prepared table (stream-ordered, graph-capturable); args_arr is the
+    ctypes array built once by the caller."""
+    _lib.check(_lib.load().abft_gemm_group_launch(args_arr, count, ctypes.c_void_p(table.data_ptr()),
+                                                  stream_handle()))
+

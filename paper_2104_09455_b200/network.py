@@ -60,6 +60,8 @@ class ProtectedChain:
     ck_split: bool = False
     faults: Optional[dict] = None        # {layer: [(row, col, delta)]}: deltas added to the fp32 accumulator
     pdl: bool = True                     # programmatic dependent launch between consecutive layers
+    tile_ns: Optional[Sequence[int]] = None   # per-layer CTA tile (0: the planner's), e.g. a grouped launch's
+    plan_flags: int = 0                  # abft_gemm_args_t.plan_flags for every layer
     # (sums [nl, 2] fp64, counters int32 [2], vdone int32 [1][, partials [nl, cap, 2] fp64]) views of
     # a ChainGroup's block: the group clears them and verifies every member's global layers in one
     # launch; with partials, each CTA of a global layer writes its (lhs, rhs) to its own slot
@@ -122,7 +124,8 @@ class ProtectedChain:
         t = self.tiling
         m = self.batch
         kw = dict(out=self.acts[i], ldc=self.acts[i].stride(0),
-                  out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu)
+                  out_kind="bf16" if self.acts[i].dtype == D.torch().bfloat16 else "f16", relu=L.relu,
+                  tile_n=self.tile_ns[i] if self.tile_ns else 0, plan_flags=self.plan_flags)
         if i in self._fault_dev:
             kw["faults"], kw["nfaults"] = self._fault_dev[i]
         if L.scheme is Scheme.GLOBAL_ABFT:
@@ -211,10 +214,24 @@ class ChainGroup:
     every member — the reference's deferred verification (checksum.py:207-211) batched across
     the group, instead of a done-count round trip at the end of each member's last kernel."""
 
-    def __init__(self, specs, **chain_kw):
-        """specs: [(weights, batch, schemes)]; chain_kw: ProtectedChain fields shared by all."""
+    def __init__(self, specs, grouped: bool = False, **chain_kw):
+        """specs: [(weights, batch, schemes)]; chain_kw: ProtectedChain fields shared by all.
+        grouped: run each layer depth of all members as grouped launches (abft_gemm_group_*: one
+        persistent launch per (depth, scheme) over every member's tiles) instead of one launch per
+        layer and member; members must have equally many layers and no injected faults."""
         t = D.torch()
         nls = [len(w) for w, _, _ in specs]
+        self.grouped = bool(grouped)
+        if self.grouped:
+            if len(set(nls)) != 1 or chain_kw.get("faults"):
+                raise ValueError("grouped ChainGroup: members with equally many layers and no faults")
+            # one CTA tile per depth (the group's common kernel configuration); k-block pairs off and
+            # double output staging, which would otherwise depend on each member's K
+            tiles = []
+            for d in range(nls[0]):
+                nmax = max(D.round8(D.shape2d(w[d], "w")[1]) for w, _, _ in specs)
+                tiles.append(64 if nmax <= 64 else 128)
+            chain_kw = dict(chain_kw, tile_ns=tiles, plan_flags=1 | 4)
         total = sum(nls)
         off_cnt = 16 * total
         off_flag = off_cnt + 16 * len(specs)
@@ -240,6 +257,31 @@ class ChainGroup:
         self.flagged = self.block[off_flag:off_flag + 4].view(t.int32)
         self.tail = self.block[off_cnt:off_part]    # counters + flag count: one D2H read
         self.numeric = self.chains[0].numeric
+        self._groups = []
+        if self.grouped:
+            self._build_groups()
+
+    def _build_groups(self) -> None:
+        """Per layer depth and scheme: the members' launch arguments and a prepared problem table."""
+        t = D.torch()
+        pb = kernels.group_problem_bytes()
+        for d in range(len(self.chains[0].layers)):
+            by_scheme = {}
+            for ch in self.chains:
+                L = ch.layers[d]
+                a = ch.x if d == 0 else ch.acts[d - 1]
+                kw = ch._gemm_kwargs(d, L)
+                kw["pdl"] = d > 0 and ch.pdl and not _NO_PDL
+                args = kernels._gemm_args(a, a.stride(0), L.pw.bt, L.pw.ldbt, ch.batch, L.n, L.k, ch.dtype, ch.numeric,
+                                          L.scheme, ck_rows=L.ck_rows, **kw)
+                by_scheme.setdefault(L.scheme, []).append(args)
+            for sch, lst in by_scheme.items():
+                raw = t.empty(pb * len(lst) + 64, dtype=t.uint8, device="cuda")
+                off = (-raw.data_ptr()) % 64
+                table = raw[off:off + pb * len(lst)]
+                kernels.gemm_group_prepare(lst, table)
+                arr = (kernels._lib.GemmArgs * len(lst))(*lst)
+                self._groups.append((arr, len(lst), table, raw, lst))
 
     def begin(self) -> None:
         """Clear every member's per-forward accumulators and the flag count (one memset)."""
@@ -253,8 +295,12 @@ class ChainGroup:
 
     def forward(self) -> None:
         self.begin()
-        for ch in self.chains:
-            ch.forward()
+        if self.grouped:
+            for arr, n, table, _raw, _keep in self._groups:
+                kernels.gemm_group_launch(arr, n, table)
+        else:
+            for ch in self.chains:
+                ch.forward()
         self.end()
 
     def flags(self) -> tuple:

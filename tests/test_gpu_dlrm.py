@@ -49,9 +49,11 @@ def _plan(policy, S, key):
         [S.THREAD_ONE_SIDED, S.GLOBAL_ABFT, S.UNPROTECTED]
 
 
+@pytest.mark.parametrize("grouped", [False, True])
 @pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("policy", ["global", "thread", "mixed"])
-def test_dlrm_24_chains_match_reference(P, policy, exact):
+def test_dlrm_24_chains_match_reference(P, policy, exact, grouped):
+    """(grouped: every layer depth of the 24 chains as grouped launches, one per depth and scheme.)"""
     import torch
     from paper_2104_09455_b200.network import ChainGroup
     S = P.Scheme
@@ -60,7 +62,9 @@ def test_dlrm_24_chains_match_reference(P, policy, exact):
     wt = {n: [torch.from_numpy(w).cuda() for w in ws] for n, ws in mlps.items()}
     plans = {k: _plan(policy, S, k) for k in keys}
     grp = ChainGroup([(wt[k[0]], k[1], plans[k]) for k in keys], dtype=P.EXACT_INT if exact else P.BINARY16,
-                     ck_split=True)
+                     ck_split=True, grouped=grouped)
+    if grouped:
+        assert len(grp._groups) <= 9
     for k, ch in zip(keys, grp.chains):
         ch.x.copy_(torch.from_numpy(inputs[k]).cuda())
     grp.forward()
