@@ -2754,7 +2754,10 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
     // augmented weights: the B operand (tile rows + checksum rows per N-block) is ck_rows
     if (a->ck_rows == nullptr || a->ck_rows_n != p.num_n_blocks * p.b_rows_blk || a->ldck < a->K || (a->ldck % 8) ||
         (reinterpret_cast<uintptr_t>(a->ck_rows) & 15))
-      return fail(ABFT_E_SHAPE, "augmented weights do not match this call's plan (see abft_gemm_plan / abft_aug_weights)");
+      return fail(ABFT_E_SHAPE, "augmented weights do not match this call's plan (see abft_gemm_plan / abft_aug_weights): "
+                                "rows " + std::to_string(a->ck_rows_n) + " vs " + std::to_string(p.num_n_blocks) + " x " +
+                                std::to_string(p.b_rows_blk) + ", ld " + std::to_string(a->ldck) + " vs K " +
+                                std::to_string(a->K));
     rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.ck_mode == 4 ? p.bn : p.b_rows_blk);
     // split: the block's checksum rows (and the next block's first rows, whose products land in
     // ignored checksum columns) by a second box
