@@ -348,34 +348,58 @@ __global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ 
   for (int b = 0; b < 8; ++b)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
-  // images strided over the CTAs (registers accumulate across images: one flush per CTA)
-  if (part < parts) for (long long img = blockIdx.x; img < nimg; img += gridDim.x) {
-    for (int i = part; i < nrow + ncol; i += parts) {
+  // (image, border pixel) items strided over every thread slot of the grid, four items in flight
+  // per thread (the loop is latency-bound); registers accumulate: one flush per CTA
+  const long long per_img = nrow + ncol;
+  const long long items = nimg * per_img;
+  const long long step = (long long)gridDim.x * parts;
+  auto item_px = [&](long long it, int& hh, int& ww) -> long long {
+    const long long img = it / per_img;
+    const int i = (int)(it - img * per_img);
+    if (i < nrow) {
+      hh = (i < W) ? 0 : H - 1;
+      ww = i % W;
+    } else {
+      const int j = i - nrow;
+      hh = 1 + j % (H - 2);
+      ww = (W > 1 && j >= H - 2) ? W - 1 : 0;
+    }
+    return (img * H + hh) * W + ww;
+  };
+  auto accum = [&](const uint4& u, int hh, int ww) {
+    float v[8];
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = Unpack2<T>::f(w4[e]);
+      v[2 * e] = f.x;
+      v[2 * e + 1] = f.y;
+    }
+    const bool p0 = hh == 0, pl = hh == H - 1, q0 = ww == 0, ql = ww == W - 1;
+    const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (in[b])
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[b][e] += v[e];
+  };
+  if (part < parts) {
+    long long it = (long long)blockIdx.x * parts + part;
+    for (; it + 3 * step < items; it += 4 * step) {
+      int hh[4], ww[4];
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long px = item_px(it + k * step, hh[k], ww[k]);
+        u[k] = __ldg(reinterpret_cast<const uint4*>(x + px * ldx + c8 * 8));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) accum(u[k], hh[k], ww[k]);
+    }
+    for (; it < items; it += step) {
       int hh, ww;
-      if (i < nrow) {
-        hh = (i < W) ? 0 : H - 1;
-        ww = i % W;
-      } else {
-        const int j = i - nrow;
-        hh = 1 + j % (H - 2);
-        ww = (W > 1 && j >= H - 2) ? W - 1 : 0;
-      }
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + ((img * H + hh) * W + ww) * ldx + c8 * 8));
-      float v[8];
-      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = Unpack2<T>::f(w4[e]);
-        v[2 * e] = f.x;
-        v[2 * e + 1] = f.y;
-      }
-      const bool p0 = hh == 0, pl = hh == H - 1, q0 = ww == 0, ql = ww == W - 1;
-      const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (in[b])
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[b][e] += v[e];
+      const long long px = item_px(it, hh, ww);
+      accum(__ldg(reinterpret_cast<const uint4*>(x + px * ldx + c8 * 8)), hh, ww);
     }
   }
   if (part < parts) {
@@ -400,7 +424,8 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(cons
   const int threads = cv >= 256 ? cv : (256 / cv) * cv;
   if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "border_sums: more than 256 channel vectors");
   const size_t smem = (size_t)8 * c * sizeof(float);
-  const int grid = std::min(n, num_sms());
+  const long long items = (long long)n * ((h > 1 ? 2 : 1) * w + (h > 2 ? (w > 1 ? 2 : 1) * (h - 2) : 0));
+  const int grid = (int)std::max(1LL, std::min<long long>(4LL * num_sms(), items / 16));
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
     border_sums_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, n, h, w, c, ldx, wsum, ws_ld);

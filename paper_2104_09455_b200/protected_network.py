@@ -304,12 +304,12 @@ class ProtectedNetwork:
         self.pools.append(prod)
 
         def run():
+            kernels.maxpool_nhwc(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad, ceil_mode, self.dtype, out.buf,
+                                 out.ld)
             if prod.ws_active:
-                kernels.maxpool_nhwc_ws(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad, ceil_mode, self.dtype, out.buf,
-                                        out.ld, prod._wsum, out.cp, prod.ws_mode)
-            else:
-                kernels.maxpool_nhwc(x.buf, x.n, x.h, x.w, x.cp, x.ld, k, stride, pad, ceil_mode, self.dtype, out.buf,
-                                     out.ld)
+                # the consumer's column sums by one streaming pass over the pooled output (measured
+                # cheaper than accumulating them inside the pooling kernel, abft_nhwc_maxpool_ws)
+                kernels.colsum(out.buf, out.n * out.h * out.w, out.cp, out.ld, self.dtype, prod._wsum, accumulate=True)
         self.add_glue("maxpool", run)
         prod.run = run
         return out
