@@ -145,7 +145,8 @@ typedef struct {
    * (both warp sets on every tile) for narrow tiles, which otherwise alternate whole tiles; bits 6-8
    * = k-blocks of gathered-stem copies in flight (3..7, 0 = 3); bit 9 = 64-byte-row output stores
    * (32-column boxes) instead of 128-byte rows; bit 10 = the global lhs comes from outside the
-   * kernel (see wsum below). */
+   * kernel (see wsum below); bit 11 = (abft_conv2d) per-tap im2col boxes instead of the halo
+   * windows for a stride-1 conv (full 128-row tiles, no row-shifted A operands). */
   int32_t plan_flags;
   /* optional window column sums of THIS layer's stored output (after bias / residual / ReLU /
    * rounding) for the next layer's global lhs (the fused activation checksum):

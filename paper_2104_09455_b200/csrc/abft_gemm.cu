@@ -866,15 +866,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_after();
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
             const uint64_t bd = b_base + (uint64_t)s * b_sstep;
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              ptx::mma_f16_ss_w(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0);
-            if (kb + 1 < L_nkb) {
+            if (ptx::elect_one()) {
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
-                ptx::mma_f16_ss_w(d, ad + a_half + 2ull * k, bd + b_half + 2ull * k, idesc_m, 1u);
+                ptx::mma_f16_ss(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0);
+              if (kb + 1 < L_nkb) {
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  ptx::mma_f16_ss(d, ad + a_half + 2ull * k, bd + b_half + 2ull * k, idesc_m, 1u);
+              }
+              ptx::mma_commit(&empty[s]);
             }
-            ptx::mma_commit_w(&empty[s]);
+            __syncwarp();
             if (++s == L_stages) { s = 0; ph ^= 1; }
           }
           ptx::mma_commit_w(&tfull[acc]);
@@ -889,13 +892,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
             const uint64_t bd = b_base + (uint64_t)(b_res ? kb : s) * b_sstep;   // resident B: by k-block
             const uint64_t cd = c_base + (uint64_t)s * c_sstep;
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              const uint32_t accum = (kb | k) != 0;
-              ptx::mma_f16_ss_w(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
-              if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint32_t accum = (kb | k) != 0;
+                ptx::mma_f16_ss(d, ad + (uint64_t)k * a_kstep, bd + 2ull * k, idesc_m, accum);
+                if (ck_loaded) ptx::mma_f16_ss(d + bn, ad + (uint64_t)k * a_kstep, cd + 2ull * k, L_idesc_ck, accum);
+              }
+              ptx::mma_commit(&empty[s]);
             }
-            ptx::mma_commit_w(&empty[s]);
+            __syncwarp();
             if (++s == L_stages) { s = 0; ph ^= 1; }
           }
           ptx::mma_commit_w(&tfull[acc]);
@@ -916,19 +922,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bd0 = b_base + (uint64_t)(b_res ? kb : s) * b_sstep;
             const uint64_t cd0 = c_base + (uint64_t)s * c_sstep;
             const uint64_t b_tstep = L_b_tile_bytes >> 4, c_tstep = (uint64_t)(L_nck_pad * 128) >> 4;
+            if (ptx::elect_one()) {
 #pragma unroll 1
-            for (int si = 0; si < L_cv_S; ++si) {
-              const uint64_t ad = ad0 + 8ull * (uint64_t)si;
-              const uint64_t bdt = bd0 + b_tstep * (uint64_t)si;
-              const uint64_t cdt = cd0 + c_tstep * (uint64_t)si;
+              for (int si = 0; si < L_cv_S; ++si) {
+                const uint64_t ad = ad0 + 8ull * (uint64_t)si;
+                const uint64_t bdt = bd0 + b_tstep * (uint64_t)si;
+                const uint64_t cdt = cd0 + c_tstep * (uint64_t)si;
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k) {
-                const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
-                ptx::mma_f16_ss_w(d, ad + 2ull * k, bdt + 2ull * k, idesc_m, accum);
-                if (ck_loaded) ptx::mma_f16_ss_w(d + bn, ad + 2ull * k, cdt + 2ull * k, L_idesc_ck, accum);
+                for (int k = 0; k < BK / 16; ++k) {
+                  const uint32_t accum = (kb | si | k) != 0 ? 1u : 0u;
+                  ptx::mma_f16_ss(d, ad + 2ull * k, bdt + 2ull * k, idesc_m, accum);
+                  if (ck_loaded) ptx::mma_f16_ss(d + bn, ad + 2ull * k, cdt + 2ull * k, L_idesc_ck, accum);
+                }
               }
+              ptx::mma_commit(&empty[s]);
             }
-            ptx::mma_commit_w(&empty[s]);
+            __syncwarp();
             if (++s == L_stages) { s = 0; ph ^= 1; }
             continue;
           }
@@ -2851,7 +2860,8 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
                                                          c->gemm.lhs_rowck != nullptr)
                                                       : c->gemm.ck_layout == 1);   // plan == launch
     const int mt = thread_level ? std::max(1, c->gemm.thread_m) : 1;
-    if (mode == 1 && c->stride_h == 1 && c->stride_w == 1 && c->s <= 16 && ck_ok && c->gemm.a_colck == nullptr &&
+    if (mode == 1 && !(c->gemm.plan_flags & 2048) && c->stride_h == 1 && c->stride_w == 1 && c->s <= 16 && ck_ok &&
+        c->gemm.a_colck == nullptr &&
         c->gemm.scheme != ABFT_REPL_FULL && c->gemm.scheme != ABFT_REPL_SINGLE) {
       for (int t = 128; t >= 64; t -= 16)
         if (g.Q % t == 0 && t % mt == 0) { g.Qt = t; break; }

@@ -239,6 +239,13 @@ __host__ __device__ __forceinline__ uint32_t idesc_f16(uint32_t ab_fmt, uint32_t
 // registers; a loop confined to lane 0 makes ptxas wrap every TMA / MMA operand in a
 // per-instruction uniformity loop (ELECT / R2UR.BROADCAST / BRA.U.ANY).
 #define ABFT_ELECT_PRED "elect.sync _|P, 0xffffffff;\n\t"
+// one elected lane of a converged warp (the MMA issuer's batches: a k-block's MMAs and their commit
+// under one election instead of an elect / divergence check per instruction)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED "selp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0u;
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
   asm volatile("{\n\t.reg .pred P;\n\t" ABFT_ELECT_PRED
                "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),

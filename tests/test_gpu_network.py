@@ -266,3 +266,45 @@ def test_fused_window_checksums(PN, name):
     # switching the consumer away from the fused lhs stops the producer's window sums
     net.set_global_variant(C, "slice")
     assert not P.ws_active or any(L.gvar == "fused" for L in net.fused_consumers(P))
+
+
+@pytest.mark.parametrize("name", ["vgg16", "resnet50"])
+def test_per_tap_im2col_plan_flag(PN, name):
+    """plan_flags bit 11 (per-tap im2col boxes instead of halo windows on stride-1 convs, a plan the
+    profiler times): every layer still matches the fp32 checker under every scheme and global
+    variant, clean runs flag nothing, and a fault in a 3x3 layer on that plan is flagged there."""
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model(name), 2)
+    x = _input(2, seed=6)
+    convs = [L for L in net.layers if L.kind == "conv" and L.r == 3 and L.stride == 1 and L.x.c >= 48]
+    assert convs
+    for L in convs:
+        for key in net.keys_of(L):
+            net.set_tile(L, key, 0, 2048)
+    for scheme, variant in ((S.UNPROTECTED, None), (S.GLOBAL_ABFT, "slice"), (S.GLOBAL_ABFT, "dot"),
+                            (S.GLOBAL_ABFT, "fused"), (S.THREAD_ONE_SIDED, None)):
+        net.set_schemes(scheme)
+        if variant:
+            for L in convs:
+                if variant != "fused" or L.producer is not None:
+                    net.set_global_variant(L, variant)
+        net.forward(x)
+        torch.cuda.synchronize()
+        assert net.flags() == (0, 0), (scheme, variant, net.flags())
+        for L in net.layers:
+            check_layer(L)
+        if scheme is S.GLOBAL_ABFT:
+            vs = net.verdicts()
+            assert all(not v.detected and abs(v.lhs - v.rhs) < 0.05 * v.tolerance_used for v in vs), variant
+    net.set_schemes(S.GLOBAL_ABFT)
+    for L in convs:
+        net.set_global_variant(L, "slice")
+    net.forward(x)
+    # (K <= 600: above ~1024 the reference tau grows with the fault itself, checksum.py:143-148)
+    T = [L for L in convs if L.k_ref <= 600][-1]
+    tau = net.verdicts()[T.index].tolerance_used
+    net.inject({T.index: [(T.m // 5, 2, 8.0 * tau + 64.0)]})
+    net.forward(x)
+    assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [T.index]
+    net.inject({})

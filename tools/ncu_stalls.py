@@ -1,6 +1,6 @@
 """Stall-reason breakdown of the SASS lines executed exactly `ex` times (one code region) in an ncu report.
 usage: python tools/ncu_stalls.py REP [ex ...]   (no ex: list the most-sampled execution counts)"""
-import csv, subprocess, sys
+import csv, os, subprocess, sys
 from collections import defaultdict
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
@@ -32,5 +32,12 @@ for ex in exs:
             tot[hdr[i]] += int(r[i] or 0)
         top.append((int(r[ist] or 0), r[isrc][:80]))
     print(f"ex={ex}: " + ", ".join(f"{k[6:]}={v}" for k, v in sorted(tot.items(), key=lambda x: -x[1]) if v))
-    for st, src in sorted(top, reverse=True)[:12]:
+    # (STALL_ORDER=1: every sampled line of the region in program order, with its top stall reason)
+    if os.environ.get("STALL_ORDER"):
+        for r in body:
+            if int(r[iex] or 0) == ex and int(r[ist] or 0) > 0:
+                why = max(stall_cols, key=lambda i: int(r[i] or 0))
+                print(f"   {int(r[ist]):5d} {hdr[why][6:18]:12s} {r[isrc][:90]}")
+        continue
+    for st, src in sorted(top, reverse=True)[:int(os.environ.get("STALL_TOP", "12"))]:
         print(f"   {st:5d}  {src}")
