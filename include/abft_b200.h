@@ -146,7 +146,11 @@ typedef struct {
    * = k-blocks of gathered-stem copies in flight (3..7, 0 = 3); bit 9 = 64-byte-row output stores
    * (32-column boxes) instead of 128-byte rows; bit 10 = the global lhs comes from outside the
    * kernel (see wsum below); bit 11 = (abft_conv2d) per-tap im2col boxes instead of the halo
-   * windows for a stride-1 conv (full 128-row tiles, no row-shifted A operands). */
+   * windows for a stride-1 conv (full 128-row tiles, no row-shifted A operands); bit 12 = CTA pairs:
+   * 2-CTA clusters on the two SMs of a TPC, one M = 256 tcgen05.mma.cta_group::2 per k-step issued
+   * by the leader, each CTA staging its own 128 A rows and half of the B rows (plain-class GEMMs /
+   * 64-channel im2col convs: unprotected, global with the checksum slice in the weight tile or the
+   * external lhs; ABFT_E_UNSUPPORTED otherwise). */
   int32_t plan_flags;
   /* optional window column sums of THIS layer's stored output (after bias / residual / ReLU /
    * rounding) for the next layer's global lhs (the fused activation checksum):

@@ -156,6 +156,10 @@ struct GemmParams {
   uint32_t off_ws;
   const GroupProblem* group;         // grouped launch: the problem table (device memory), else null
   int group_n;
+  // CTA pairs (the AM 3 instances, plan_flags bit 12): M tiles per N block (even; tiles numbered
+  // M-fastest, so CTAs 2c and 2c+1 of a cluster take M blocks 2j, 2j+1 of one N block) and the B
+  // rows each CTA of the pair stages (half of the MMA's N)
+  int pair, m_tiles, b_half;
 };
 
 template <typename T>
@@ -505,7 +509,9 @@ __device__ __forceinline__ void lean_store_row(const float (&v)[32], void* C, in
 }
 
 // AM: the A-load family of the instance — 0 TMA tiles / im2col boxes (a_mode 0-2), 1 halo
-// windows (a_mode 4), 2 gathered stems (a_mode 5)
+// windows (a_mode 4), 2 gathered stems (a_mode 5), 3 CTA pairs over TMA tiles / 64-channel im2col
+// boxes (a_mode 0-1; plain class): 2-CTA clusters, one M = 256 cta_group::2 MMA per k-step issued
+// by the leader, each CTA staging its 128 A rows and half of the B rows
 // WS: the instance accumulates window sums of its output (a producer of fused consumers); kept out
 // of the other instances, whose epilogue loops would otherwise spill
 template <typename T, int CLASS, int NT, int AM, bool WS>
@@ -562,6 +568,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // keeping the GEMM instances' hot loops free of them
   constexpr bool HALO = AM == 1;
   constexpr bool gather = AM == 2;
+  constexpr bool PAIR = AM == 3;
+  const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0u;
   const bool halo = HALO && p.a_mode == 4;
   const bool b_res = (HALO || gather) && p.b_resident;
   const int bn = p.bn;
@@ -580,7 +588,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 4; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], p.epi_tiles ? 4 : 8);    // one arrival per epilogue warp of the tile
+      // one arrival per epilogue warp of the tile (of both CTAs: a pair's leader holds the barrier)
+      ptx::mbar_init(&tempty[a], (p.epi_tiles ? 4 : 8) * (PAIR ? 2 : 1));
     }
     ptx::fence_mbar_init();
   }
@@ -595,7 +604,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (p.out_wide) ptx::tma_prefetch(&tmC2);
     }
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
+  if (warp == 1) {
+    if constexpr (PAIR) ptx::tmem_alloc2(tmem_holder, (uint32_t)p.tmem_cols);
+    else ptx::tmem_alloc(tmem_holder, (uint32_t)p.tmem_cols);
+  }
   if (warp >= EPI_WARP0 && warp < CK_WARP0 && p.colck_in_smem) {
     for (int i = threadIdx.x - EPI_WARP0 * 32; i < p.N; i += 256) colck_s[i] = 0.f;
   }
@@ -613,9 +625,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::fence_proxy_async_smem();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  // (a pair: both CTAs' barriers initialised before either signals the other's)
+  if constexpr (PAIR) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // an accumulator stage read out: hand it back to the MMA issuer (a pair's leader)
+  auto tempty_arrive = [&](int acc) {
+    if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+    else ptx::mbar_arrive(&tempty[acc]);
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -691,8 +710,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // gathered stems: the checksum warps fill the A stages; B is resident (loaded above)
       for (int tile = (gather || p.group != nullptr) ? L_num_tiles : (int)blockIdx.x; tile < L_num_tiles;
            tile += gridDim.x) {
-        const int nb = tile % L_num_n_blocks;
-        const int m0 = (tile / L_num_n_blocks) * L_bm_eff;
+        const int nb = PAIR ? tile / p.m_tiles : tile % L_num_n_blocks;
+        const int m0 = (PAIR ? tile % p.m_tiles : tile / L_num_n_blocks) * L_bm_eff;
         const int n0 = nb * L_bn_eff;
         // global lhs dot: the tile row's first N block also brings each k-block's rowck(B) slice
         const bool w_tile = p.lhs_w != nullptr && nb == 0;
@@ -706,6 +725,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int pp = rem / L_cv_Q;
           ho = pp * p.cv_sh - p.cv_ph;
           wo = (rem - pp * L_cv_Q) * p.cv_sw - p.cv_pw;
+        }
+        if constexpr (PAIR) {
+          // CTA pair: this CTA's 128 A rows and its half of the B rows, both completing on the
+          // leader's full barrier, which expects the pair's bytes
+          const uint32_t tx2 = 2u * (L_stage_a_bytes + L_tx_b);
+          const int brow = (ck_aug ? nb * L_b_rows_blk : n0) + (int)crank * p.b_half;
+#pragma unroll 1
+          for (int kb = 0; kb < L_nkb; ++kb) {
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            if (crank == 0) ptx::mbar_arrive_expect_tx_w2(&full[s], tx2);
+            const uint32_t fb = ptx::mapa_shared(ptx::smem_u32(&full[s]), 0);
+            uint8_t* a_dst = sm_a + s * L_stage_a_bytes;
+            if (L_a_mode == 0) {
+              ptx::tma_load_2d_w2(a_dst, &tmA, fb, kb * BK, m0);
+            } else {
+              const int tap = kb / L_cv_chunks;
+              const int r = tap / L_cv_S;
+              ptx::tma_load_im2col_4d_w2(a_dst, &tmA, fb, (kb - tap * L_cv_chunks) * BK, wo, ho, img,
+                                         (uint16_t)(tap - r * L_cv_S), (uint16_t)r);
+            }
+            ptx::tma_load_2d_w2(sm_b + s * L_stage_b_bytes, &tmB, fb, kb * BK, brow);
+            if (++s == L_stages) { s = 0; ph ^= 1; }
+          }
+          continue;
         }
         if (p.kpair) {
           // two k-blocks per stage: A (kb, kb+1) and B (kb, kb+1) boxes side by side
@@ -801,6 +844,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
+    if constexpr (PAIR) {
+      // CTA pair: the leader issues M = 256 MMAs over both CTAs' stages; each commit arrives on
+      // the stage / accumulator barriers of both CTAs
+      if (crank == 0) {
+        const uint64_t a_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_a));
+        const uint64_t b_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_b));
+        const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4;
+        const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
+        const int L_nkb = p.nkb, L_stages = p.stages, L_acc_stages = p.acc_stages, L_cols = p.cols_per_acc;
+        const int L_num_tiles = p.num_tiles;
+        int s = 0;
+        uint32_t ph = 0;
+        int t_local = 0;
+        for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x, ++t_local) {
+          const int acc = t_local % L_acc_stages;
+          const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
+          ptx::mbar_wait(&tempty[acc], aph ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d = tmem_base + (uint32_t)(acc * L_cols);
+#pragma unroll 1
+          for (int kb = 0; kb < L_nkb; ++kb) {
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            const uint64_t ad = a_base + (uint64_t)s * a_sstep;
+            const uint64_t bd = b_base + (uint64_t)s * b_sstep;
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
+              ptx::mma_commit2_mc(&empty[s], 3);
+            }
+            __syncwarp();
+            if (++s == L_stages) { s = 0; ph ^= 1; }
+          }
+          if (ptx::elect_one()) ptx::mma_commit2_mc(&tfull[acc], 3);
+          __syncwarp();
+        }
+      }
+    } else {
     // loop-invariant parameters in registers (the asm memory clobbers would otherwise reload them)
     const auto L_a_mode = p.a_mode;
     const auto L_acc_stages = p.acc_stages;
@@ -999,6 +1081,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mma_commit_w(&tfull[acc]);
       }
     }
+    }   // !PAIR
   } else if (warp >= CK_WARP0) {
     if constexpr (gather) {
       // ------------------------------------------ gathered stem A tiles (a_mode 5)
@@ -1530,9 +1613,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mc = &gpr->mc; mc2 = &gpr->mc2; Cp = gpr->C; ldc = gpr->ldc;
           lt = tile - gpr->tile_begin;
         }
-        const int mb = lt / nnb;
+        const int mb = PAIR ? lt % p.m_tiles : lt / nnb;
         const int m0 = mb * bm_eff;
-        const int n0 = (lt - mb * nnb) * bn_eff;
+        const int n0 = (PAIR ? lt / p.m_tiles : lt - mb * nnb) * bn_eff;
         const int gm = m0 + row;
         const bool row_in_tile = row < bm_eff;
         const bool row_valid = row_in_tile && gm < M;
@@ -1588,7 +1671,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        if (lane == 0) tempty_arrive(acc);
         if (row_valid) rhs_acc += (double)tsum;
       }
       if (gpr != nullptr) group_flush(gpr);
@@ -1628,9 +1711,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mc = &gpr->mc; mc2 = &gpr->mc2; Cp = gpr->C; ldc = gpr->ldc;
             lt = tile - gpr->tile_begin;
           }
-          const int mb = lt / nnb;
+          const int mb = PAIR ? lt % p.m_tiles : lt / nnb;
           const int m0 = mb * bm_eff;
-          const int n0 = (lt - mb * nnb) * bn_eff;
+          const int n0 = (PAIR ? lt / p.m_tiles : lt - mb * nnb) * bn_eff;
           const int gm = m0 + row;
           const bool row_in_tile = row < bm_eff;
           const int t_row = gm / mt;
@@ -1695,15 +1778,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          if (lane == 0) tempty_arrive(acc);
         }
       }
     }
     for (int tile = lean ? p.num_tiles : (int)blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++t_local) {
       const int acc = t_local % p.acc_stages;
       const uint32_t aph = (uint32_t)(t_local / p.acc_stages) & 1u;
-      const int m0 = (tile / p.num_n_blocks) * p.bm_eff;
-      const int n0 = (tile % p.num_n_blocks) * p.bn_eff;
+      const int m0 = (PAIR ? tile % p.m_tiles : tile / p.num_n_blocks) * p.bm_eff;
+      const int n0 = (PAIR ? tile / p.m_tiles : tile % p.num_n_blocks) * p.bn_eff;
       const int gm = m0 + row;
       const bool row_in_tile = row < p.bm_eff;
       const bool row_store = row_in_tile && gm < p.M;
@@ -2008,7 +2091,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // TMEM accumulator stage fully read: hand it back to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) tempty_arrive(acc);
       if (row_store) rhs_acc += (double)tsum;
 
       if (thread_level && !p.shuffle_verdicts && h == 0) {
@@ -2049,7 +2132,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  // (a pair: neither CTA leaves while the leader's MMAs / the peer's barrier arrivals are in flight)
+  if constexpr (PAIR) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   __syncwarp();
   if (p.group == nullptr && (p.out_sum != nullptr || p.out_partials != nullptr || p.lhs_epi) && warp == EPI_WARP0) {
@@ -2074,7 +2159,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (warp == 1) ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+  if (warp == 1) {
+    if constexpr (PAIR) ptx::tmem_dealloc2(tmem_base, (uint32_t)p.tmem_cols);
+    else ptx::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+  }
   if (p.vn > 0 && warp == EPI_WARP0) {
     // fused deferred verification: the launch's last CTA to finish (done-count) forms every
     // layer's verdict from the accumulated (lhs, rhs) pairs (checksum.py:151-153, :237).  Lane 0
@@ -2181,19 +2269,28 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
-  if (p.pdl) {
+  if (p.pdl || p.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (p.pair) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = 2;
+      attr[na].val.clusterDim.y = 1;
+      attr[na++].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return cuda_check(cudaLaunchKernelEx(&cfg, abft_gemm_kernel<T, CLASS, NT, AM, WS>, ma, mb, mc, mo, mo2, p),
-                      "abft_gemm_kernel launch (PDL)");
+                      "abft_gemm_kernel launch (PDL / CTA pairs)");
   }
   abft_gemm_kernel<T, CLASS, NT, AM, WS><<<grid, NUM_THREADS, smem, st>>>(ma, mb, mc, mo, mo2, p);
   return cuda_check(cudaGetLastError(), "abft_gemm_kernel launch");
@@ -2232,6 +2329,11 @@ int launch_cls(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, c
 template <typename T>
 int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                  const CUtensorMap& mo, const CUtensorMap& mo2, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+  if (p.pair) {
+    if (cls != CLASS_PLAIN) return fail(ABFT_E_UNSUPPORTED, "CTA pairs: plain class only");
+    if (p.wsum != nullptr) return launch_inst<T, CLASS_PLAIN, 0, 3, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    return launch_inst<T, CLASS_PLAIN, 0, 3, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+  }
   if (p.a_mode == 4) return launch_cls<T, 1>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
   if (p.a_mode == 5) return launch_cls<T, 2>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
   return launch_cls<T, 0>(cls, ntc, ma, mb, mc, mo, mo2, p, smem, grid, st);
@@ -2374,7 +2476,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
       const long long waves = tiles <= 4LL * sms ? 100 * ((tiles + sms - 1) / sms) : (100 * tiles + sms - 1) / sms;
       const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
       const bool asplit = a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256;
-      if (asplit && cand != 256) continue;
+      if (asplit && (cand != 256 || (a->plan_flags & 4096))) continue;   // (CTA pairs: one B box per k-block)
       // the split's second (N = nck) MMA per k-step costs about 64 rows' worth
       // im2col A boxes cost about twice a tiled box; tiles whose width is not a whole number of
       // 32-column chunks lose the bulk-tensor output stores (~4 k-blocks of epilogue)
@@ -2504,7 +2606,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.kpair = (!halo && (cg == nullptr || cg->a_mode == 0 || cg->a_mode == 1 || cg->a_mode == 3) &&
              (p.ck_mode == 0 || p.ck_mode == 3) &&
              !has_shadow && !want_acolck && a->lhs_rowck == nullptr && p.nkb >= 2 &&
-             ov.kpair && !(a->plan_flags & 1)) ? 1 : 0;
+             ov.kpair && !(a->plan_flags & 1) && !(a->plan_flags & 4096)) ? 1 : 0;
   if (p.kpair) {
     // only while the pipeline keeps >= 3 stages of pairs (tiles up to ~128 columns: the
     // latency-bound GEMMs); wide tiles keep single k-block stages
@@ -2515,6 +2617,23 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   if (p.kpair) {
     p.stage_a_bytes *= 2;
     p.stage_b_bytes *= 2;
+  }
+  if (a->plan_flags & 4096) {
+    // CTA pairs (plan_flags bit 12): 2-CTA clusters, M = 256 per MMA, each CTA staging half of
+    // the B rows; the plain-class paths over TMA tiles / 64-channel im2col boxes only
+    const int n_mma = p.ck_mode == 3 ? bn + p.nck_pad : bn;
+    if (halo || gather || (cg != nullptr && cg->a_mode == 2) || out.cls != CLASS_PLAIN ||
+        p.lhs_w != nullptr || want_acolck || (p.ck_mode != 0 && p.ck_mode != 3) || n_mma % 16 != 0)
+      return fail(ABFT_E_UNSUPPORTED, "CTA pairs: plain / global-slice GEMMs and 64-channel im2col convs only");
+    p.pair = 1;
+    p.b_half = n_mma / 2;
+    p.stage_b_bytes = (uint32_t)round_up(p.b_half * BK * 2, 1024);
+    p.b_tile_bytes = p.stage_b_bytes;
+    p.tx_b = (uint32_t)p.b_half * BK * 2;
+    p.idesc_main = ptx::idesc_f16(fmt, 2 * BM, bn);
+    p.idesc_aug = ptx::idesc_f16(fmt, 2 * BM, (uint32_t)n_mma);
+    p.m_tiles = round_up(p.num_m_blocks, 2);
+    p.num_tiles = p.m_tiles * p.num_n_blocks;
   }
   p.rec_stride = (thread_level && !p.shuffle_verdicts) ? (p.groups | 1) : 0;
   const uint32_t cks_bytes = has_ck ? (uint32_t)(32 * BM * 4) : 0;
@@ -2614,6 +2733,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.off_bar = p.off_ws + ws_bytes;
   out.smem = (size_t)p.off_bar + bar_bytes + 1024;
   out.grid = std::min(p.num_tiles, sms);
+  if (p.pair) out.grid &= ~1;      // whole clusters (num_tiles is even)
   out.ck_offline_recommended = (has_ck && p.num_m_blocks > 2) ? 1 : 0;
   return ABFT_OK;
 }
@@ -2767,7 +2887,8 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
                                 "rows " + std::to_string(a->ck_rows_n) + " vs " + std::to_string(p.num_n_blocks) + " x " +
                                 std::to_string(p.b_rows_blk) + ", ld " + std::to_string(a->ldck) + " vs K " +
                                 std::to_string(a->K));
-    rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.ck_mode == 4 ? p.bn : p.b_rows_blk);
+    rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck,
+                    p.pair ? p.b_half : p.ck_mode == 4 ? p.bn : p.b_rows_blk);
     // split: the block's checksum rows (and the next block's first rows, whose products land in
     // ignored checksum columns) by a second box
     if (rc == ABFT_OK && p.ck_mode == 4) rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
@@ -2775,7 +2896,7 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
     // plan_flags bit 1: Bt holds zero rows up to a whole number of tiles, so the weight boxes never
     // cross the tensor's edge (no out-of-bounds fill on the load path)
     const int64_t b_rows = (a->plan_flags & 2) ? (int64_t)round_up(a->N, p.bn) : (int64_t)a->N;
-    rc = cached_map(&mb, a->Bt, a->dtype, a->K, b_rows, a->ldbt, p.bn);
+    rc = cached_map(&mb, a->Bt, a->dtype, a->K, b_rows, a->ldbt, p.pair ? p.b_half : p.bn);
   }
   if (rc != ABFT_OK) return rc;
   if (p.ck_mode == 2) {
@@ -2959,6 +3080,7 @@ int group_plans(const abft_gemm_args_t* args, int count, Plan& common, std::vect
   for (int i = 0; i < count; ++i) {
     abft_gemm_args_t a = args[i];
     a.plan_flags |= 1 | 4;
+    if (a.plan_flags & 4096) return fail(ABFT_E_UNSUPPORTED, "group: no CTA pairs");
     if (a.lda < a.K || (a.lda % 8)) return fail(ABFT_E_SHAPE, "group: lda must be >= K and a multiple of 8");
     int rc = validate_common(&a);
     if (rc != ABFT_OK) return rc;
@@ -3097,8 +3219,9 @@ static int conv_make_plan(const abft_conv_args_t* c, ConvGeom& g, abft_gemm_args
   rc = validate_common(&ga);
   if (rc != ABFT_OK) return rc;
   rc = make_plan(&ga, pl, &g);
-  if (rc != ABFT_OK && g.a_mode == 5) {
+  if (rc != ABFT_OK && g.a_mode == 5 && !(c->gemm.plan_flags & 4096)) {
     // a call the gathered stem cannot take: the explicit im2col on the same (tap, 4-channel) K
+    // (not for a plan hint the stem cannot take: that call fails instead of needing a workspace)
     g.a_mode = 3;
     g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
     rc = make_plan(&ga, pl, &g);

@@ -328,113 +328,105 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
 }
 
 // The border buckets (1..8) of a 3x3 consumer's window sums, from the activation's border pixels
-// only (first / last row and column of every image): CTA = one image; a thread keeps one
-// 8-channel vector and a slice of the border, sums in registers, one smem reduction and one
-// atomic per (bucket, channel) per image.  Bucket 0 (all pixels) comes from the producer's epilogue.
+// only.  Each bucket is one pixel segment per image — 1: row 0, 2: row H-1, 3: column 0,
+// 4: column W-1 (all of them, corners included), 5..8: the corners (0,0), (0,W-1), (H-1,0),
+// (H-1,W-1) — so a CTA = (bucket, group of images) and a thread = (8-channel vector, slice of the
+// group's segment pixels) keeps ONE 8-float accumulator, with up to 8 loads in flight.  The CTA's
+// slices meet in shared memory and leave as one 16-byte atomic per 4 channels.  Bucket 0 (all
+// pixels) comes from the producer's epilogue.
 template <typename T>
-__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, long long nimg, int H, int W, int C,
-                                                          long long ldx, float* __restrict__ ws, int ws_ld) {
-  extern __shared__ float bsm[];           // [8][C]
+__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, int nimg, int imgs_per_cta, int H,
+                                                          int W, int C, long long ldx, float* __restrict__ ws,
+                                                          int ws_ld) {
+  extern __shared__ float bsm[];           // [parts][C]
+  const int bucket = 1 + (int)blockIdx.y;
   const int cv = C / 8;
   const int parts = blockDim.x / cv;
-  for (int i = threadIdx.x; i < 8 * C; i += blockDim.x) bsm[i] = 0.f;
-  __syncthreads();
   const int c8 = threadIdx.x % cv, part = threadIdx.x / cv;
-  // border pixel list: rows 0 and H-1 (all W columns), then columns 0 and W-1 of rows 1..H-2
-  const int nrow = (H > 1 ? 2 : 1) * W;
-  const int ncol = H > 2 ? (W > 1 ? 2 : 1) * (H - 2) : 0;
-  float acc[8][8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[b][e] = 0.f;
-  // (image, border pixel) items strided over every thread slot of the grid, four items in flight
-  // per thread (the loop is latency-bound); registers accumulate: one flush per CTA
-  const long long per_img = nrow + ncol;
-  const long long items = nimg * per_img;
-  const long long step = (long long)gridDim.x * parts;
-  auto item_px = [&](long long it, int& hh, int& ww) -> long long {
-    const long long img = it / per_img;
-    const int i = (int)(it - img * per_img);
-    if (i < nrow) {
-      hh = (i < W) ? 0 : H - 1;
-      ww = i % W;
-    } else {
-      const int j = i - nrow;
-      hh = 1 + j % (H - 2);
-      ww = (W > 1 && j >= H - 2) ? W - 1 : 0;
+  const int seg = bucket <= 2 ? W : (bucket <= 4 ? H : 1);      // pixels per image
+  const int img0 = blockIdx.x * imgs_per_cta;
+  const int nimg_cta = min(imgs_per_cta, nimg - img0);
+  const int items = nimg_cta * seg;
+  auto pixel = [&](int it) -> long long {
+    const int im = img0 + it / seg, i = it - (it / seg) * seg;
+    int hh, ww;
+    switch (bucket) {
+      case 1: hh = 0; ww = i; break;
+      case 2: hh = H - 1; ww = i; break;
+      case 3: hh = i; ww = 0; break;
+      case 4: hh = i; ww = W - 1; break;
+      case 5: hh = 0; ww = 0; break;
+      case 6: hh = 0; ww = W - 1; break;
+      case 7: hh = H - 1; ww = 0; break;
+      default: hh = H - 1; ww = W - 1; break;
     }
-    return (img * H + hh) * W + ww;
+    return ((long long)im * H + hh) * W + ww;
   };
-  auto accum = [&](const uint4& u, int hh, int ww) {
-    float v[8];
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  auto add = [&](const uint4& u) {
     const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = Unpack2<T>::f(w4[e]);
-      v[2 * e] = f.x;
-      v[2 * e + 1] = f.y;
+      acc[2 * e] += f.x;
+      acc[2 * e + 1] += f.y;
     }
-    const bool p0 = hh == 0, pl = hh == H - 1, q0 = ww == 0, ql = ww == W - 1;
-    const bool in[8] = {p0, pl, q0, ql, p0 && q0, p0 && ql, pl && q0, pl && ql};
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (in[b])
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[b][e] += v[e];
   };
   if (part < parts) {
-    long long it = (long long)blockIdx.x * parts + part;
-    for (; it + 3 * step < items; it += 4 * step) {
-      int hh[4], ww[4];
-      uint4 u[4];
+    const T* xc = x + c8 * 8;
+    int it = part;
+    for (; it + 7 * parts < items; it += 8 * parts) {
+      uint4 u[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long px = item_px(it + k * step, hh[k], ww[k]);
-        u[k] = __ldg(reinterpret_cast<const uint4*>(x + px * ldx + c8 * 8));
-      }
+      for (int k = 0; k < 8; ++k) u[k] = __ldg(reinterpret_cast<const uint4*>(xc + pixel(it + k * parts) * ldx));
 #pragma unroll
-      for (int k = 0; k < 4; ++k) accum(u[k], hh[k], ww[k]);
+      for (int k = 0; k < 8; ++k) add(u[k]);
     }
-    for (; it < items; it += step) {
-      int hh, ww;
-      const long long px = item_px(it, hh, ww);
-      accum(__ldg(reinterpret_cast<const uint4*>(x + px * ldx + c8 * 8)), hh, ww);
-    }
-  }
-  if (part < parts) {
+    for (; it < items; it += parts) add(__ldg(reinterpret_cast<const uint4*>(xc + pixel(it) * ldx)));
 #pragma unroll
-    for (int b = 0; b < 8; ++b)
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (acc[b][e] != 0.f) atomicAdd(&bsm[b * C + c8 * 8 + e], acc[b][e]);
+    for (int e = 0; e < 8; ++e) bsm[part * C + c8 * 8 + e] = acc[e];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 8 * C; i += blockDim.x)
-    if (bsm[i] != 0.f) atomicAdd(&ws[(long long)(1 + i / C) * ws_ld + (i % C)], bsm[i]);
+  float* dst = ws + (long long)bucket * ws_ld;
+  for (int c4 = threadIdx.x; c4 < C / 4; c4 += blockDim.x) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < parts; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(bsm + q * C + c4 * 4);
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    atomicAdd(reinterpret_cast<float4*>(dst + c4 * 4), t);
+  }
 }
 
 extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(const void* x, int32_t n, int32_t h,
                                                                            int32_t w, int32_t c, int64_t ldx,
                                                                            int32_t dtype, float* wsum, int32_t ws_ld,
                                                                            void* stream) {
-  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || c > 1024 || ldx < c || ldx % 8 || wsum == nullptr || ws_ld < c)
-    return fail(ABFT_E_SHAPE, "border_sums: bad extents (channels a multiple of 8 up to 1024, ldx >= c)");
+  if (n < 1 || h < 1 || w < 1 || c < 8 || c % 8 || c > 1024 || ldx < c || ldx % 8 || wsum == nullptr || ws_ld < c ||
+      ws_ld % 4 || (reinterpret_cast<uintptr_t>(wsum) & 15))
+    return fail(ABFT_E_SHAPE, "border_sums: bad extents (channels a multiple of 8 up to 1024, ldx >= c, "
+                              "16-byte aligned wsum rows)");
   const int cv = c / 8;
-  const int threads = cv >= 256 ? cv : (256 / cv) * cv;
-  if (threads > 256) return fail(ABFT_E_UNSUPPORTED, "border_sums: more than 256 channel vectors");
-  const size_t smem = (size_t)8 * c * sizeof(float);
-  const long long items = (long long)n * ((h > 1 ? 2 : 1) * w + (h > 2 ? (w > 1 ? 2 : 1) * (h - 2) : 0));
-  const int grid = (int)std::max(1LL, std::min<long long>(4LL * num_sms(), items / 16));
+  const int parts = 256 / cv;
+  const int threads = parts * cv;
+  const size_t smem = (size_t)parts * c * sizeof(float);
+  // images per CTA: ~16 segment pixels per thread slot of the longest (row / column) buckets
+  const int seg = std::max(h, w);
+  const int ipc = std::max(1, std::min(n, (16 * parts + seg - 1) / seg));
+  const dim3 grid((unsigned)((n + ipc - 1) / ipc), 8u);
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
-    border_sums_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, n, h, w, c, ldx, wsum, ws_ld);
+    border_sums_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, n, ipc, h, w, c, ldx, wsum,
+                                                                   ws_ld);
   else
-    border_sums_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, n, h, w, c, ldx, wsum, ws_ld);
+    border_sums_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, n, ipc, h, w, c, ldx, wsum, ws_ld);
   return cuda_check(cudaGetLastError(), "border_sums launch");
 }
 
-// The consumer's global lhs from the producer's window sums (abft_window_lhs): one CTA, fp64.
+// The consumer's global lhs from the producer's window sums (abft_window_lhs): one (tap, channel)
+// term per thread over up to 64 CTAs, fp64, one atomic per CTA.
 // colck_im2col(r, s, c) of a 3x3 / stride 1 / pad 1 conv over an H x W input = the sum over the
 // input rows / columns tap (r, s) reads: all of them minus the row the tap never reaches (r = 0
 // misses the last row, r = 2 the first) minus the column likewise, plus their corner (counted
@@ -446,7 +438,7 @@ __global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict
   __shared__ double red[8];
   double acc = 0.0;
   const int taps = R * S;
-  for (int i = threadIdx.x; i < taps * C; i += blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < taps * C; i += gridDim.x * blockDim.x) {
     const int tap = i / C, c = i - (i / C) * C;
     double col = ws[c];
     if (R == 3) {
@@ -459,7 +451,7 @@ __global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict
     }
     acc += col * (double)rowck[(long long)tap * ck + c];
   }
-  if (bias != nullptr)
+  if (bias != nullptr && blockIdx.x == 0)
     for (int j = threadIdx.x; j < n_out; j += blockDim.x) acc += (double)M * (double)bias[j];
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -481,7 +473,8 @@ extern "C" __attribute__((visibility("default"))) int abft_window_lhs(const floa
   if (!((R == 1 && S == 1) || (R == 3 && S == 3))) return fail(ABFT_E_UNSUPPORTED, "window_lhs: 1x1 or 3x3 consumers");
   if (C < 1 || ws_ld < C || ck < C || M < 0 || (bias != nullptr && n_out < 1))
     return fail(ABFT_E_SHAPE, "window_lhs: bad extents");
-  window_lhs_kernel<<<1, 256, 0, as_stream(stream)>>>(wsum, ws_ld, C, R, S, ck, rowck, bias, n_out, M, lhs);
+  const int grid = std::max(1, std::min(64, (R * S * C + 255) / 256));
+  window_lhs_kernel<<<grid, 256, 0, as_stream(stream)>>>(wsum, ws_ld, C, R, S, ck, rowck, bias, n_out, M, lhs);
   return cuda_check(cudaGetLastError(), "window_lhs launch");
 }
 

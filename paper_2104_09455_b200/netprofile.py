@@ -28,8 +28,9 @@ from .shapes import DeviceProfile
 
 # plan hints tried: none, no k-block pairs, double output staging, both; direct (unstaged) output
 # stores; the chunk-split epilogue for narrow tiles; 64-byte-row output stores; per-tap im2col
-# instead of halo windows (stride-1 convs)
-PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 512, 2048)
+# instead of halo windows (stride-1 convs); CTA pairs (2-CTA clusters, M = 256 cta_group::2 MMAs),
+# alone and over per-tap im2col
+PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 512, 2048, 4096, 6144)
 
 
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,

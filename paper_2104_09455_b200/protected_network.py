@@ -50,6 +50,7 @@ GLOBAL_DOT = "global-dot"      # argument-set key of the global scheme with the 
 GLOBAL_FUSED = "global-fused"
 ARG_KEYS = SELECTABLE + (GLOBAL_DOT, GLOBAL_FUSED)
 EXT_LHS = 1024
+PAIR_FLAG = 4096   # plan_flags bit 12: CTA pairs (2-CTA clusters, M = 256 cta_group::2 MMAs)
 _VERDICT_DTYPE = np.dtype([("lhs", "<f8"), ("rhs", "<f8"), ("tol", "<f8"), ("det", "<i4"), ("k", "<i4")])
 
 
@@ -435,9 +436,14 @@ class ProtectedNetwork:
         scheme = Scheme.GLOBAL_ABFT if key in (GLOBAL_DOT, GLOBAL_FUSED) else key
         oc8 = _r8(L.oc)
         if key is Scheme.GLOBAL_ABFT:
-            if not hasattr(L, "_gck"):
-                L._gck = kernels.global_ck_rows(L._bt, oc8, L._k, self.dtype, self._plan(L, scheme, kw))
-            kw["ck_rows"] = L._gck
+            # augmented weights per plan (tile / N blocks): plan hints such as CTA pairs may pick
+            # another tile than the default plan
+            pl = self._plan(L, scheme, kw)
+            cache = L.__dict__.setdefault("_gck_by_plan", {})
+            ck_key = (pl["tile_n"], pl["aug_rows"], pl["n_blocks"], pl["nck_pad"])
+            if ck_key not in cache:
+                cache[ck_key] = kernels.global_ck_rows(L._bt, oc8, L._k, self.dtype, pl)
+            kw["ck_rows"] = cache[ck_key]
         elif scheme is Scheme.THREAD_ONE_SIDED:
             if not hasattr(L, "_ock"):
                 L._ock = kernels.aug_weights(L._bt, oc8, L._k, self.dtype, self._plan(L, scheme, kw),
@@ -458,7 +464,15 @@ class ProtectedNetwork:
         old = (L.tile_n.get(key, 0), L.flags.get(key, 0))
         L.tile_n[key], L.flags[key] = int(tile_n), int(flags)
         try:
-            L.args[key] = self._make_args(L, key)
+            kind, a = self._make_args(L, key)
+            # the plan must exist for these hints (a hint the layer's A-load mode cannot take, e.g.
+            # CTA pairs on a gathered stem, fails here rather than at launch)
+            if kind == "conv":
+                kernels.conv_gemm_plan(a)
+            else:
+                kernels._lib.check(kernels._lib.load().abft_gemm_plan(kernels.ctypes.byref(a),
+                                                                       (kernels.ctypes.c_int32 * 10)()))
+            L.args[key] = (kind, a)
         except Exception:
             L.tile_n[key], L.flags[key] = old
             raise

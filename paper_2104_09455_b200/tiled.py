@@ -112,7 +112,7 @@ def _thread_verdicts(raw: np.ndarray, exact: bool) -> tuple:
 
 def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme.UNPROTECTED,
             faults: Sequence[FaultSpec] = (), dtype: DType | None = None, *, ck_split: bool = True,
-            tile_n: int = 0, ck_source: str = "auto") -> ExecutionReport:
+            tile_n: int = 0, ck_source: str = "auto", plan_flags: int = 0) -> ExecutionReport:
     """Run the protected GEMM under ``scheme`` with optional injected faults.
 
     Output is fp32 (int64 in exact-int mode) and identical across schemes for
@@ -157,7 +157,8 @@ def execute(a, b, tiling: TilingConfig = TilingConfig(), scheme: Scheme = Scheme
     split = ck_split and not dtype.is_exact
     call = dict(out=out, ldc=n, out_kind="f32", thread_m=tiling.thread_m, thread_n=tiling.thread_n,
                 m_ext=padded.m, n_ext=padded.n, tol_k=padded.k, faults=f_dev, nfaults=nf,
-                out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, out_lhs=out_lhs)
+                out_sum=out_sum, verdicts=verdicts, ck_split=split, tile_n=tile_n, out_lhs=out_lhs,
+                plan_flags=plan_flags)
     ckr = None
     # checksum rows of the weights: appended to each weight tile ("aug": one MMA per k-step),
     # as separate rows ("offline": their own MMA slice) or generated on chip ("onchip").

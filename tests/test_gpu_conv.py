@@ -239,3 +239,26 @@ def test_gathered_stem_copy_depths_bit_exact(P, depth):
     assert np.array_equal(rep.output.reshape(cols.shape[0], oc), out)
     v, rv = rep.verdicts[0], verdicts[0]
     assert (v.detected, v.lhs, v.rhs) == (rv.detected, rv.lhs, rv.rhs)
+
+
+@pytest.mark.parametrize("n,h,w,c,ld", [(3, 28, 28, 512, 512), (5, 1, 7, 64, 72), (2, 2, 1, 8, 8), (4, 56, 56, 64, 64),
+                                        (7, 13, 9, 24, 32), (1, 224, 224, 64, 64)])
+def test_border_sums_buckets(n, h, w, c, ld):
+    """abft_nhwc_border_sums: buckets 1..8 (rows 0 / H-1, columns 0 / W-1, the four corners) of the
+    activation's border pixels, accumulated onto wsum (bucket 0 untouched), against fp64 sums."""
+    import torch
+    from paper_2104_09455_b200 import BINARY16, kernels
+    g = torch.Generator(device="cuda").manual_seed(n * h + w)
+    x = (torch.rand((n, h, w, ld), generator=g, device="cuda") * 2 - 1).half()
+    wsum = torch.ones((9, c + 8), dtype=torch.float32, device="cuda")
+    kernels.border_sums(x, n, h, w, c, ld, BINARY16, wsum, c + 8)
+    torch.cuda.synchronize()
+    xd = x[..., :c].double()
+    want = [xd[:, 0].sum((0, 1)), xd[:, -1].sum((0, 1)), xd[:, :, 0].sum((0, 1)), xd[:, :, -1].sum((0, 1)),
+            xd[:, 0, 0].sum(0), xd[:, 0, -1].sum(0), xd[:, -1, 0].sum(0), xd[:, -1, -1].sum(0)]
+    got = wsum.double()
+    assert torch.equal(got[0], torch.ones_like(got[0]))
+    for b, ref in enumerate(want):
+        err = (got[b + 1, :c] - 1.0 - ref).abs().max().item()
+        assert err <= 1e-5 * (1 + n * max(h, w)), (b + 1, err)
+        assert torch.equal(got[b + 1, c:], torch.ones_like(got[b + 1, c:]))

@@ -308,3 +308,53 @@ def test_per_tap_im2col_plan_flag(PN, name):
     net.forward(x)
     assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [T.index]
     net.inject({})
+
+
+@pytest.mark.parametrize("name", ["vgg16", "resnet50"])
+def test_cta_pair_plans_in_network(PN, name):
+    """CTA pairs (plan_flags bit 12) on every layer whose unprotected / global-slice launch takes
+    them (3x3 stride-1 convs through per-tap im2col, bit 11): layers match the fp32 checker, clean
+    runs flag nothing, and a fault in a paired layer is flagged there only."""
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model(name), 2)
+    x = _input(2, seed=7)
+    paired = {S.UNPROTECTED: [], S.GLOBAL_ABFT: []}
+    for L in net.layers:
+        for key in paired:
+            try:
+                net.set_tile(L, key, 0, 4096 | 2048)
+                paired[key].append(L)
+            except Exception:      # noqa: BLE001 — a plan the pairs do not take (stems, strided, thin)
+                pass
+    assert len(paired[S.UNPROTECTED]) >= 8 and len(paired[S.GLOBAL_ABFT]) >= 8, \
+        {k.value: [L.name for L in v] for k, v in paired.items()}
+    for scheme in paired:
+        net.set_schemes(scheme)
+        net.forward(x)
+        torch.cuda.synchronize()
+        assert net.flags() == (0, 0), scheme
+        for L in net.layers:
+            check_layer(L)
+        if scheme is S.GLOBAL_ABFT:
+            vs = net.verdicts()
+            assert all(not v.detected and abs(v.lhs - v.rhs) < 0.05 * v.tolerance_used for v in vs)
+    T = [L for L in paired[S.GLOBAL_ABFT] if L.k_ref <= 600][-1]
+    tau = net.verdicts()[T.index].tolerance_used
+    net.inject({T.index: [(T.m // 3, 1, 8.0 * tau + 64.0)]})
+    net.forward(x)
+    assert [i for i, v in enumerate(net.verdicts()) if v.detected] == [T.index]
+    net.inject({})
+    # fused consumers: paired producers accumulate window sums in their epilogues
+    for L in net.layers:
+        if L.producer is not None:
+            net.set_tile(L, PN.GLOBAL_FUSED, 0, 4096 | 2048) if L in paired[S.GLOBAL_ABFT] else None
+            net.set_global_variant(L, "fused")
+    assert any(P.ws_active and P in paired[S.UNPROTECTED] for P in net.producers() if isinstance(P, PN.LinearLayer))
+    net.forward(x)
+    torch.cuda.synchronize()
+    assert net.flags() == (0, 0)
+    vs = net.verdicts()
+    for L in net.layers:
+        check_layer(L)
+        assert not vs[L.index].detected and abs(vs[L.index].lhs - vs[L.index].rhs) < 0.05 * vs[L.index].tolerance_used

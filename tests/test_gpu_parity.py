@@ -327,3 +327,31 @@ def test_kblock_pairs_match_single_kblock_stages(P, monkeypatch, scheme, m, n, k
         rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults)
         assert np.array_equal(rep.output, out_ref), kp
         assert rep.detected == any(v.detected for v in v_ref), kp
+
+
+@pytest.mark.parametrize("scheme", ["unprotected", "global-abft"])
+@pytest.mark.parametrize("m,n,k", [(700, 300, 200), (300, 256, 1000), (2048, 64, 576), (130, 120, 136),
+                                   (1, 512, 13), (4096, 512, 320)])
+def test_cta_pairs_match_oracle(P, scheme, m, n, k):
+    """CTA pairs (plan_flags bit 12): 2-CTA clusters running one M = 256 cta_group::2 MMA per
+    k-step, each CTA staging its own 128 A rows and half of the B rows (odd M-block counts end with
+    an out-of-range tile).  Exact-int outputs and global verdicts equal the oracle's, with a fault;
+    binary16 outputs equal the single-CTA kernel's."""
+    rng = np.random.default_rng(m + 5 * n + k)
+    a = rng.integers(-8, 9, size=(m, k), dtype=np.int64)
+    b = rng.integers(-8, 9, size=(k, n), dtype=np.int64)
+    fr = [("output", m - 1, n // 2, 5)] if scheme != "unprotected" else []
+    out_ref, v_ref = O.execute(a, b, O.Tiling(), scheme, fr)
+    faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
+    rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults, plan_flags=4096)
+    assert np.array_equal(rep.output, out_ref)
+    if scheme == "global-abft":
+        v = rep.verdicts[0]
+        assert (v.detected, v.lhs, v.rhs) == (v_ref[0].detected, v_ref[0].lhs, v_ref[0].rhs)
+        assert v.detected
+    af = rng.uniform(-1, 1, size=(m, k)).astype(np.float16)
+    bf = rng.uniform(-1, 1, size=(k, n)).astype(np.float16)
+    r1 = P.execute(af, bf, P.TilingConfig(), P.Scheme(scheme), plan_flags=4096)
+    r0 = P.execute(af, bf, P.TilingConfig(), P.Scheme(scheme))
+    assert np.allclose(np.asarray(r1.output), np.asarray(r0.output), rtol=1e-5, atol=1e-5)
+    assert r1.detected is False
