@@ -511,7 +511,8 @@ __device__ __forceinline__ void lean_store_row(const float (&v)[32], void* C, in
 // AM: the A-load family of the instance — 0 TMA tiles / im2col boxes (a_mode 0-2), 1 halo
 // windows (a_mode 4), 2 gathered stems (a_mode 5), 3 CTA pairs over TMA tiles / 64-channel im2col
 // boxes (a_mode 0-1; plain class): 2-CTA clusters, one M = 256 cta_group::2 MMA per k-step issued
-// by the leader, each CTA staging its 128 A rows and half of the B rows
+// by the leader, each CTA staging its 128 A rows and half of the B rows; 4 CTA pairs over halo
+// windows (a_mode 4)
 // WS: the instance accumulates window sums of its output (a producer of fused consumers); kept out
 // of the other instances, whose epilogue loops would otherwise spill
 template <typename T, int CLASS, int NT, int AM, bool WS>
@@ -566,9 +567,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool ck_aug = p.ck_mode == 3 || p.ck_mode == 4;
   // halo-reuse conv (a_mode 4) and its weight-stationary B exist only in the HALO instances,
   // keeping the GEMM instances' hot loops free of them
-  constexpr bool HALO = AM == 1;
+  constexpr bool HALO = AM == 1 || AM == 4;
   constexpr bool gather = AM == 2;
-  constexpr bool PAIR = AM == 3;
+  constexpr bool PAIR = AM == 3 || AM == 4;
   const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0u;
   const bool halo = HALO && p.a_mode == 4;
   const bool b_res = (HALO || gather) && p.b_resident;
@@ -673,13 +674,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (b_res && blockIdx.x < L_num_tiles) {
         // weight-stationary: the single N-block's B for every k-block (and, in halo mode, every
         // tap of the k-block's filter row), loaded once per CTA
-        ptx::mbar_arrive_expect_tx_w(bres, (uint32_t)L_nkb * (halo ? (uint32_t)L_cv_S : 1u) * L_tx_b);
+        const uint32_t bres_tx = (uint32_t)L_nkb * (halo ? (uint32_t)L_cv_S : 1u) * L_tx_b;
+        // (a pair: each CTA its half of the rows, both on the leader's barrier)
+        if (!PAIR) ptx::mbar_arrive_expect_tx_w(bres, bres_tx);
+        else if (crank == 0) ptx::mbar_arrive_expect_tx_w2(bres, 2u * bres_tx);
+        const uint32_t bres_cl = PAIR ? ptx::mapa_shared(ptx::smem_u32(bres), 0) : 0u;
         for (int kb = 0; kb < L_nkb; ++kb) {
           if (halo) {
             const int r = kb / L_cv_chunks, cc = kb - (kb / L_cv_chunks) * L_cv_chunks;
-            for (int si = 0; si < L_cv_S; ++si)
-              ptx::tma_load_2d_w(sm_b + kb * L_stage_b_bytes + si * L_b_tile_bytes, &tmB, bres,
-                               (r * L_cv_S + si) * L_cv_kstride + cc * BK, 0);
+            for (int si = 0; si < L_cv_S; ++si) {
+              uint8_t* bdst = sm_b + kb * L_stage_b_bytes + si * L_b_tile_bytes;
+              const int kx = (r * L_cv_S + si) * L_cv_kstride + cc * BK;
+              if constexpr (PAIR) ptx::tma_load_2d_w2(bdst, &tmB, bres_cl, kx, (int)crank * p.b_half);
+              else ptx::tma_load_2d_w(bdst, &tmB, bres, kx, 0);
+            }
           } else {
             ptx::tma_load_2d_w(sm_b + kb * L_stage_b_bytes, &tmB, bres, kb * BK, 0);
           }
@@ -729,7 +737,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (PAIR) {
           // CTA pair: this CTA's 128 A rows and its half of the B rows, both completing on the
           // leader's full barrier, which expects the pair's bytes
-          const uint32_t tx2 = 2u * (L_stage_a_bytes + L_tx_b);
+          const uint32_t tx2 = 2u * (halo ? p.tx_a + (b_res ? 0u : (uint32_t)L_cv_S * L_tx_b)
+                                          : L_stage_a_bytes + L_tx_b);
           const int brow = (ck_aug ? nb * L_b_rows_blk : n0) + (int)crank * p.b_half;
 #pragma unroll 1
           for (int kb = 0; kb < L_nkb; ++kb) {
@@ -737,6 +746,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (crank == 0) ptx::mbar_arrive_expect_tx_w2(&full[s], tx2);
             const uint32_t fb = ptx::mapa_shared(ptx::smem_u32(&full[s]), 0);
             uint8_t* a_dst = sm_a + s * L_stage_a_bytes;
+            if (halo) {
+              // this CTA's input-row window (its Qt output pixels + S - 1 halo pixels)
+              const int r = kb / L_cv_chunks;
+              const int cc = kb - r * L_cv_chunks;
+              ptx::tma_load_im2col_4d_w2(a_dst, &tmA, fb, cc * BK, wo, ho + r, img, 0, 0);
+              if (!b_res) {
+#pragma unroll 1
+                for (int si = 0; si < L_cv_S; ++si)
+                  ptx::tma_load_2d_w2(sm_b + s * L_stage_b_bytes + si * L_b_tile_bytes, &tmB, fb,
+                                      (r * L_cv_S + si) * L_cv_kstride + cc * BK, brow);
+              }
+              if (++s == L_stages) { s = 0; ph ^= 1; }
+              continue;
+            }
             if (L_a_mode == 0) {
               ptx::tma_load_2d_w2(a_dst, &tmA, fb, kb * BK, m0);
             } else {
@@ -853,10 +876,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4;
         const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
         const int L_nkb = p.nkb, L_stages = p.stages, L_acc_stages = p.acc_stages, L_cols = p.cols_per_acc;
-        const int L_num_tiles = p.num_tiles;
+        const int L_num_tiles = p.num_tiles, L_cv_S = p.cv_S;
+        const uint64_t b_tstep = p.b_tile_bytes >> 4;
         int s = 0;
         uint32_t ph = 0;
         int t_local = 0;
+        if (b_res && blockIdx.x < L_num_tiles) ptx::mbar_wait(bres, 0);
         for (int tile = blockIdx.x; tile < L_num_tiles; tile += gridDim.x, ++t_local) {
           const int acc = t_local % L_acc_stages;
           const uint32_t aph = (uint32_t)(t_local / L_acc_stages) & 1u;
@@ -868,11 +893,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
             const uint64_t ad = a_base + (uint64_t)s * a_sstep;
-            const uint64_t bd = b_base + (uint64_t)s * b_sstep;
+            const uint64_t bd = b_base + (uint64_t)(b_res ? kb : s) * b_sstep;
             if (ptx::elect_one()) {
+              if (halo) {
+                // the S taps of this filter row: A = the window shifted by si rows (both CTAs' windows
+                // at the same offsets), B = tap si's tile
+#pragma unroll 1
+                for (int si = 0; si < L_cv_S; ++si) {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
+                  for (int k = 0; k < BK / 16; ++k)
+                    ptx::mma_f16_ss2(d, ad + 8ull * (uint64_t)si + 2ull * k, bd + b_tstep * (uint64_t)si + 2ull * k,
+                                     idesc_m, (kb | si | k) != 0 ? 1u : 0u);
+                }
+              } else {
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
+              }
               ptx::mma_commit2_mc(&empty[s], 3);
             }
             __syncwarp();
@@ -2331,6 +2368,10 @@ int launch_typed(int cls, int ntc, const CUtensorMap& ma, const CUtensorMap& mb,
                  const CUtensorMap& mo, const CUtensorMap& mo2, const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
   if (p.pair) {
     if (cls != CLASS_PLAIN) return fail(ABFT_E_UNSUPPORTED, "CTA pairs: plain class only");
+    if (p.a_mode == 4) {
+      if (p.wsum != nullptr) return launch_inst<T, CLASS_PLAIN, 0, 4, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+      return launch_inst<T, CLASS_PLAIN, 0, 4, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
+    }
     if (p.wsum != nullptr) return launch_inst<T, CLASS_PLAIN, 0, 3, true>(ma, mb, mc, mo, mo2, p, smem, grid, st);
     return launch_inst<T, CLASS_PLAIN, 0, 3, false>(ma, mb, mc, mo, mo2, p, smem, grid, st);
   }
@@ -2622,13 +2663,13 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // CTA pairs (plan_flags bit 12): 2-CTA clusters, M = 256 per MMA, each CTA staging half of
     // the B rows; the plain-class paths over TMA tiles / 64-channel im2col boxes only
     const int n_mma = p.ck_mode == 3 ? bn + p.nck_pad : bn;
-    if (halo || gather || (cg != nullptr && cg->a_mode == 2) || out.cls != CLASS_PLAIN ||
+    if (gather || (cg != nullptr && cg->a_mode == 2) || out.cls != CLASS_PLAIN ||
         p.lhs_w != nullptr || want_acolck || (p.ck_mode != 0 && p.ck_mode != 3) || n_mma % 16 != 0)
       return fail(ABFT_E_UNSUPPORTED, "CTA pairs: plain / global-slice GEMMs and 64-channel im2col convs only");
     p.pair = 1;
     p.b_half = n_mma / 2;
-    p.stage_b_bytes = (uint32_t)round_up(p.b_half * BK * 2, 1024);
-    p.b_tile_bytes = p.stage_b_bytes;
+    p.b_tile_bytes = (uint32_t)round_up(p.b_half * BK * 2, 1024);
+    p.stage_b_bytes = p.b_tile_bytes * (uint32_t)(halo ? cg->S : 1);
     p.tx_b = (uint32_t)p.b_half * BK * 2;
     p.idesc_main = ptx::idesc_f16(fmt, 2 * BM, bn);
     p.idesc_aug = ptx::idesc_f16(fmt, 2 * BM, (uint32_t)n_mma);

@@ -262,3 +262,27 @@ def test_border_sums_buckets(n, h, w, c, ld):
         err = (got[b + 1, :c] - 1.0 - ref).abs().max().item()
         assert err <= 1e-5 * (1 + n * max(h, w)), (b + 1, err)
         assert torch.equal(got[b + 1, c:], torch.ones_like(got[b + 1, c:]))
+
+
+@pytest.mark.parametrize("case", [(2, 9, 64, 64, 64, 3, 3, 1, 1),       # halo windows, Qt = 64, N = 64
+                                  (3, 6, 112, 64, 128, 3, 3, 1, 1),     # Qt = 112 (partial quadrant), N = 128
+                                  (1, 5, 80, 128, 96, 3, 3, 1, 1),      # two 64-channel chunks, odd tile count
+                                  (2, 11, 13, 64, 200, 3, 3, 1, 1),     # no halo tile: per-tap im2col
+                                  (2, 12, 12, 64, 48, 1, 1, 1, 0)])     # pointwise
+@pytest.mark.parametrize("flags", [4096, 4096 | 2048])
+def test_conv_cta_pairs_exact(P, case, flags):
+    """CTA pairs on the conv A-load modes (halo windows with resident or streamed weights, per-tap
+    im2col, pointwise): exact-int outputs and global verdicts equal the oracle's, faults flagged."""
+    n, h, w, c, oc, r, s, st, pd = case
+    x, wt, cols, wmat = _data(case, exact=True, seed=8)
+    m = cols.shape[0]
+    for scheme in ("unprotected", "global-abft"):
+        fr = [("output", m - 1, oc - 1, 6), ("output", 3, oc // 2, -2)] if scheme != "unprotected" else []
+        faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
+        rep = P.conv2d(x, wt, stride=st, padding=pd, scheme=P.Scheme(scheme), faults=faults, plan_flags=flags)
+        out, verdicts = O.execute(cols, wmat, O.Tiling(), scheme, fr)
+        assert np.array_equal(rep.output.reshape(m, oc), out), (case, flags, scheme)
+        if scheme == "global-abft":
+            v, rv = rep.verdicts[0], verdicts[0]
+            assert (v.detected, v.lhs, v.rhs) == (rv.detected, rv.lhs, rv.rhs)
+            assert v.detected
