@@ -381,6 +381,9 @@ def main():
               key=lambda p: p[0]["meas"].get(p[1].index, p[1].scheme))
     de, dL = dom
     dom_us = profiler.graph_time_us(lambda: de["net"].launch(dL), 10)
+    dkey = de["net"]._key(dL, dL.scheme)
+    dtile, dflags = de["net"].config_of(dL, dkey)
+    dvar = dL.gvar if dL.scheme is PN.Scheme.GLOBAL_ABFT else "-"
     dflops, dbytes = dL.flops(), dL.bytes()
     cmr = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
     if dflops / dbytes < cmr:
@@ -395,10 +398,12 @@ def main():
         dj = json.load(open(dpath))
         c = dj.get("config", {})
         if (c.get("net"), c.get("layer"), c.get("batch"), c.get("scheme")) == (de["name"], dL.name, lb,
-                                                                              dL.scheme.value):
+                                                                              dL.scheme.value) and \
+                c.get("flags", dflags) == dflags and c.get("variant", dvar) == dvar:
             roof["traffic"] = dj["dram_bytes_read"] + dj["dram_bytes_write"]
             roof["traffic_source"] = dj["source"]
     roof["kernel"] = (f"abft_gemm_kernel {de['name']} {dL.name} {dL.scheme.value} M={dL.m} N={dL.oc} K={dL.k_ref}, "
+                      f"plan variant={dvar} tile_n={dtile} flags={dflags}, "
                       f"{dom_us:.1f} us/launch, algorithmic {dflops / 1e9:.1f} GFLOP / {dbytes / 1e6:.1f} MB")
     roof["peak_source"] = peak_src
 

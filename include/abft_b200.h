@@ -193,6 +193,23 @@ int abft_nhwc_border_sums(const void* x, int32_t n, int32_t h, int32_t w, int32_
 int abft_window_lhs(const float* wsum, int32_t ws_ld, int32_t C, int32_t R, int32_t S, int32_t ck,
                     const float* rowck, const float* bias, int32_t n_out, int64_t M, double* lhs, void* stream);
 
+/* The two calls above for a whole forward in two launches: every producer's border buckets, then
+ * every fused consumer's window lhs (tasks = the calls' arguments).  _prepare validates the tasks
+ * and writes the device table (16-byte aligned, abft_fused_lhs_batch_bytes) synchronously, once;
+ * grids[2] (out) = the two launches' CTA counts; _launch is stream-ordered and graph-capturable.
+ * The activations must still hold the producers' outputs when the batch runs. */
+typedef struct {
+  const void* x; float* wsum; int64_t ldx; int32_t n, h, w, c, ws_ld;
+} abft_border_task_t;
+typedef struct {
+  const float* wsum; const float* rowck; const float* bias; double* lhs; int64_t M;
+  int32_t ws_ld, C, R, S, ck, n_out;
+} abft_window_task_t;
+int64_t abft_fused_lhs_batch_bytes(int32_t n_border, int32_t n_window);
+int abft_fused_lhs_batch_prepare(const abft_border_task_t* border, int32_t n_border, const abft_window_task_t* window,
+                                 int32_t n_window, void* table, int64_t table_bytes, int32_t* grids);
+int abft_fused_lhs_batch_launch(const void* table, const int32_t* grids, int32_t dtype, void* stream);
+
 /* The kernel configuration abft_gemm would use for `args` (no launch):
  * out[0] tile_n, [1] bn_eff, [2] checksum groups per tile, [3] nck_pad, [4] pipeline stages,
  * [5] 1 if offline checksum rows are recommended (B tiles re-read by > 2 M-blocks),

@@ -56,6 +56,9 @@ EXPORTED_SYMBOLS = (
     "abft_nhwc_avgpool",
     "abft_nhwc_interleave2",
     "abft_sum_partials",
+    "abft_fused_lhs_batch_bytes",
+    "abft_fused_lhs_batch_prepare",
+    "abft_fused_lhs_batch_launch",
 )
 
 
@@ -79,6 +82,20 @@ class VerdictC(ctypes.Structure):
 class ThreadVerdictC(ctypes.Structure):
     _fields_ = [("t_row", ctypes.c_int32), ("t_col", ctypes.c_int32), ("detected", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("max_abs_diff", ctypes.c_double), ("tol", ctypes.c_double)]
+
+
+class BorderTask(ctypes.Structure):
+    """abft_border_task_t: one producer's border buckets (abft_nhwc_border_sums arguments)."""
+    _fields_ = [("x", ctypes.c_void_p), ("wsum", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+                ("n", ctypes.c_int32), ("h", ctypes.c_int32), ("w", ctypes.c_int32), ("c", ctypes.c_int32),
+                ("ws_ld", ctypes.c_int32)]
+
+
+class WindowTask(ctypes.Structure):
+    """abft_window_task_t: one fused consumer's window lhs (abft_window_lhs arguments)."""
+    _fields_ = [("wsum", ctypes.c_void_p), ("rowck", ctypes.c_void_p), ("bias", ctypes.c_void_p),
+                ("lhs", ctypes.c_void_p), ("M", ctypes.c_int64), ("ws_ld", ctypes.c_int32), ("C", ctypes.c_int32),
+                ("R", ctypes.c_int32), ("S", ctypes.c_int32), ("ck", ctypes.c_int32), ("n_out", ctypes.c_int32)]
 
 
 class GemmArgs(ctypes.Structure):
@@ -158,6 +175,8 @@ def _declare(lib):
         fn = getattr(lib, name)
         if name != "abft_last_error":
             fn.restype = ctypes.c_int
+    lib.abft_fused_lhs_batch_bytes.restype = ctypes.c_int64
+    lib.abft_fused_lhs_batch_bytes.argtypes = [i32, i32]
     return lib
 
 

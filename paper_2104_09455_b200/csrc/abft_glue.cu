@@ -11,6 +11,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <string>
+#include <vector>
 
 #include "abft_common.cuh"
 
@@ -334,17 +336,16 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
 // group's segment pixels) keeps ONE 8-float accumulator, with up to 8 loads in flight.  The CTA's
 // slices meet in shared memory and leave as one 16-byte atomic per 4 channels.  Bucket 0 (all
 // pixels) comes from the producer's epilogue.
+// one CTA of the border pass: bucket `bucket`, images [grp * imgs_per_cta, ...); bsm >= parts * C floats
 template <typename T>
-__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, int nimg, int imgs_per_cta, int H,
-                                                          int W, int C, long long ldx, float* __restrict__ ws,
-                                                          int ws_ld) {
-  extern __shared__ float bsm[];           // [parts][C]
-  const int bucket = 1 + (int)blockIdx.y;
+__device__ __forceinline__ void border_block(const T* __restrict__ x, int nimg, int imgs_per_cta, int H, int W, int C,
+                                             long long ldx, float* __restrict__ ws, int ws_ld, int bucket, int grp,
+                                             float* bsm) {
   const int cv = C / 8;
-  const int parts = blockDim.x / cv;
+  const int parts = 256 / cv;
   const int c8 = threadIdx.x % cv, part = threadIdx.x / cv;
   const int seg = bucket <= 2 ? W : (bucket <= 4 ? H : 1);      // pixels per image
-  const int img0 = blockIdx.x * imgs_per_cta;
+  const int img0 = grp * imgs_per_cta;
   const int nimg_cta = min(imgs_per_cta, nimg - img0);
   const int items = nimg_cta * seg;
   auto pixel = [&](int it) -> long long {
@@ -400,6 +401,21 @@ __global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ 
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) border_sums_kernel(const T* __restrict__ x, int nimg, int imgs_per_cta, int H,
+                                                          int W, int C, long long ldx, float* __restrict__ ws,
+                                                          int ws_ld) {
+  __shared__ __align__(16) float bsm[2048];     // [parts][C]: parts * C = 256 / (C / 8) * C <= 2048
+  border_block<T>(x, nimg, imgs_per_cta, H, W, C, ldx, ws, ws_ld, 1 + (int)blockIdx.y, (int)blockIdx.x, bsm);
+}
+
+// images per CTA of the border pass: ~16 segment pixels per thread slot of the longest buckets
+static int border_imgs_per_cta(int n, int h, int w, int c) {
+  const int parts = 256 / (c / 8);
+  const int seg = std::max(h, w);
+  return std::max(1, std::min(n, (16 * parts + seg - 1) / seg));
+}
+
 extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(const void* x, int32_t n, int32_t h,
                                                                            int32_t w, int32_t c, int64_t ldx,
                                                                            int32_t dtype, float* wsum, int32_t ws_ld,
@@ -408,20 +424,13 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(cons
       ws_ld % 4 || (reinterpret_cast<uintptr_t>(wsum) & 15))
     return fail(ABFT_E_SHAPE, "border_sums: bad extents (channels a multiple of 8 up to 1024, ldx >= c, "
                               "16-byte aligned wsum rows)");
-  const int cv = c / 8;
-  const int parts = 256 / cv;
-  const int threads = parts * cv;
-  const size_t smem = (size_t)parts * c * sizeof(float);
-  // images per CTA: ~16 segment pixels per thread slot of the longest (row / column) buckets
-  const int seg = std::max(h, w);
-  const int ipc = std::max(1, std::min(n, (16 * parts + seg - 1) / seg));
+  const int ipc = border_imgs_per_cta(n, h, w, c);
   const dim3 grid((unsigned)((n + ipc - 1) / ipc), 8u);
   cudaStream_t st = as_stream(stream);
   if (dtype == ABFT_BF16)
-    border_sums_kernel<__nv_bfloat16><<<grid, threads, smem, st>>>((const __nv_bfloat16*)x, n, ipc, h, w, c, ldx, wsum,
-                                                                   ws_ld);
+    border_sums_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, n, ipc, h, w, c, ldx, wsum, ws_ld);
   else
-    border_sums_kernel<__half><<<grid, threads, smem, st>>>((const __half*)x, n, ipc, h, w, c, ldx, wsum, ws_ld);
+    border_sums_kernel<__half><<<grid, 256, 0, st>>>((const __half*)x, n, ipc, h, w, c, ldx, wsum, ws_ld);
   return cuda_check(cudaGetLastError(), "border_sums launch");
 }
 
@@ -431,14 +440,13 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_border_sums(cons
 // input rows / columns tap (r, s) reads: all of them minus the row the tap never reaches (r = 0
 // misses the last row, r = 2 the first) minus the column likewise, plus their corner (counted
 // twice).  Buckets: 0 all, 1 p0, 2 pL, 3 q0, 4 qL, 5 (p0,q0), 6 (p0,qL), 7 (pL,q0), 8 (pL,qL).
-__global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict__ ws, int ld, int C, int R, int S,
-                                                         int ck, const float* __restrict__ rowck,
-                                                         const float* __restrict__ bias, int n_out, long long M,
-                                                         double* __restrict__ lhs) {
-  __shared__ double red[8];
+__device__ __forceinline__ void window_block(const float* __restrict__ ws, int ld, int C, int R, int S, int ck,
+                                             const float* __restrict__ rowck, const float* __restrict__ bias,
+                                             int n_out, long long M, double* __restrict__ lhs, int blk, int nblk,
+                                             double* red) {
   double acc = 0.0;
   const int taps = R * S;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < taps * C; i += gridDim.x * blockDim.x) {
+  for (int i = blk * blockDim.x + threadIdx.x; i < taps * C; i += nblk * blockDim.x) {
     const int tap = i / C, c = i - (i / C) * C;
     double col = ws[c];
     if (R == 3) {
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict
     }
     acc += col * (double)rowck[(long long)tap * ck + c];
   }
-  if (bias != nullptr && blockIdx.x == 0)
+  if (bias != nullptr && blk == 0)
     for (int j = threadIdx.x; j < n_out; j += blockDim.x) acc += (double)M * (double)bias[j];
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -462,6 +470,58 @@ __global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
     atomicAdd(lhs, t);
   }
+}
+
+__global__ void __launch_bounds__(256) window_lhs_kernel(const float* __restrict__ ws, int ld, int C, int R, int S,
+                                                         int ck, const float* __restrict__ rowck,
+                                                         const float* __restrict__ bias, int n_out, long long M,
+                                                         double* __restrict__ lhs) {
+  __shared__ double red[8];
+  window_block(ws, ld, C, R, S, ck, rowck, bias, n_out, M, lhs, (int)blockIdx.x, (int)gridDim.x, red);
+}
+
+// ---- batched fused-checksum work of a whole forward (abft_fused_lhs_batch_*): every producer's
+// border buckets in ONE launch, then every fused consumer's window lhs in ONE launch, from a
+// device table written once (the activations stay live until the end of the forward)
+struct __align__(16) BorderEntry {
+  const void* x;
+  float* ws;
+  long long ldx;
+  int n, h, w, c, ws_ld, ipc, groups, begin;
+  int pad[3];
+};
+struct __align__(16) WindowEntry {
+  const float* ws;
+  const float* rowck;
+  const float* bias;
+  double* lhs;
+  long long M;
+  int ld, C, R, S, ck, n_out, begin, nblk;
+};
+struct __align__(16) FusedBatchHeader {
+  int nb, nw, border_blocks, window_blocks;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) border_batch_kernel(const FusedBatchHeader* __restrict__ hdr) {
+  __shared__ __align__(16) float bsm[2048];
+  const BorderEntry* e = reinterpret_cast<const BorderEntry*>(hdr + 1);
+  int i = 0;
+  while (i + 1 < hdr->nb && (int)blockIdx.x >= e[i + 1].begin) ++i;
+  const BorderEntry& t = e[i];
+  const int local = (int)blockIdx.x - t.begin;
+  border_block<T>(reinterpret_cast<const T*>(t.x), t.n, t.ipc, t.h, t.w, t.c, t.ldx, t.ws, t.ws_ld,
+                  1 + local / t.groups, local % t.groups, bsm);
+}
+
+__global__ void __launch_bounds__(256) window_batch_kernel(const FusedBatchHeader* __restrict__ hdr) {
+  __shared__ double red[8];
+  const WindowEntry* e = reinterpret_cast<const WindowEntry*>(reinterpret_cast<const BorderEntry*>(hdr + 1) + hdr->nb);
+  int i = 0;
+  while (i + 1 < hdr->nw && (int)blockIdx.x >= e[i + 1].begin) ++i;
+  const WindowEntry& t = e[i];
+  window_block(t.ws, t.ld, t.C, t.R, t.S, t.ck, t.rowck, t.bias, t.n_out, t.M, t.lhs, (int)blockIdx.x - t.begin,
+               t.nblk, red);
 }
 
 extern "C" __attribute__((visibility("default"))) int abft_window_lhs(const float* wsum, int32_t ws_ld, int32_t C,
@@ -476,6 +536,74 @@ extern "C" __attribute__((visibility("default"))) int abft_window_lhs(const floa
   const int grid = std::max(1, std::min(64, (R * S * C + 255) / 256));
   window_lhs_kernel<<<grid, 256, 0, as_stream(stream)>>>(wsum, ws_ld, C, R, S, ck, rowck, bias, n_out, M, lhs);
   return cuda_check(cudaGetLastError(), "window_lhs launch");
+}
+
+extern "C" __attribute__((visibility("default"))) int64_t abft_fused_lhs_batch_bytes(int32_t n_border,
+                                                                                     int32_t n_window) {
+  return (int64_t)sizeof(FusedBatchHeader) + (int64_t)n_border * (int64_t)sizeof(BorderEntry) +
+         (int64_t)n_window * (int64_t)sizeof(WindowEntry);
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_fused_lhs_batch_prepare(
+    const abft_border_task_t* bt, int32_t nb, const abft_window_task_t* wt, int32_t nw, void* table,
+    int64_t table_bytes, int32_t* grids) {
+  if (nb < 0 || nw < 0 || (nb > 0 && bt == nullptr) || (nw > 0 && wt == nullptr) || table == nullptr ||
+      grids == nullptr || (reinterpret_cast<uintptr_t>(table) & 15))
+    return fail(ABFT_E_VALUE, "fused_lhs_batch: bad arguments (16-byte aligned device table)");
+  if (table_bytes < abft_fused_lhs_batch_bytes(nb, nw)) return fail(ABFT_E_SHAPE, "fused_lhs_batch: table too small");
+  std::vector<uint8_t> host((size_t)abft_fused_lhs_batch_bytes(nb, nw), 0);
+  auto* hdr = reinterpret_cast<FusedBatchHeader*>(host.data());
+  auto* be = reinterpret_cast<BorderEntry*>(hdr + 1);
+  auto* we = reinterpret_cast<WindowEntry*>(be + nb);
+  int blocks = 0;
+  for (int i = 0; i < nb; ++i) {
+    const abft_border_task_t& t = bt[i];
+    if (t.n < 1 || t.h < 1 || t.w < 1 || t.c < 8 || t.c % 8 || t.c > 1024 || t.ldx < t.c || t.ldx % 8 ||
+        t.wsum == nullptr || t.x == nullptr || t.ws_ld < t.c || t.ws_ld % 4 || (reinterpret_cast<uintptr_t>(t.wsum) & 15))
+      return fail(ABFT_E_SHAPE, "fused_lhs_batch: bad border task " + std::to_string(i));
+    BorderEntry& e = be[i];
+    e.x = t.x; e.ws = t.wsum; e.ldx = t.ldx; e.n = t.n; e.h = t.h; e.w = t.w; e.c = t.c; e.ws_ld = t.ws_ld;
+    e.ipc = border_imgs_per_cta(t.n, t.h, t.w, t.c);
+    e.groups = (t.n + e.ipc - 1) / e.ipc;
+    e.begin = blocks;
+    blocks += 8 * e.groups;
+  }
+  hdr->nb = nb; hdr->border_blocks = blocks;
+  int wblocks = 0;
+  for (int i = 0; i < nw; ++i) {
+    const abft_window_task_t& t = wt[i];
+    if (t.wsum == nullptr || t.rowck == nullptr || t.lhs == nullptr || !((t.R == 1 && t.S == 1) || (t.R == 3 && t.S == 3)) ||
+        t.C < 1 || t.ws_ld < t.C || t.ck < t.C || t.M < 0 || (t.bias != nullptr && t.n_out < 1))
+      return fail(ABFT_E_SHAPE, "fused_lhs_batch: bad window task " + std::to_string(i));
+    WindowEntry& e = we[i];
+    e.ws = t.wsum; e.rowck = t.rowck; e.bias = t.bias; e.lhs = t.lhs; e.M = t.M; e.ld = t.ws_ld; e.C = t.C;
+    e.R = t.R; e.S = t.S; e.ck = t.ck; e.n_out = t.n_out;
+    e.nblk = std::max(1, std::min(64, (t.R * t.S * t.C + 255) / 256));
+    e.begin = wblocks;
+    wblocks += e.nblk;
+  }
+  hdr->nw = nw; hdr->window_blocks = wblocks;
+  grids[0] = blocks; grids[1] = wblocks;
+  return cuda_check(cudaMemcpy(table, host.data(), host.size(), cudaMemcpyHostToDevice), "fused_lhs_batch table copy");
+}
+
+extern "C" __attribute__((visibility("default"))) int abft_fused_lhs_batch_launch(const void* table,
+                                                                                  const int32_t* grids,
+                                                                                  int32_t dtype, void* stream) {
+  if (table == nullptr || grids == nullptr) return fail(ABFT_E_VALUE, "fused_lhs_batch: null table");
+  cudaStream_t st = as_stream(stream);
+  const auto* hdr = reinterpret_cast<const FusedBatchHeader*>(table);
+  if (grids[0] > 0) {
+    if (dtype == ABFT_BF16) border_batch_kernel<__nv_bfloat16><<<grids[0], 256, 0, st>>>(hdr);
+    else border_batch_kernel<__half><<<grids[0], 256, 0, st>>>(hdr);
+    int rc = cuda_check(cudaGetLastError(), "border batch launch");
+    if (rc != ABFT_OK) return rc;
+  }
+  if (grids[1] > 0) {
+    window_batch_kernel<<<grids[1], 256, 0, st>>>(hdr);
+    return cuda_check(cudaGetLastError(), "window batch launch");
+  }
+  return ABFT_OK;
 }
 
 extern "C" __attribute__((visibility("default"))) int abft_sum_partials(const double* partials, int32_t cap,

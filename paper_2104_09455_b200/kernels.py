@@ -295,6 +295,35 @@ def window_lhs(wsum, ws_ld: int, c: int, r: int, s: int, ck: int, rowck, bias, n
               ptr(bias) if bias is not None else None, int(n_out), ctypes.c_int64(int(m)), ptr(lhs), stream_handle())
 
 
+class FusedLhsBatch:
+    """Every producer's border buckets and every fused consumer's window lhs of a forward as two
+    launches (abft_fused_lhs_batch_*): the table is written once, launch() is graph-capturable."""
+
+    def __init__(self, border, window, dtype: DType):
+        import torch
+        nb, nw = len(border), len(window)
+        bt = (_lib.BorderTask * max(nb, 1))()
+        for i, (x, n, h, w, c, ldx, wsum, ws_ld) in enumerate(border):
+            bt[i] = _lib.BorderTask(ptr(x), ptr(wsum), int(ldx), int(n), int(h), int(w), int(c), int(ws_ld))
+        wt = (_lib.WindowTask * max(nw, 1))()
+        for i, (wsum, ws_ld, c, r, s, ck, rowck, bias, n_out, m, lhs) in enumerate(window):
+            wt[i] = _lib.WindowTask(ptr(wsum), ptr(rowck), ptr(bias) if bias is not None else None, ptr(lhs),
+                                    int(m), int(ws_ld), int(c), int(r), int(s), int(ck), int(n_out))
+        nbytes = int(_lib.load().abft_fused_lhs_batch_bytes(nb, nw))
+        self.table = torch.empty(-(-nbytes // 16) * 16, dtype=torch.uint8, device="cuda")
+        self.grids = (ctypes.c_int32 * 2)()
+        _lib.check(_lib.load().abft_fused_lhs_batch_prepare(bt, nb, wt, nw, ctypes.c_void_p(self.table.data_ptr()),
+                                                            ctypes.c_int64(self.table.numel()), self.grids))
+        self.dtype = storage_code(dtype)
+        self._keep = (border, window)
+        self.empty = nb == 0 and nw == 0
+
+    def launch(self) -> None:
+        if not self.empty:
+            _lib.check(_lib.load().abft_fused_lhs_batch_launch(ctypes.c_void_p(self.table.data_ptr()), self.grids,
+                                                               self.dtype, stream_handle()))
+
+
 def group_problem_bytes() -> int:
     return int(_lib.load().abft_group_problem_bytes())
 

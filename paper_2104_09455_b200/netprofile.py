@@ -33,6 +33,14 @@ from .shapes import DeviceProfile
 PLAN_FLAGS = (0, 1, 4, 5, 8, 16, 512, 2048, 4096, 6144)
 
 
+def _batched_share(L) -> float:
+    """A fused consumer's share (us) of the forward's two batched launches (ProtectedNetwork.fused_batch):
+    its producer's border pixels at ~3 TB/s for a 3x3 consumer, plus its window-lhs CTAs."""
+    x = L.x
+    border_px = x.n * ((2 * x.w + 2 * x.h) if L.r == 3 else 0)
+    return border_px * x.cp * 2 / 3e6 + 0.5
+
+
 def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = True,
             global_variants: bool = True) -> MeasuredTimings:
     S = Scheme
@@ -71,7 +79,8 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
             # and the producer-fused activation checksum (this kernel + the window-lhs launch + the
             # producer epilogue's window sums)
             if L.producer is not None:
-                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED), it) + ws_cost.get(id(L.producer), 0.0)
+                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED, deferred=True), it) + \
+                    ws_cost.get(id(L.producer), 0.0) + _batched_share(L)
                 if t_fused < times[S.GLOBAL_ABFT]:
                     times[S.GLOBAL_ABFT], best_var = t_fused, "fused"
             net.set_global_variant(L, best_var)
@@ -83,8 +92,8 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
                     net.set_tile(L, gkey, 0, fl)
                 except Exception:      # noqa: BLE001
                     continue
-                t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT), it) + \
-                    (ws_cost.get(id(L.producer), 0.0) if L.gvar == "fused" else 0.0)
+                t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT, deferred=True), it) + \
+                    (ws_cost.get(id(L.producer), 0.0) + _batched_share(L) if L.gvar == "fused" else 0.0)
                 if t_fl < times[S.GLOBAL_ABFT]:
                     times[S.GLOBAL_ABFT], best_fl = t_fl, fl
             net.set_tile(L, gkey, 0, best_fl)

@@ -501,10 +501,33 @@ class ProtectedNetwork:
             return GLOBAL_FUSED
         return scheme
 
-    def launch(self, L: LinearLayer, scheme=None) -> None:
+    def fused_batch(self):
+        """The forward's deferred fused-checksum work: the border buckets of every producer with a
+        fused 3x3 consumer and the window lhs of every fused consumer, as two launches after the
+        layers (every activation keeps its own buffer, so the producers' outputs are still there)."""
+        fused = [L for L in self.layers
+                 if L.producer is not None and L.scheme is Scheme.GLOBAL_ABFT and L.gvar == "fused"]
+        sig = tuple(L.index for L in fused)
+        # one table per set of fused layers, kept for the network's lifetime: captured graphs of
+        # earlier configurations still point at theirs
+        cache = self.__dict__.setdefault("_fused_batches", {})
+        if sig not in cache:
+            border, window, seen = [], [], set()
+            for L in fused:
+                P, x = L.producer, L.x
+                if L.r == 3 and id(P) not in seen:
+                    seen.add(id(P))
+                    border.append((x.buf, x.n, x.h, x.w, x.cp, x.ld, P._wsum, P.out.cp))
+                window.append((P._wsum, P.out.cp, L.x.cp, L.r, L.s, L._k // (L.r * L.s), L._rowck, L._bias_dev,
+                               _r8(L.oc), L.m, self.partials[L.index, 0, 0:1]))
+            cache[sig] = kernels.FusedLhsBatch(border, window, self.dtype)
+        return cache[sig]
+
+    def launch(self, L: LinearLayer, scheme=None, deferred: bool = False) -> None:
         """One layer's kernel under `scheme` (default: the layer's; GLOBAL_DOT / GLOBAL_FUSED pick a
         global variant explicitly).  The fused variant is the kernel (output summation only) plus
-        the window-lhs launch adding colck(A) . rowck(B) + M * sum(bias) to the layer's lhs slot."""
+        the window-lhs launch adding colck(A) . rowck(B) + M * sum(bias) to the layer's lhs slot
+        (deferred=True: left to the forward's batched launches, fused_batch)."""
         if scheme in (GLOBAL_DOT, GLOBAL_FUSED):
             key = scheme
         else:
@@ -514,7 +537,7 @@ class ProtectedNetwork:
             kernels._lib.check(kernels._lib.load().abft_gemm(kernels.ctypes.byref(args), D.stream_handle()))
         else:
             kernels.conv2d(args)
-        if key == GLOBAL_FUSED:
+        if key == GLOBAL_FUSED and not deferred:
             P = L.producer
             # (once per forward and producer: by its first 3x3 consumer running the fused lhs)
             fc = [C for C in self.fused_consumers(P)
@@ -570,9 +593,10 @@ class ProtectedNetwork:
         kernels.zero(self._block)
         for op in self.ops:
             if isinstance(op, LinearLayer):
-                self.launch(op)
+                self.launch(op, deferred=True)
             else:
                 op.fn()
+        self.fused_batch().launch()
         if verify:
             self.verify()
         return self.logits()
@@ -586,7 +610,9 @@ class ProtectedNetwork:
 
     def n_launches(self) -> int:
         """Kernel launches of one forward (layers, glue, the verification launch)."""
-        return len(self.ops) + int(any(L.scheme is Scheme.GLOBAL_ABFT for L in self.layers))
+        fb = self.fused_batch()
+        return len(self.ops) + int(any(L.scheme is Scheme.GLOBAL_ABFT for L in self.layers)) + \
+            int(fb.grids[0] > 0) + int(fb.grids[1] > 0)
 
     def verify(self) -> None:
         if any(L.scheme is Scheme.GLOBAL_ABFT for L in self.layers):

@@ -358,3 +358,35 @@ def test_cta_pair_plans_in_network(PN, name):
     for L in net.layers:
         check_layer(L)
         assert not vs[L.index].detected and abs(vs[L.index].lhs - vs[L.index].rhs) < 0.05 * vs[L.index].tolerance_used
+
+
+@pytest.mark.parametrize("name", ["squeezenet1_0", "shufflenet_v2_x1_0", "resnet50"])
+def test_deferred_fused_lhs_batch_all_networks(PN, name):
+    """Every fused-eligible consumer on the producer-fused checksum: the forward leaves the border
+    buckets and window lhs of all of them to two batched launches after the layers; each layer's lhs
+    still equals its output summation far inside tau (no activation was overwritten meanwhile), in
+    eager runs and in a replayed graph."""
+    import torch
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model(name), 2, schemes=S.GLOBAL_ABFT)
+    fused = [L for L in net.layers if L.producer is not None]
+    assert fused
+    for L in fused:
+        net.set_global_variant(L, "fused")
+    x = _input(2, seed=9)
+    net.forward(x)
+    torch.cuda.synchronize()
+    assert net.flags() == (0, 0)
+    vs = net.verdicts()
+    for L in net.layers:
+        check_layer(L)
+        v = vs[L.index]
+        assert not v.detected and abs(v.lhs - v.rhs) < 0.05 * v.tolerance_used, (L.name, v)
+    g = PN.GraphedNetwork(net)
+    net.load_input(x)
+    g.replay()
+    torch.cuda.synchronize()
+    assert net.flags() == (0, 0)
+    vs2 = net.verdicts()
+    # (fp32 window sums accumulate by atomics: replays agree to rounding, far inside tau)
+    assert all(abs(a.lhs - b.lhs) < 0.05 * a.tolerance_used and not b.detected for a, b in zip(vs, vs2))

@@ -23,7 +23,7 @@ PKG = os.path.join(ROOT, "paper_2104_09455_b200")
 def _declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:int|const char\*)\s+(abft_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(?:int|int64_t|const char\*)\s+(abft_\w+)\s*\(", text)))
 
 
 def test_header_declares_the_boundary():

@@ -1,6 +1,6 @@
 """Summary of a one-kernel ncu --set full report (the profiles/ text format), optionally writing
 profiles/dominant.json for bench.py's roofline traffic:
-  python tools/ncu_layer_summary.py REP "description" [net layer batch scheme -> dominant.json]"""
+  python tools/ncu_layer_summary.py REP "description" [net layer batch scheme [flags variant] -> dominant.json]"""
 import csv
 import json
 import os
@@ -45,7 +45,10 @@ if len(sys.argv) > 6:
     def byt(k):
         v, u = m[k]
         return float(v) * SCALE.get(u, 1)
-    dj = {"tag": "r02", "config": {"net": net, "layer": layer, "batch": int(batch), "scheme": scheme},
+    cfg = {"net": net, "layer": layer, "batch": int(batch), "scheme": scheme}
+    if len(sys.argv) > 8:      # the launch's plan: plan_flags and global variant (bench.py matches both)
+        cfg.update(flags=int(sys.argv[7]), variant=sys.argv[8])
+    dj = {"tag": "r02", "config": cfg,
           "dram_bytes_read": byt("dram__bytes_read.sum"), "dram_bytes_write": byt("dram__bytes_write.sum"),
           "source": f"profiles/r02_ncu_{layer}_{scheme}.txt"}
     with open(os.path.join(ROOT, "gpurun_out", "dominant.json"), "w") as fh:
