@@ -225,6 +225,16 @@ def main():
         for pure, sch in (("global", S.GLOBAL_ABFT), ("thread", S.THREAD_ONE_SIDED)):
             if all(c is sch for c in chosen):
                 graphs["ig"], alias = graphs[pure], pure
+        if alias is None:
+            # the in-network A/B over whole plans: the per-layer plan against the two pure plans
+            # (interleaved replays, medians); a pure plan replaces it unless the per-layer plan wins
+            # by more than 1 % of the forward (ties go to global, cost.py:186)
+            t_ig, t_g, t_t = NP._forward_ms([graphs["ig"].graph, graphs["global"].graph, graphs["thread"].graph], 11)
+            best = min((t_g / 1.01, "global", S.GLOBAL_ABFT), (t_t, "thread", S.THREAD_ONE_SIDED))
+            if best[0] < t_ig:
+                chosen = [best[2]] * len(net.layers)
+                net.set_schemes(chosen)
+                graphs["ig"], alias = graphs[best[1]], best[1]
         graphs["glue"] = NP.capture(net.forward_glue)
         vfn, vx = NP.vendor_forward(model, lb)
         vx.copy_(x)
