@@ -738,7 +738,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // CTA pair: this CTA's 128 A rows and its half of the B rows, both completing on the
           // leader's full barrier, which expects the pair's bytes
           const uint32_t tx2 = 2u * (halo ? p.tx_a + (b_res ? 0u : (uint32_t)L_cv_S * L_tx_b)
-                                          : L_stage_a_bytes + L_tx_b);
+                                          : L_stage_a_bytes + L_tx_b +
+                                                (ck_loaded ? (uint32_t)(L_nck_pad / 2) * 128u : 0u));
           const int brow = (ck_aug ? nb * L_b_rows_blk : n0) + (int)crank * p.b_half;
 #pragma unroll 1
           for (int kb = 0; kb < L_nkb; ++kb) {
@@ -769,6 +770,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                          (uint16_t)(tap - r * L_cv_S), (uint16_t)r);
             }
             ptx::tma_load_2d_w2(sm_b + s * L_stage_b_bytes, &tmB, fb, kb * BK, brow);
+            if (ck_loaded)
+              ptx::tma_load_2d_w2(sm_ck + s * L_stage_ck_bytes, &tmCK, fb, kb * BK,
+                                  nb * L_ck_rstride + L_ck_roff + (int)crank * (L_nck_pad / 2));
             if (++s == L_stages) { s = 0; ph ^= 1; }
           }
           continue;
@@ -873,7 +877,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (crank == 0) {
         const uint64_t a_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_a));
         const uint64_t b_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_b));
-        const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4;
+        const uint64_t c_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_ck));
+        const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4, c_sstep = p.stage_ck_bytes >> 4;
         const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
         const int L_nkb = p.nkb, L_stages = p.stages, L_acc_stages = p.acc_stages, L_cols = p.cols_per_acc;
         const int L_num_tiles = p.num_tiles, L_cv_S = p.cv_S;
@@ -906,9 +911,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      idesc_m, (kb | si | k) != 0 ? 1u : 0u);
                 }
               } else {
+                const uint64_t cd = c_base + (uint64_t)s * c_sstep;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k)
+                for (int k = 0; k < BK / 16; ++k) {
                   ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
+                  if (ck_loaded)
+                    ptx::mma_f16_ss2(d + bn, ad + 2ull * k, cd + 2ull * k, p.idesc_ck, (kb | k) != 0 ? 1u : 0u);
+                }
               }
               ptx::mma_commit2_mc(&empty[s], 3);
             }
@@ -2517,7 +2526,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
       const long long waves = tiles <= 4LL * sms ? 100 * ((tiles + sms - 1) / sms) : (100 * tiles + sms - 1) / sms;
       const int nck = has_ck ? round_up((cand / nt) * (split ? 2 : 1), 16) : (gck ? 16 : 0);
       const bool asplit = a->ck_layout == 1 && (has_ck || gck) && cand + nck > 256;
-      if (asplit && (cand != 256 || (a->plan_flags & 4096))) continue;   // (CTA pairs: one B box per k-block)
+      if (asplit && cand != 256) continue;
       // the split's second (N = nck) MMA per k-step costs about 64 rows' worth
       // im2col A boxes cost about twice a tiled box; tiles whose width is not a whole number of
       // 32-column chunks lose the bulk-tensor output stores (~4 k-blocks of epilogue)
@@ -2664,7 +2673,8 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     // the B rows; the plain-class paths over TMA tiles / 64-channel im2col boxes only
     const int n_mma = p.ck_mode == 3 ? bn + p.nck_pad : bn;
     if (gather || (cg != nullptr && cg->a_mode == 2) || out.cls != CLASS_PLAIN ||
-        p.lhs_w != nullptr || want_acolck || (p.ck_mode != 0 && p.ck_mode != 3) || n_mma % 16 != 0)
+        p.lhs_w != nullptr || want_acolck || (p.ck_mode != 0 && p.ck_mode != 3 && p.ck_mode != 4) ||
+        (p.ck_mode == 4 && halo) || n_mma % 16 != 0)
       return fail(ABFT_E_UNSUPPORTED, "CTA pairs: plain / global-slice GEMMs and 64-channel im2col convs only");
     p.pair = 1;
     p.b_half = n_mma / 2;
@@ -2673,6 +2683,12 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
     p.tx_b = (uint32_t)p.b_half * BK * 2;
     p.idesc_main = ptx::idesc_f16(fmt, 2 * BM, bn);
     p.idesc_aug = ptx::idesc_f16(fmt, 2 * BM, (uint32_t)n_mma);
+    if (p.ck_mode == 4) {
+      // tile_n 256 + the checksum rows by their own box (half per CTA) into their own N = 16 slice
+      p.idesc_aug = p.idesc_main;
+      p.idesc_ck = ptx::idesc_f16(fmt, 2 * BM, (uint32_t)p.nck_pad);
+      p.stage_ck_bytes = (uint32_t)round_up(p.nck_pad / 2 * BK * 2, 1024);
+    }
     p.m_tiles = round_up(p.num_m_blocks, 2);
     p.num_tiles = p.m_tiles * p.num_n_blocks;
   }
@@ -2930,9 +2946,11 @@ int launch_with_a(const abft_gemm_args_t* a, Plan& pl, const CUtensorMap& ma, vo
                                 std::to_string(a->K));
     rc = cached_map(&mb, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck,
                     p.pair ? p.b_half : p.ck_mode == 4 ? p.bn : p.b_rows_blk);
+    // (a pair's checksum box: half of the N = 16 slice per CTA)
     // split: the block's checksum rows (and the next block's first rows, whose products land in
     // ignored checksum columns) by a second box
-    if (rc == ABFT_OK && p.ck_mode == 4) rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.nck_pad);
+    if (rc == ABFT_OK && p.ck_mode == 4)
+      rc = cached_map(&mc, a->ck_rows, a->dtype, a->K, a->ck_rows_n, a->ldck, p.pair ? p.nck_pad / 2 : p.nck_pad);
   } else {
     // plan_flags bit 1: Bt holds zero rows up to a whole number of tiles, so the weight boxes never
     // cross the tensor's edge (no out-of-bounds fill on the load path)

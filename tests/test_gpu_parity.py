@@ -343,12 +343,14 @@ def test_cta_pairs_match_oracle(P, scheme, m, n, k):
     fr = [("output", m - 1, n // 2, 5)] if scheme != "unprotected" else []
     out_ref, v_ref = O.execute(a, b, O.Tiling(), scheme, fr)
     faults = [P.OutputFault(row=f[1], col=f[2], delta=f[3]) for f in fr]
-    rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults, plan_flags=4096)
-    assert np.array_equal(rep.output, out_ref)
-    if scheme == "global-abft":
-        v = rep.verdicts[0]
-        assert (v.detected, v.lhs, v.rhs) == (v_ref[0].detected, v_ref[0].lhs, v_ref[0].rhs)
-        assert v.detected
+    # (global with tile_n 256: the checksum rows by their own half boxes into their own pair slice)
+    for tn in ((0, 256) if scheme == "global-abft" and n >= 256 else (0,)):
+        rep = P.execute(a, b, P.TilingConfig(), P.Scheme(scheme), faults, plan_flags=4096, tile_n=tn)
+        assert np.array_equal(rep.output, out_ref), tn
+        if scheme == "global-abft":
+            v = rep.verdicts[0]
+            assert (v.detected, v.lhs, v.rhs) == (v_ref[0].detected, v_ref[0].lhs, v_ref[0].rhs), tn
+            assert v.detected
     af = rng.uniform(-1, 1, size=(m, k)).astype(np.float16)
     bf = rng.uniform(-1, 1, size=(k, n)).astype(np.float16)
     r1 = P.execute(af, bf, P.TilingConfig(), P.Scheme(scheme), plan_flags=4096)

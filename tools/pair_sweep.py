@@ -40,6 +40,19 @@ def run(m, n, k):
         res[f"global{'_pair' if fl else ''}"] = graph_time_us(
             lambda: kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, ck_rows=gck,
                                  **g), it)
+    # global with the lhs outside the GEMM (plan_flags bit 10): colck(A) by one column-sum pass,
+    # dotted with the weights' offline rowck(B) (checksum.py:108-117), the GEMM only sums its output
+    rowck = kernels.weight_rowck(pw.bt, n, k, P.BINARY16)
+    colck = torch.zeros(k, dtype=torch.float32, device="cuda")
+    sums = torch.zeros(2, dtype=torch.float64, device="cuda")
+    tasks = kernels.global_tasks([(colck, rowck, None, k)])
+    ekw = dict(base, out_sum=sums[1:2], plan_flags=1024 | 4096)
+
+    def ext():
+        kernels.colsum(a, m, k, k, P.BINARY16, colck)
+        kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, **ekw)
+        kernels.global_lhs(tasks, 1, sums)
+    res["global_ext_pair"] = graph_time_us(ext, it)
     tf = {key: 2 * m * n * k / (v * 1e-6) / 1e12 for key, v in res.items()}
     print(f"{m:8d} {n:5d} {k:5d} | " + " ".join(f"{key}={v:9.2f}us({tf[key]:6.0f})" for key, v in res.items()) +
           " | tiles " + " ".join(f"{key}={pl['tile_n']}/{pl['stages']}st" for key, pl in plans.items()), flush=True)
