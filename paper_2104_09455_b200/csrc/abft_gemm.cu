@@ -880,6 +880,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint64_t c_base = ptx::desc_kmajor_sw128(ptx::smem_u32(sm_ck));
         const uint64_t a_sstep = p.stage_a_bytes >> 4, b_sstep = p.stage_b_bytes >> 4, c_sstep = p.stage_ck_bytes >> 4;
         const uint32_t idesc_m = ck_aug ? p.idesc_aug : p.idesc_main;
+        const uint32_t L_idesc_ck = p.idesc_ck;
         const int L_nkb = p.nkb, L_stages = p.stages, L_acc_stages = p.acc_stages, L_cols = p.cols_per_acc;
         const int L_num_tiles = p.num_tiles, L_cv_S = p.cv_S;
         const uint64_t b_tstep = p.b_tile_bytes >> 4;
@@ -910,13 +911,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::mma_f16_ss2(d, ad + 8ull * (uint64_t)si + 2ull * k, bd + b_tstep * (uint64_t)si + 2ull * k,
                                      idesc_m, (kb | si | k) != 0 ? 1u : 0u);
                 }
+              } else if (!ck_loaded) {
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
               } else {
+                // tile_n 256 + the checksum slice (its own N = 16 pair MMA into columns bn..)
                 const uint64_t cd = c_base + (uint64_t)s * c_sstep;
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) {
                   ptx::mma_f16_ss2(d, ad + 2ull * k, bd + 2ull * k, idesc_m, (kb | k) != 0 ? 1u : 0u);
-                  if (ck_loaded)
-                    ptx::mma_f16_ss2(d + bn, ad + 2ull * k, cd + 2ull * k, p.idesc_ck, (kb | k) != 0 ? 1u : 0u);
+                  ptx::mma_f16_ss2(d + bn, ad + 2ull * k, cd + 2ull * k, L_idesc_ck, (kb | k) != 0 ? 1u : 0u);
                 }
               }
               ptx::mma_commit2_mc(&empty[s], 3);
@@ -2315,6 +2320,34 @@ int launch_inst(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                                     max_smem_optin());
   });
   if (attr_err != cudaSuccess) return cuda_check(attr_err, "cudaFuncSetAttribute(abft_gemm_kernel)");
+  if (p.pair) {
+    // a persistent grid of pairs must be co-resident: GPCs with an odd number of usable SMs
+    // host fewer 2-CTA clusters than SMs / 2 (a second wave of a few clusters doubles the tail)
+    static std::mutex mu;
+    static std::map<size_t, int> max_clusters;     // by dynamic smem bytes
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = max_clusters.find(smem);
+    if (it == max_clusters.end()) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(2);
+      q.blockDim = dim3(NUM_THREADS);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = 2;
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      q.attrs = ca;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, abft_gemm_kernel<T, CLASS, NT, AM, WS>, &q) != cudaSuccess || n < 1) {
+        (void)cudaGetLastError();
+        n = 0;
+      }
+      it = max_clusters.emplace(smem, n).first;
+    }
+    if (it->second > 0) grid = std::max(2, std::min(grid, 2 * it->second));
+  }
   if (p.pdl || p.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
