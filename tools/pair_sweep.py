@@ -53,6 +53,18 @@ def run(m, n, k):
         kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, **ekw)
         kernels.global_lhs(tasks, 1, sums)
     res["global_ext_pair"] = graph_time_us(ext, it)
+    # the same with the column-sum pass on a second stream, overlapping the (compute-bound) GEMM
+    side = torch.cuda.Stream()
+
+    def ext_overlap():
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            kernels.colsum(a, m, k, k, P.BINARY16, colck)
+        kernels.gemm(a, k, pw.bt, pw.ldbt, m, n, k, P.BINARY16, 1, P.Scheme.GLOBAL_ABFT, **ekw)
+        cur.wait_stream(side)
+        kernels.global_lhs(tasks, 1, sums)
+    res["global_ext_pair_overlap"] = graph_time_us(ext_overlap, it)
     tf = {key: 2 * m * n * k / (v * 1e-6) / 1e12 for key, v in res.items()}
     print(f"{m:8d} {n:5d} {k:5d} | " + " ".join(f"{key}={v:9.2f}us({tf[key]:6.0f})" for key, v in res.items()) +
           " | tiles " + " ".join(f"{key}={pl['tile_n']}/{pl['stages']}st" for key, pl in plans.items()), flush=True)
