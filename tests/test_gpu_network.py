@@ -310,11 +310,13 @@ def test_per_tap_im2col_plan_flag(PN, name):
     net.inject({})
 
 
-@pytest.mark.parametrize("name", ["vgg16", "resnet50"])
-def test_cta_pair_plans_in_network(PN, name):
+@pytest.mark.parametrize("name,pflags", [("vgg16", 4096 | 2048), ("resnet50", 4096 | 2048), ("vgg16", 4096),
+                                         ("resnet50", 4096)])
+def test_cta_pair_plans_in_network(PN, name, pflags):
     """CTA pairs (plan_flags bit 12) on every layer whose unprotected / global-slice launch takes
-    them (3x3 stride-1 convs through per-tap im2col, bit 11): layers match the fp32 checker, clean
-    runs flag nothing, and a fault in a paired layer is flagged there only."""
+    them (3x3 stride-1 convs through per-tap im2col with bit 11, else through paired halo windows):
+    layers match the fp32 checker, clean runs flag nothing, a fault in a paired layer is flagged
+    there only, and paired producers feed fused consumers their window sums."""
     import torch
     S = PN.Scheme
     net = PN.ProtectedNetwork(PN.build_model(name), 2)
@@ -323,7 +325,7 @@ def test_cta_pair_plans_in_network(PN, name):
     for L in net.layers:
         for key in paired:
             try:
-                net.set_tile(L, key, 0, 4096 | 2048)
+                net.set_tile(L, key, 0, pflags)
                 paired[key].append(L)
             except Exception:      # noqa: BLE001 — a plan the pairs do not take (stems, strided, thin)
                 pass
@@ -348,7 +350,7 @@ def test_cta_pair_plans_in_network(PN, name):
     # fused consumers: paired producers accumulate window sums in their epilogues
     for L in net.layers:
         if L.producer is not None:
-            net.set_tile(L, PN.GLOBAL_FUSED, 0, 4096 | 2048) if L in paired[S.GLOBAL_ABFT] else None
+            net.set_tile(L, PN.GLOBAL_FUSED, 0, pflags) if L in paired[S.GLOBAL_ABFT] else None
             net.set_global_variant(L, "fused")
     assert any(P.ws_active and P in paired[S.UNPROTECTED] for P in net.producers() if isinstance(P, PN.LinearLayer))
     net.forward(x)
