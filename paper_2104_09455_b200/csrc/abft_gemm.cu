@@ -1532,9 +1532,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // rows, one bulk tensor store), 32-column bulk stores (64-byte rows), or direct row stores
     // (16-column tails, partial halo quadrants)
     // (mc / mc2 / Cp / ldc / N: the output of the tile's problem — the launch's, or a grouped one's)
+    // WS: column sums of a staged 32-column chunk read back from the staging rows (the stored,
+    // rounded values; rows past M excluded) — 16 loads per lane instead of a register transpose;
+    // lane = (column pair, row parity)
+    auto ws_staged = [&](const uint8_t* base, int rowbytes, int chunk0, bool wide_rows, int gc0, int N, int nrows) {
+      const int cp = lane & 15, half = lane >> 4;
+      const uint32_t jj = (uint32_t)(chunk0 + (cp >> 2));
+      const uint32_t wofs = (uint32_t)(cp & 3) * 4u;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int r = half + 2 * i;
+        if (r < nrows) {
+          const uint32_t sw = wide_rows ? (uint32_t)(r & 7) : (uint32_t)((r >> 1) & 3);
+          const float2 f = TR::unpack2(*reinterpret_cast<const uint32_t*>(base + r * rowbytes + ((jj ^ sw) << 4) + wofs));
+          a0 += f.x;
+          a1 += f.y;
+        }
+      }
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 16);
+      const int c = gc0 + 2 * cp;
+      if (half == 0) {
+        if (c < N && a0 != 0.f) atomicAdd(&ws_s[c], a0);
+        if (c + 1 < N && a1 != 0.f) atomicAdd(&ws_s[c + 1], a1);
+      }
+    };
     auto store_chunk = [&](const float (&v)[32], int c0, int cmax, int gc0, int m0, int gm, bool row_ok, bool relu,
                            bool tma, bool& unit_wide, const CUtensorMap* mc, const CUtensorMap* mc2, void* Cp,
-                           long long ldc, int N) {
+                           long long ldc, int N, bool& ws_done, int ws_rows) {
       const bool single = p.out_single != 0;
       const int sub = (c0 >> 5) & 1;
       if (wide && sub == 0) unit_wide = tma && cmax >= 64;
@@ -1562,6 +1588,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             u.w = TR::pack2(v[8 * j + 6], v[8 * j + 7]);
           }
           *reinterpret_cast<uint4*>(rowp + (((uint32_t)(sub * 4 + j) ^ (uint32_t)(lane & 7)) << 4)) = u;
+        }
+        if constexpr (WS) {
+          if (p.ws_mode == 1) {
+            __syncwarp();
+            ws_staged(my_stage + sbuf * 4096, 128, sub * 4, true, gc0, N, ws_rows);
+            ws_done = true;
+          }
         }
         if (sub == 1) {
           ptx::fence_proxy_async_smem();
@@ -1597,6 +1630,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
+        if constexpr (WS) {
+          if (p.ws_mode == 1) {
+            ws_staged(my_stage + sbuf * (wide ? 4096 : 2048), 64, 0, false, gc0, N, ws_rows);
+            ws_done = true;
+          }
+        }
         if (lane == 0) {
           ptx::tma_store_2d(mc, my_stage + sbuf * (wide ? 4096 : 2048), gc0, m0 + q * 32);
           ptx::bulk_commit();
@@ -1712,13 +1751,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int cn = c_next(c0);
             have_rb = cn < bn_eff && residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
           }
+          bool ws_done = false;
+          store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide, mc, mc2, Cp, ldc, N, ws_done,
+                      min(32, M - (m0 + q * 32)));
           if constexpr (WS) {
-            float vr[32];
+            if (!ws_done) {      // (chunks stored directly: the register transpose-reduce)
+              float vr[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
-            wsum_chunk(p, ws_s, vr, gm, row_valid, gc0, min(cmax, N - gc0), lane);
+              for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
+              wsum_chunk(p, ws_s, vr, gm, row_valid, gc0, min(cmax, N - gc0), lane);
+            }
           }
-          store_chunk(v, c0, cmax, gc0, m0, gm, row_valid, relu, tma, unit_wide, mc, mc2, Cp, ldc, N);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -1808,13 +1851,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               have_rb = cn < bn_eff &&
                         residual_prefetch<T>(rb, resid, ld_res, gm, n0 + cn, min(bn_eff - cn, N - n0 - cn));
             }
+            bool ws_done = false;
+            store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide, mc, mc2, Cp, ldc, N,
+                        ws_done, min(32, M - (m0 + q * 32)));
             if constexpr (WS) {
-              float vr[32];
+              if (!ws_done) {
+                float vr[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
-              wsum_chunk(p, ws_s, vr, gm, row_in_tile && gm < M, gc0, min(cmax, N - gc0), lane);
+                for (int j = 0; j < 32; ++j) vr[j] = round_out(relu ? fmaxf(v[j], 0.f) : v[j], p.out_dtype);
+                wsum_chunk(p, ws_s, vr, gm, row_in_tile && gm < M, gc0, min(cmax, N - gc0), lane);
+              }
             }
-            store_chunk(v, c0, cmax, gc0, m0, gm, row_in_tile && gm < M, relu, tma, unit_wide, mc, mc2, Cp, ldc, N);
           }
           // fired groups of the thread tile's Mt rows -> verdicts (rare)
           uint32_t m = row_verdict ? fmask : 0u;
