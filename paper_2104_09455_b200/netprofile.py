@@ -20,7 +20,7 @@ from typing import Dict
 from . import device as D
 from . import kernels
 from .cost import MeasuredTimings, select
-from .profiler import graph_time_us
+from .profiler import capture_graph, graph_time_us, interleaved_min_us
 from .protected_network import GLOBAL_DOT, GLOBAL_FUSED, SELECTABLE, GraphedNetwork, PoolProducer, ProtectedNetwork
 from .schemes import Scheme
 from .shapes import DeviceProfile
@@ -69,51 +69,56 @@ def profile(net: ProtectedNetwork, iters: int = 10, best_unprotected: bool = Tru
             ws_cost[id(P)] = max(0.0, t_on - t_off)
     for L in net.layers:
         it = iters if L.flops() < 2e11 else max(3, iters // 3)
-        times = {s: graph_time_us(lambda s=s: net.launch(L, s), it) for s in SELECTABLE}
-        if global_variants:
-            # the global scheme's lhs source: checksum MMA slice vs checksum-warp dot, the faster
-            t_dot = graph_time_us(lambda: net.launch(L, GLOBAL_DOT), it)
-            best_var = "slice"
-            if t_dot < times[S.GLOBAL_ABFT]:
-                times[S.GLOBAL_ABFT], best_var = t_dot, "dot"
-            # and the producer-fused activation checksum (this kernel + the window-lhs launch + the
-            # producer epilogue's window sums)
-            if L.producer is not None:
-                t_fused = graph_time_us(lambda: net.launch(L, GLOBAL_FUSED, deferred=True), it) + \
-                    ws_cost.get(id(L.producer), 0.0) + _batched_share(L)
-                if t_fused < times[S.GLOBAL_ABFT]:
-                    times[S.GLOBAL_ABFT], best_var = t_fused, "fused"
-            net.set_global_variant(L, best_var)
-            # and its plan hints (no k-block pairs / double output staging), the fastest
-            gkey = {"dot": GLOBAL_DOT, "fused": GLOBAL_FUSED}.get(L.gvar, S.GLOBAL_ABFT)
-            best_fl = 0
-            for fl in PLAN_FLAGS[1:]:
+        # every candidate launch of the layer, captured with its own arguments, then timed in
+        # interleaved rounds (the same clock / power state for all of them)
+        cands = []          # (kind, config, extra_us, graph)
+
+        def add(kind, config, fn, extra=0.0):
+            cands.append((kind, config, extra, capture_graph(fn, it)))
+        add("thread", None, lambda: net.launch(L, S.THREAD_ONE_SIDED))
+        # unprotected: the planner's configuration and every tile / plan-hint alternative
+        ucfgs = [(0, 0)]
+        if best_unprotected:
+            tiles = {net.plan_of(L, s)["tile_n"] for s in (S.GLOBAL_ABFT, S.THREAD_ONE_SIDED)}
+            base_tile = net.plan_of(L, S.UNPROTECTED)["tile_n"]
+            ucfgs += [(tn, fl) for tn in sorted(tiles - {base_tile}) + [0] for fl in PLAN_FLAGS if (tn, fl) != (0, 0)]
+        for tn, fl in ucfgs:
+            try:
+                net.set_tile(L, S.UNPROTECTED, tn, fl)
+            except Exception:     # noqa: BLE001 — a configuration the unprotected plan cannot take
+                continue
+            add("unprotected", (tn, fl), lambda: net.launch(L, S.UNPROTECTED))
+        # global: the lhs source (checksum MMA slice, checksum-warp dot, producer-fused activation
+        # checksum + its producer's window-sum cost and its share of the batched launches) x plan hints
+        variants = [("slice", S.GLOBAL_ABFT), ("dot", GLOBAL_DOT)] if global_variants else [("slice", S.GLOBAL_ABFT)]
+        if global_variants and L.producer is not None:
+            variants.append(("fused", GLOBAL_FUSED))
+        keep_var = L.gvar
+        for var, key in variants:
+            extra = ws_cost.get(id(L.producer), 0.0) + _batched_share(L) if var == "fused" else 0.0
+            for fl in (PLAN_FLAGS if global_variants else (0,)):
                 try:
-                    net.set_tile(L, gkey, 0, fl)
+                    net.set_tile(L, key, 0, fl)
                 except Exception:      # noqa: BLE001
                     continue
-                t_fl = graph_time_us(lambda: net.launch(L, S.GLOBAL_ABFT, deferred=True), it) + \
-                    (ws_cost.get(id(L.producer), 0.0) + _batched_share(L) if L.gvar == "fused" else 0.0)
-                if t_fl < times[S.GLOBAL_ABFT]:
-                    times[S.GLOBAL_ABFT], best_fl = t_fl, fl
-            net.set_tile(L, gkey, 0, best_fl)
-        if best_unprotected:
-            cands = {net.plan_of(L, s)["tile_n"] for s in (S.GLOBAL_ABFT, S.THREAD_ONE_SIDED)}
-            base_tile = net.plan_of(L, S.UNPROTECTED)["tile_n"]
-            best = (times[S.UNPROTECTED], 0)
-            for tn in sorted(cands - {base_tile}) + [0]:
-                for fl in PLAN_FLAGS:
-                    if (tn, fl) == (0, 0):
-                        continue
-                    try:
-                        net.set_tile(L, S.UNPROTECTED, tn, fl)
-                    except Exception:     # noqa: BLE001 — a tile the unprotected plan cannot take
-                        continue
-                    tt = graph_time_us(lambda: net.launch(L, S.UNPROTECTED), it)
-                    if tt < best[0]:
-                        best = (tt, (tn, fl))
-            net.set_tile(L, S.UNPROTECTED, *(best[1] if best[1] else (0, 0)))
-            times[S.UNPROTECTED] = best[0]
+                L.gvar = var           # (the launch key of the variant; window sums are not needed here)
+                add("global", (var, fl), lambda: net.launch(L, S.GLOBAL_ABFT, deferred=True), extra)
+                L.gvar = keep_var
+        tms = interleaved_min_us([c[3] for c in cands], it)
+        times = {}
+        best = {}
+        for (kind, cfg, extra, _), tm in zip(cands, tms):
+            tt = tm + extra
+            if kind not in best or tt < best[kind][0]:
+                best[kind] = (tt, cfg)
+        del cands
+        times[S.THREAD_ONE_SIDED] = best["thread"][0]
+        times[S.UNPROTECTED], (utn, ufl) = best["unprotected"]
+        net.set_tile(L, S.UNPROTECTED, utn, ufl)
+        times[S.GLOBAL_ABFT], (gvar, gfl) = best["global"]
+        for var, key in variants:
+            net.set_tile(L, key, 0, gfl if var == gvar else 0)
+        net.set_global_variant(L, gvar)
         out[(L.index, S.UNPROTECTED)] = times[S.UNPROTECTED] * 1e-6
         out[(L.index, S.GLOBAL_ABFT)] = (times[S.GLOBAL_ABFT] + t_ver / len(net.layers)) * 1e-6
         out[(L.index, S.THREAD_ONE_SIDED)] = times[S.THREAD_ONE_SIDED] * 1e-6

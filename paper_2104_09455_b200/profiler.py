@@ -25,6 +25,42 @@ from .schemes import Scheme, TilingConfig
 from .shapes import BINARY16, DType
 
 
+def capture_graph(fn, iters: int):
+    """`iters` back-to-back calls of fn() captured in one CUDA graph (after one eager call); the
+    launches' arguments are fixed at capture."""
+    t = D.torch()
+    s = t.cuda.Stream()
+    s.wait_stream(t.cuda.current_stream())
+    with t.cuda.stream(s):
+        fn()
+        t.cuda.synchronize()
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g, stream=s):
+            for _ in range(iters):
+                fn()
+    t.cuda.synchronize()
+    g.replay()
+    t.cuda.synchronize()
+    return g
+
+
+def interleaved_min_us(graphs, iters: int, reps: int = 5) -> list:
+    """Per-launch time (us) of each captured graph, best over `reps` rounds that replay every graph in
+    turn: candidates compared under the same clock / power state (a power-capped B200 drifts by
+    several % between back-to-back measurements of the same kernel)."""
+    t = D.torch()
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    best = [float("inf")] * len(graphs)
+    for _ in range(reps):
+        for i, g in enumerate(graphs):
+            e0.record()
+            g.replay()
+            e1.record()
+            t.cuda.synchronize()
+            best[i] = min(best[i], e0.elapsed_time(e1) * 1e3 / iters)
+    return best
+
+
 def graph_time_us(fn, iters: int = 40, reps: int = 5) -> float:
     """Best-of-reps mean time of `iters` back-to-back calls replayed from one CUDA graph."""
     t = D.torch()
