@@ -392,3 +392,30 @@ def test_deferred_fused_lhs_batch_all_networks(PN, name):
     vs2 = net.verdicts()
     # (fp32 window sums accumulate by atomics: replays agree to rounding, far inside tau)
     assert all(abs(a.lhs - b.lhs) < 0.05 * a.tolerance_used and not b.detected for a, b in zip(vs, vs2))
+
+
+def test_profiler_selects_and_applies_plans(PN):
+    """netprofile.profile on a small network: every layer gets unprotected / global / one-sided
+    timings from interleaved candidate rounds, the chosen variant and plan hints are applied, and
+    the IG-selected forward still matches the fp32 checker with zero false positives."""
+    import torch
+    from paper_2104_09455_b200 import netprofile as NP
+    from paper_2104_09455_b200.shapes import DeviceProfile
+    S = PN.Scheme
+    net = PN.ProtectedNetwork(PN.build_model("squeezenet1_0"), 2)
+    x = _input(2, seed=11)
+    net.load_input(x)
+    net.forward()
+    torch.cuda.synchronize()
+    meas = NP.profile(net, iters=2)
+    for L in net.layers:
+        for s in PN.SELECTABLE:
+            assert meas.get(L.index, s) > 0, (L.name, s)
+        assert meas.get(L.index, S.UNPROTECTED) <= meas.get(L.index, S.GLOBAL_ABFT) * 1.5
+    dev = DeviceProfile(name="B200", tensor_throughput=1.65e15, alu_throughput=74e12, memory_bandwidth=6.5e12)
+    NP.select_ig(net, dev, meas)
+    net.forward(x)
+    torch.cuda.synchronize()
+    assert net.flags() == (0, 0)
+    for L in net.layers:
+        check_layer(L)
