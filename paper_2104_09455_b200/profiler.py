@@ -103,13 +103,18 @@ def profile_layers(weights: Sequence, batch: int, dtype: DType = BINARY16,
               (Scheme.UNPROTECTED, Scheme.GLOBAL_ABFT, Scheme.THREAD_ONE_SIDED)}
     entries = {}
     for i in range(n):
+        # the three schemes' launches of layer i, timed in interleaved rounds
+        keys, graphs = [], []
         for s, ch in chains.items():
             L = ch.layers[i]
             a = ch.x if i == 0 else ch.acts[i - 1]
             kw = ch._gemm_kwargs(i, L)
-            entries[(i, s)] = graph_time_us(lambda: kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, batch, L.n, L.k,
-                                                                 dtype, ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw),
-                                            iters)
+            keys.append((i, s))
+            graphs.append(capture_graph(lambda: kernels.gemm(a, a.stride(0), L.pw.bt, L.pw.ldbt, batch, L.n, L.k,
+                                                             dtype, ch.numeric, L.scheme, ck_rows=L.ck_rows, **kw),
+                                        iters))
+        for key, tm in zip(keys, interleaved_min_us(graphs, iters)):
+            entries[key] = tm
     # the chain's deferred verification runs in the last CTA of its last launch (no extra launch),
     # so a layer's global-ABFT time is its kernel time
     out = {}
