@@ -316,7 +316,10 @@ int abft_conv2d(const abft_conv_args_t* args, void* stream);
  *              e.g. network stems, where K = r*s*c_real is packed densely)
  *   out[1] packed-weight channel stride ck, out[2] P, out[3] Q,
  *   out[4] K of the GEMM (r*s*ck, or round8(r*s*c_real) in mode 3), out[5] M = n*P*Q,
- *   out[6] workspace bytes (mode 3) */
+ *          5 = gathered A tiles (the checksum warps copy (tap, channel) chunks with cp.async:
+ *              <= 4 real channels, or C < 48 a multiple of 8), weights resident in shared memory;
+ *   out[6] workspace bytes (mode 3; for mode 5 the size of the explicit im2col the call falls back
+ *          to when the gather cannot take it, e.g. weights + window sums past shared memory) */
 int abft_conv_plan(const abft_conv_args_t* args, int32_t* out /*[8]*/);
 /* The kernel plan abft_conv2d would use for `args` (no launch), laid out as abft_gemm_plan's
  * out[0..8]; out[9] = the A-load mode actually used.  Augmented weights / checksum rows for a

@@ -149,6 +149,7 @@ struct GemmParams {
   // while B (all k-blocks, one N block) stays resident; no im2col workspace
   const void* cv_x;
   int cv_H, cv_W, cv_taps;
+  int cv_gc;             // gathered channels per tap: 4 (stems, 8-byte copies) or C % 8 == 0 (16-byte copies)
   // window column sums of the stored output for the next layer's global lhs (abft_gemm_args_t.wsum):
   // CTA-private [ws_nb][N] fp32 buckets in smem (off_ws), flushed once by atomics into wsum[b * ws_ld + col]
   float* wsum;
@@ -1184,6 +1185,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int* gtab = reinterpret_cast<int*>(smem + p.off_acolck);
       if (ct < 64)
         gtab[ct] = ct < taps ? (int)(((ct / S - ph0) * (long long)W + (ct % S - pw0)) * pix_bytes) : 0;
+      // wide gathers (cv_gc = C, a multiple of 8): 16-byte chunk j of K = (tap, channel) elements
+      // [8j, 8j + 8) -> its byte offset from the window centre (gtab8) and its tap (gtap8)
+      const int gc = p.cv_gc;
+      int* gtab8 = gtab + 64;
+      uint8_t* gtap8 = reinterpret_cast<uint8_t*>(gtab + 64 + 256);
+      if (gc != 4) {
+        ptx::named_bar_sync(2, 128);
+        for (int j = ct; j < 256; j += 128) {
+          const int k0 = j * 8, t = k0 / gc;
+          gtab8[j] = t < taps ? gtab[t] + (k0 - t * gc) * 2 : 0;
+          gtap8[j] = (uint8_t)(t < taps ? t : 255);
+        }
+      }
       for (int i = ct; i < (int)(stages * p.stage_a_bytes / 16); i += 128)
         reinterpret_cast<uint4*>(sm_a)[i] = make_uint4(0u, 0u, 0u, 0u);
       ptx::named_bar_sync(2, 128);
@@ -1217,7 +1231,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t vk = (uint32_t)(vm >> (kb * 16));
           const int t0 = kb * 16;
           const int4* g4 = reinterpret_cast<const int4*>(gtab + t0);
-          if (t0 + 16 <= taps) {
+          if (gc != 4) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int jj = kb * 8 + j;
+              const uint32_t t = gtap8[jj];
+              const bool in = t < 64u && ((vm >> t) & 1ull);
+              ptx::cp_async16(dst + dcol[j], pc + (in ? gtab8[jj] : 0), in ? 16u : 0u);
+            }
+          } else if (t0 + 16 <= taps) {
             int oo[16];
 #pragma unroll
             for (int j4 = 0; j4 < 4; ++j4) {
@@ -2499,7 +2521,7 @@ uint32_t pow2_at_least(uint32_t x) {
 }
 
 struct ConvGeom {
-  int a_mode, ck, P, Q, K, cr;
+  int a_mode, ck, P, Q, K, cr, gc;
   long long ws;
   int R, S, chunks, Qt;     // halo mode (4): filter extents, 64-channel chunks, output pixels per tile
 };
@@ -2815,7 +2837,7 @@ int make_plan(const abft_gemm_args_t* a, Plan& out, const ConvGeom* cg = nullptr
   p.a_colck = a->scheme == ABFT_GLOBAL ? a->a_colck : nullptr;
   p.acolck_in_smem = (p.a_colck != nullptr && a->K <= 8192) ? 1 : 0;
   // (gathered stems keep their tap -> input-offset table in this region)
-  const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : (gather ? 1024u : 0u);
+  const uint32_t acolck_bytes = p.acolck_in_smem ? (uint32_t)round_up(a->K * 4, 1024) : (gather ? 2048u : 0u);
   const uint32_t ones_bytes = p.acolck_mode == 1 ? 8192u : 0u;
   const uint32_t bar_bytes = 1024;
   const uint32_t ws_bytes = p.wsum != nullptr ? (uint32_t)round_up(p.ws_nb * a->N * 4, 1024) : 0u;
@@ -3137,7 +3159,14 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   // A tiles gathered in shared memory (mode 5); the explicit im2col (mode 3) keeps the same K
   // layout so both run on the same packed weights
   const bool stem4 = mode == 3 && g.cr <= 4 && c->r * c->s <= 64;
-  if (stem4) {
+  // narrow inputs (C < 48, a multiple of 8): gathered too, 16-byte copies of (tap, 8-channel) chunks,
+  // while the weights (all k-blocks, one N block, + 16 checksum rows) fit shared memory beside the
+  // A stages (else the explicit im2col)
+  const int taps_all = c->r * c->s;
+  const long long g8_b = (long long)((taps_all * c->c + 63) / 64) * ((c->gemm.N + 16 + 31) / 32 * 32) * 128;
+  const bool gather8 = mode == 3 && !stem4 && g.cr == c->c && c->c % 8 == 0 && c->c >= 8 && taps_all <= 64 &&
+                       taps_all * c->c <= 2048 && g8_b <= 110LL * 1024;
+  if (stem4 || gather8) {
     const int s = c->gemm.scheme;
     const bool ok = c->gemm.a_colck == nullptr && s != ABFT_REPL_FULL && s != ABFT_REPL_SINGLE &&
                     (s == ABFT_UNPROTECTED || c->gemm.ck_layout == 1 || c->gemm.lhs_rowck != nullptr ||
@@ -3147,10 +3176,11 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   }
   g.a_mode = mode;
   g.ws = 0;
+  g.gc = stem4 ? 4 : (gather8 ? c->c : 0);
   if (stem4) {
     g.ck = 4;
     g.K = (c->r * c->s * 4 + 7) / 8 * 8;
-    if (mode == 3) g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
+    g.ws = (long long)c->n * g.P * g.Q * g.K * 2;          // (the fallback's, as below)
   } else if (mode == 0 || mode == 2) {
     g.ck = c->c;
     g.K = c->r * c->s * c->c;
@@ -3161,6 +3191,9 @@ int conv_geom(const abft_conv_args_t* c, ConvGeom& g) {
   } else {
     g.ck = g.cr;                              // dense (r, s, c_real) columns
     g.K = (c->r * c->s * g.cr + 7) / 8 * 8;
+    // (gathered: no workspace, but the size of the explicit im2col it falls back to for a call the
+    // gather cannot take — e.g. weights plus window-sum buckets past shared memory — is reported so
+    // callers can provide it)
     g.ws = (long long)c->n * g.P * g.Q * g.K * 2;
   }
   return ABFT_OK;
@@ -3452,6 +3485,7 @@ extern "C" __attribute__((visibility("default"))) int abft_conv2d(const abft_con
     // gathered stem: no A tensor map (the checksum warps load the input directly)
     p.cv_x = c->gemm.A;
     p.cv_H = c->h; p.cv_W = c->w; p.cv_taps = c->r * c->s;
+    p.cv_gc = g.gc;
     CUtensorMap ma{};
     return launch_with_a(&ga, pl, ma, stream);
   }
