@@ -50,20 +50,22 @@ struct Unpack2<__nv_bfloat16> {
   }
 };
 
-// out[n][p][q][c] = max over the window (padding never wins), one 8-channel vector per thread
-template <typename T>
+// out[n][p][q][c] = max over the window (padding never wins), one 8-channel vector per thread.
+// I: the index type of the (pixel, vector) decomposition — 32-bit whenever the tensor allows (the
+// 64-bit divisions made the kernel instruction-bound, ~2/3 of HBM bandwidth)
+template <typename T, typename I>
 __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const T* __restrict__ x, int H, int W, int C, long long ldx,
                                                            int P, int Q, int k, int s, int pad, T* __restrict__ out,
                                                            long long ldo, long long total_vec) {
-  const int cv = C / 8;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total_vec;
-       i += (long long)gridDim.x * blockDim.x) {
+  const I cv = (I)(C / 8);
+  const I total = (I)total_vec;
+  for (I i = (I)(blockIdx.x * blockDim.x + threadIdx.x); i < total; i += (I)(gridDim.x * blockDim.x)) {
     const int c8 = (int)(i % cv);
-    long long pix = i / cv;
-    const int q = (int)(pix % Q);
-    pix /= Q;
-    const int p = (int)(pix % P);
-    const long long n = pix / P;
+    I pix = i / cv;
+    const int q = (int)(pix % (I)Q);
+    pix /= (I)Q;
+    const int p = (int)(pix % (I)P);
+    const long long n = (long long)(pix / (I)P);
     uint4 m = make_uint4(Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest, Max2<T>::lowest);
     const int h0 = p * s - pad, w0 = q * s - pad;
     for (int dh = 0; dh < k; ++dh) {
@@ -191,19 +193,27 @@ __global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const T* __restrict__
 // (g = 0) or b[i] (g = 1); stored in the "halves" layout (logical channels [0, C/2) at physical
 // [0, C/2), [C/2, C) at physical [half_pad, half_pad + C/2)) so the next unit's chunk(2) halves
 // are 16-byte aligned channel slices.  One (x1[i], b[i]) pair -> one 4-byte store per thread.
-template <typename T>
+template <typename T, typename I>
 __global__ void __launch_bounds__(256) interleave2_kernel(const T* __restrict__ x1, long long ld1,
                                                           const T* __restrict__ b, long long ld2, int half,
                                                           T* __restrict__ out, long long ldo, int half_pad,
                                                           long long total) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long pix = t / half;
-    const int i = (int)(t - pix * half);
-    const int l = 2 * i;   // even: the pair never straddles the half boundary (half is even)
-    const int phys = l < half ? l : half_pad + (l - half);
-    T pair[2] = {x1[pix * ld1 + i], b[pix * ld2 + i]};
-    *reinterpret_cast<uint32_t*>(out + pix * ldo + phys) = *reinterpret_cast<uint32_t*>(pair);
+  // one thread: channels (2j, 2j+1) of both sources (one 4-byte load each) -> output channels
+  // 4j .. 4j+3 as two 4-byte pairs (a pair never straddles the half boundary: half is even)
+  const I hp = (I)(half / 2);
+  const I tot = (I)(total / 2);
+  for (I t = (I)(blockIdx.x * blockDim.x + threadIdx.x); t < tot; t += (I)(gridDim.x * blockDim.x)) {
+    const I pixi = t / hp;
+    const int j = (int)(t - pixi * hp);
+    const long long pix = (long long)pixi;
+    const uint32_t a2 = *reinterpret_cast<const uint32_t*>(x1 + pix * ld1 + 2 * j);
+    const uint32_t b2 = *reinterpret_cast<const uint32_t*>(b + pix * ld2 + 2 * j);
+    const int l0 = 4 * j, l1 = 4 * j + 2;
+    const int p0 = l0 < half ? l0 : half_pad + (l0 - half);
+    const int p1 = l1 < half ? l1 : half_pad + (l1 - half);
+    T* o = out + pix * ldo;
+    *reinterpret_cast<uint32_t*>(o + p0) = __byte_perm(a2, b2, 0x5410);   // (x1[2j], b[2j])
+    *reinterpret_cast<uint32_t*>(o + p1) = __byte_perm(a2, b2, 0x7632);   // (x1[2j+1], b[2j+1])
   }
 }
 
@@ -253,12 +263,22 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_maxpool(const vo
   if (P < 1 || Q < 1) return fail(ABFT_E_SHAPE, "maxpool: empty output");
   const long long total = (long long)n * P * Q * (c / 8);
   cudaStream_t st = as_stream(stream);
-  if (dtype == ABFT_BF16)
-    maxpool_nhwc_kernel<__nv_bfloat16><<<grid_for(total), 256, 0, st>>>((const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k,
-                                                                         stride, pad, (__nv_bfloat16*)out, ldo, total);
-  else
-    maxpool_nhwc_kernel<__half><<<grid_for(total), 256, 0, st>>>((const __half*)x, h, w, c, ldx, P, Q, k, stride, pad,
-                                                                  (__half*)out, ldo, total);
+  const bool small = total < (1LL << 31) - (long long)grid_for(total) * 256;
+  if (dtype == ABFT_BF16) {
+    if (small)
+      maxpool_nhwc_kernel<__nv_bfloat16, uint32_t><<<grid_for(total), 256, 0, st>>>(
+          (const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k, stride, pad, (__nv_bfloat16*)out, ldo, total);
+    else
+      maxpool_nhwc_kernel<__nv_bfloat16, long long><<<grid_for(total), 256, 0, st>>>(
+          (const __nv_bfloat16*)x, h, w, c, ldx, P, Q, k, stride, pad, (__nv_bfloat16*)out, ldo, total);
+  } else {
+    if (small)
+      maxpool_nhwc_kernel<__half, uint32_t><<<grid_for(total), 256, 0, st>>>((const __half*)x, h, w, c, ldx, P, Q, k,
+                                                                            stride, pad, (__half*)out, ldo, total);
+    else
+      maxpool_nhwc_kernel<__half, long long><<<grid_for(total), 256, 0, st>>>((const __half*)x, h, w, c, ldx, P, Q, k,
+                                                                             stride, pad, (__half*)out, ldo, total);
+  }
   return cuda_check(cudaGetLastError(), "maxpool launch");
 }
 
@@ -324,8 +344,15 @@ extern "C" __attribute__((visibility("default"))) int abft_nhwc_interleave2(cons
   cudaStream_t st = as_stream(stream);
   // 16-bit elements either way: the kernel only moves them
   (void)dtype;
-  interleave2_kernel<__half><<<grid_for(total), 256, 0, st>>>((const __half*)x1, ld1, (const __half*)b, ld2, half,
-                                                               (__half*)out, ldo, half_pad, total);
+  if ((ld1 % 2) || (ld2 % 2) || (ldo % 2) || (reinterpret_cast<uintptr_t>(x1) & 3) ||
+      (reinterpret_cast<uintptr_t>(b) & 3) || (reinterpret_cast<uintptr_t>(out) & 3))
+    return fail(ABFT_E_VALUE, "interleave2: 4-byte aligned rows (even ld1 / ld2 / ldo)");
+  if (total / 2 < (1LL << 31) - (long long)grid_for(total / 2) * 256)
+    interleave2_kernel<__half, uint32_t><<<grid_for(total / 2), 256, 0, st>>>(
+        (const __half*)x1, ld1, (const __half*)b, ld2, half, (__half*)out, ldo, half_pad, total);
+  else
+    interleave2_kernel<__half, long long><<<grid_for(total / 2), 256, 0, st>>>(
+        (const __half*)x1, ld1, (const __half*)b, ld2, half, (__half*)out, ldo, half_pad, total);
   return cuda_check(cudaGetLastError(), "interleave2 launch");
 }
 
