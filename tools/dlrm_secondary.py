@@ -68,12 +68,17 @@ def run(dev_profile, steps: int = 20, warmup: int = 3, profile_iters: int = 100)
     # chain, timed alone (CUDA graph), shared among the depth's layers by their FLOPs.  Every
     # layer of a depth then sees the same relative costs and the reference select (cost.py:174-238)
     # picks one scheme per depth (a per-layer split would add launches, each ~5 us).
-    depth_us = {}
+    # (all depth x scheme launches captured first, then timed in interleaved rounds)
+    depth_keys, depth_graphs, keep = [], [], []
     for sch in (S.UNPROTECTED, S.GLOBAL_ABFT, S.THREAD_ONE_SIDED):
         g = ChainGroup([(wt[k[0]], k[1], [sch] * 3) for k in keys], grouped=True)
+        keep.append(g)
         for d, (arr, n, table, _raw, _keep) in enumerate(g._groups):
-            depth_us[(d, sch)] = profiler.graph_time_us(lambda: kernels.gemm_group_launch(arr, n, table),
-                                                         profile_iters)
+            depth_keys.append((d, sch))
+            depth_graphs.append(profiler.capture_graph(
+                lambda arr=arr, n=n, table=table: kernels.gemm_group_launch(arr, n, table), profile_iters))
+    depth_us = dict(zip(depth_keys, profiler.interleaved_min_us(depth_graphs, profile_iters)))
+    del depth_graphs, keep
     depth_flops = [sum(2 * k[1] * mlps[k[0]][d].shape[0] * mlps[k[0]][d].shape[1] for k in keys) for d in range(3)]
     plans = {}
     for k in keys:
