@@ -705,6 +705,7 @@ class GraphedNetwork:
             for _ in range(warmup):
                 net.forward(verify=verify)
         t.cuda.current_stream().wait_stream(s)
+        net.fused_batch()          # (its device table is written synchronously: never during capture)
         t.cuda.synchronize()
         self.graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.graph, stream=s):
