@@ -17,8 +17,9 @@ and glue op, one verification launch).  Reported:
                  median; per-config medians over C1..C5 (C2: DLRM, C3: ResNet-50 b256, C4:
                  VGG-16 b256, C1: one 256^3 layer)
   vendor         the same BN-folded networks through torch/cuDNN fp16 channels_last
-  e2e            the step through the host API: pinned NCHW inputs H2D (on a copy stream,
-                 overlapping the earlier networks' forwards), the graphs, logits + flag counters D2H
+  e2e            the step through the host API: pinned NCHW inputs H2D (on a copy stream, step
+                 k+1's inputs overlapping step k's forwards), the graphs, logits + flag counters
+                 D2H; K steps back to back in one timed region
   roofline       the step's dominant kernel against MEASURED_PEAKS.json
   cpu_baseline   the reference algorithm (oracle port: im2col + fp32 GEMM + global check per
                  linear layer) on a bounded sample, host cores
@@ -349,38 +350,50 @@ def main():
     d2h = sum(h.numel() * h.element_size() for h in host_out) + sum(c.numel() * 4 for c in host_cnt)
 
     copy_stream = torch.cuda.Stream()
-    in_ready = [torch.cuda.Event() for _ in suite]
+    # two device input sets: step k+1's inputs cross PCIe (copy stream) while step k computes —
+    # the serving pattern; every step's H2D and D2H stay inside the timed region, which spans all
+    # K steps (inputs of 308 MB per step exceed the 126 MB L2, so no flush between steps)
+    dev_sets = [dev_in, [torch.empty_like(e["x"]) for e in suite]]
+    ready = [[torch.cuda.Event() for _ in suite] for _ in range(2)]
+    freed = [[torch.cuda.Event() for _ in suite] for _ in range(2)]
 
-    def e2e_step():
-        flush.fill_(1.0)
+    def e2e_run(k_steps):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         main = torch.cuda.current_stream()
         e0.record()
-        # every network's input crosses PCIe on a copy stream while the earlier networks compute;
-        # each forward waits only for its own input (the copies stay inside the timed region)
+
+        def copy_in(k):
+            b = k % 2
+            with torch.cuda.stream(copy_stream):
+                for i in range(len(suite)):
+                    if k >= 2:
+                        copy_stream.wait_event(freed[b][i])     # step k-2 has read this buffer
+                    dev_sets[b][i].copy_(host_in[i], non_blocking=True)
+                    ready[b][i].record()
         copy_stream.wait_stream(main)
-        with torch.cuda.stream(copy_stream):
-            for i in range(len(suite)):
-                dev_in[i].copy_(host_in[i], non_blocking=True)
-                in_ready[i].record()
-        for i, e in enumerate(suite):
-            main.wait_event(in_ready[i])
-            e["net"].load_input(dev_in[i])
-            e["graphs"]["ig"].replay()
-        if world > 1:
-            PN.verify_sharded_many(nets)
-        for i, e in enumerate(suite):
-            host_out[i].copy_(e["net"].logits(), non_blocking=True)
-            host_cnt[i].copy_(e["net"].counters, non_blocking=True)
+        copy_in(0)
+        for k in range(k_steps):
+            b = k % 2
+            if k + 1 < k_steps:
+                copy_in(k + 1)
+            for i, e in enumerate(suite):
+                main.wait_event(ready[b][i])
+                e["net"].load_input(dev_sets[b][i])
+                freed[b][i].record(main)
+                e["graphs"]["ig"].replay()
+            if world > 1:
+                PN.verify_sharded_many(nets)
+            for i, e in enumerate(suite):
+                host_out[i].copy_(e["net"].logits(), non_blocking=True)
+                host_cnt[i].copy_(e["net"].counters, non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
-    for _ in range(args.warmup):
-        e2e_step()
-    e2e_t = torch.tensor([statistics.mean([e2e_step() for _ in range(args.steps)])], device="cuda")
+        return e0.elapsed_time(e1) / k_steps
+    e2e_run(max(1, args.warmup))
+    e2e_t = torch.tensor([e2e_run(args.steps)], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
     e2e_ms = float(e2e_t.item())
